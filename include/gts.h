@@ -1,0 +1,154 @@
+/*
+ * gts.h -- C ABI of the B200-native GTS batch similarity-search engine.
+ *
+ * This is the drop-in boundary under the reference's Python index API
+ * (arXiv 2404.00966 reference package `metrictree`).  Each entry point
+ * names the reference interface it replaces (file:line under
+ * /root/reference/pkg/src/metrictree/).  Plain pointers and sizes only --
+ * no torch or C++ types cross this boundary, no C++ exception escapes it.
+ *
+ * Status codes (the Python shim maps them to the reference's exception
+ * types, search.py:231-234, 246-268, data.py:220-229):
+ *   GTS_OK        0
+ *   GTS_EINVAL    1  invalid argument            -> ValueError
+ *   GTS_EBUDGET   2  memory-unit budget          -> BudgetError
+ *   GTS_EMETRIC   3  payload / metric mismatch   -> MetricMismatchError
+ *   GTS_ECUDA     4  CUDA runtime error          -> RuntimeError
+ *   GTS_EOOM      5  device allocation failed    -> MemoryError
+ * gts_last_error() returns a thread-local message for the last failure.
+ *
+ * Ownership: the caller owns every input and output buffer; an index
+ * handle owns its device tables; a result handle owns its device CSR until
+ * gts_result_free.  Query calls on one index are reentrant (each call
+ * allocates its workspace stream-ordered on the stream it is given);
+ * tombstone updates must not overlap queries on the same index
+ * (single writer).
+ */
+#ifndef GTS_H
+#define GTS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GTS_OK 0
+#define GTS_EINVAL 1
+#define GTS_EBUDGET 2
+#define GTS_EMETRIC 3
+#define GTS_ECUDA 4
+#define GTS_EOOM 5
+
+/* metric codes = the reference snapshot codes (io.py:30-35) */
+#define GTS_EDIT 0
+#define GTS_L1 1
+#define GTS_L2 2
+#define GTS_ANGULAR 3
+
+/* A payload collection in dataset-row order (reference data.py:59-126:
+ * _VectorStore float64 matrix / _StringStore int32 code points + offsets). */
+typedef struct {
+    int32_t metric;
+    int64_t n;
+    int64_t dim;               /* vectors: D; strings: 0 */
+    const double *vectors;     /* [n*dim] row-major float64, host */
+    const int32_t *codes;      /* strings: UTF-32 code points, host */
+    const int64_t *offsets;    /* strings: [n+1], host */
+    const int64_t *ids;        /* [n] strictly increasing object ids */
+} gts_dataset;
+
+/* FlatPivotTree arrays (reference tree.py:155-175).  Node arrays have
+ * nodes+1 slots (slot 0 unused); table arrays have n slots. */
+typedef struct {
+    int64_t nc, levels, split_rounds, nodes, n;
+    int64_t *pivot_id, *pivot_row, *pos, *size;
+    double *min_dis, *max_dis;
+    int64_t *rows;
+    double *dis;
+    uint8_t *tombstone;
+} gts_tree;
+
+/* tree_height (tree.py:60-78) */
+int gts_tree_height(int64_t n, int64_t nc, int64_t *max_h, int64_t *split_rounds);
+/* node_count_for (tree.py:106-108) */
+int64_t gts_node_count(int64_t levels, int64_t nc);
+
+/* build (tree.py:370-385, _Builder 241-367) into caller-allocated arrays.
+ * root_row is the reference's seeded draw rng.integers(0, n)
+ * (tree.py:263, 288-291), made by the caller.  nthreads <= 0: all cores. */
+int gts_build_tree(const gts_dataset *ds, int64_t root_row, int nthreads, gts_tree *tree);
+
+/* Device index: uploads the flattened list tables (node table, pivot ids
+ * and ranges, object table with pivot distances, payloads in table order).
+ * Replaces the state BatchSearcher.__init__ binds (search.py:225-234). */
+typedef struct gts_index gts_index;
+int gts_index_create(const gts_dataset *ds, const gts_tree *tree, int device, gts_index **out);
+int gts_index_destroy(gts_index *ix);
+/* tombstone marks in table order (tree.tombstone, updates.py:124-135) */
+int gts_index_set_tombstones(gts_index *ix, const uint8_t *tombstone, void *stream);
+
+/* A query batch (the prepared payloads of search.py:280 / data.py:220-229).
+ * Host buffers; gts_queries_upload makes a device-resident copy. */
+typedef struct {
+    int32_t metric;
+    int64_t nq;
+    int64_t dim;
+    const double *vectors;    /* [nq*dim] float64 */
+    const int32_t *codes;     /* strings: code points */
+    const int64_t *offsets;   /* strings: [nq+1] */
+} gts_query_batch;
+
+typedef struct gts_queries gts_queries;   /* device-resident prepared batch */
+int gts_queries_upload(gts_index *ix, const gts_query_batch *qb, void *stream, gts_queries **out);
+int gts_queries_free(gts_queries *q);
+
+typedef struct gts_result gts_result;     /* device CSR + stats */
+
+/* BatchSearcher.range_batch (search.py:238-248): radii[nq] >= 0.
+ * memory_units: row budget (search.py:229, runtime.py:18); 0 = default.
+ * Answers per query are every live object with d <= r, sorted by
+ * (distance, id) (search.py:298-314). */
+int gts_range_batch(gts_index *ix, const gts_queries *q, const double *radii,
+                    int64_t memory_units, int pruning, void *stream, gts_result **out);
+/* BatchSearcher.knn_batch (search.py:250-260): ks[nq] >= 1.  Answers are
+ * the k smallest (distance, id) pairs over live objects (oracle.py:30-36). */
+int gts_knn_batch(gts_index *ix, const gts_queries *q, const int64_t *ks,
+                  int64_t memory_units, int pruning, void *stream, gts_result **out);
+/* One-call host path: upload + search + download (the e2e boundary). */
+int gts_range_batch_host(gts_index *ix, const gts_query_batch *qb, const double *radii,
+                         int64_t memory_units, int pruning, void *stream, gts_result **out);
+int gts_knn_batch_host(gts_index *ix, const gts_query_batch *qb, const int64_t *ks,
+                       int64_t memory_units, int pruning, void *stream, gts_result **out);
+
+/* Result access: sizes, then a copy into caller buffers (host or device,
+ * decided by the pointer).  offsets[nq+1], ids[total], dis[total],
+ * verified[nq], pruned[nq] (SearchStats, search.py:98-113); any may be NULL.
+ * size_limits[64]: per split layer, 0 = layer not visited. */
+int gts_result_info(const gts_result *r, int64_t *nq, int64_t *total, int64_t *peak_units,
+                    int64_t *size_limits64);
+int gts_result_copy(const gts_result *r, int64_t *offsets, int64_t *ids, double *dis,
+                    int64_t *verified, int64_t *pruned, void *stream);
+/* Device pointers of the result CSR (valid until gts_result_free). */
+int gts_result_device(const gts_result *r, const int64_t **offsets, const int64_t **ids,
+                      const double **dis);
+int gts_result_free(gts_result *r);
+
+/* Exact single-pair and row-pair distances on the device (metrics.py:196-223
+ * and data.py:245-263 row_to_row), float64 result, for tests and the cache
+ * scan of StreamingIndex (updates.py:206-215). */
+int gts_pair_distances(int32_t metric, int64_t npairs, int64_t dim,
+                       const double *a_vec, const double *b_vec,
+                       const int32_t *a_codes, const int64_t *a_off,
+                       const int32_t *b_codes, const int64_t *b_off,
+                       double *out, void *stream);
+
+/* Count of this library's kernel launches since load (bench evidence). */
+int64_t gts_launch_count(void);
+const char *gts_last_error(void);
+const char *gts_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GTS_H */

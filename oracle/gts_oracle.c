@@ -18,7 +18,7 @@
  *                            root table, process/expand/merge/verify/collect)
  *   - MemoryBudget ......... runtime.py:56-88
  *   - brute force .......... oracle.py:19-47
- * Pinned against tests/golden/*.npz, produced by running the reference
+ * Pinned against the tests/golden npz fixtures, produced by running the reference
  * itself (tests/golden/make_golden.py).
  *
  * Compile with -ffp-contract=off: numpy never fuses x*x+acc into an FMA.

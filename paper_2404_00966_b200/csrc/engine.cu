@@ -1,0 +1,1393 @@
+// engine.cu -- device index, batch range / kNN search driver and the C ABI.
+//
+// Pipeline per batch (reference BatchSearcher, search.py:273-296):
+//   root table   k_root       d(q, root pivot)                (search.py:316-334)
+//   per layer    k_expand     Eq.1 children, parent-range pre-screen,
+//                             child pivot distance, own-range post-screen,
+//                             block-aggregated compaction     (search.py:405-477)
+//   leaves       k_verify     lemma-1 entry filter, exact distance, hits
+//                                                              (search.py:507-538)
+//   collect      3 stable CUB radix sorts -> (q, d, id) CSR   (search.py:298-314)
+// The host driver walks layers depth-first in chunks of level_size_limit
+// parent rows, so no child table exceeds memory_units rows
+// (search.py:359-403, runtime.py:56-88).
+// kNN = k_probe (radius estimate from the query's nearest sibling leaves)
+// + the same range pipeline with that radius (tie-inclusive) + per-query
+// truncation to the k smallest (distance, id) (oracle.py:30-36).
+#include <algorithm>
+#include <atomic>
+#include <cfloat>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+
+#include "../../include/gts.h"
+#include "common.h"
+#include "kernels.cuh"
+
+namespace gts {
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+static thread_local char g_err[2048] = "";
+
+int set_error(int code, const char *fmt, ...)
+{
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+struct Error {
+    int code;
+};
+
+[[noreturn]] static void fail(int code, const char *fmt, ...)
+{
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    throw Error{code};
+}
+
+#define CK(x)                                                                                   \
+    do {                                                                                        \
+        cudaError_t e_ = (x);                                                                   \
+        if (e_ != cudaSuccess)                                                                  \
+            fail(e_ == cudaErrorMemoryAllocation ? GTS_EOOM : GTS_ECUDA, "%s: %s (%s:%d)", #x, \
+                 cudaGetErrorString(e_), __FILE__, __LINE__);                                   \
+    } while (0)
+
+static std::atomic<int64_t> g_launches{0};
+
+#define LAUNCH_CHECK() \
+    do {               \
+        g_launches++;  \
+        CK(cudaGetLastError()); \
+    } while (0)
+
+// stream-ordered device buffer
+template <class T>
+struct DBuf {
+    T *p = nullptr;
+    size_t n = 0;
+    cudaStream_t s = 0;
+    DBuf() = default;
+    DBuf(size_t cnt, cudaStream_t st) { alloc(cnt, st); }
+    DBuf(const DBuf &) = delete;
+    DBuf &operator=(const DBuf &) = delete;
+    DBuf(DBuf &&o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+    DBuf &operator=(DBuf &&o) noexcept
+    {
+        if (this != &o) { release(); p = o.p; n = o.n; s = o.s; o.p = nullptr; o.n = 0; }
+        return *this;
+    }
+    void alloc(size_t cnt, cudaStream_t st)
+    {
+        release();
+        s = st;
+        if (cnt) CK(cudaMallocAsync((void **)&p, cnt * sizeof(T), st));
+        n = cnt;
+    }
+    void release()
+    {
+        if (p) cudaFreeAsync(p, s);
+        p = nullptr;
+        n = 0;
+    }
+    ~DBuf() { release(); }
+};
+
+template <class T>
+static void h2d(T *dst, const T *src, size_t cnt, cudaStream_t s)
+{
+    if (cnt) CK(cudaMemcpyAsync(dst, src, cnt * sizeof(T), cudaMemcpyHostToDevice, s));
+}
+
+static inline unsigned grid_for(int64_t threads, int block, unsigned cap = 1u << 30)
+{
+    int64_t g = (threads + block - 1) / block;
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return (unsigned)g;
+}
+
+// ---------------------------------------------------------------------------
+// kernels
+// ---------------------------------------------------------------------------
+
+// Root table: d(q, root pivot) for every query (search.py:316-334).
+template <int MET>
+__global__ void k_root(IndexView ix, QueryView qv, int nq, Row *out)
+{
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    const int piv = ix.node[1].piv;
+    out[q] = Row{q, 1, dist32<MET>(ix, qv, q, piv), 0};
+}
+
+// Block-aggregated compaction: returns this thread's output slot (or -1).
+__device__ __forceinline__ long long block_append(bool keep, unsigned long long *counter, int *sh_warp,
+                                                  unsigned long long *sh_base)
+{
+    const int lane = lane_id(), warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    unsigned b = __ballot_sync(kFull, keep);
+    if (lane == 0) sh_warp[warp] = __popc(b);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int tot = 0;
+        for (int w = 0; w < nwarps; w++) { int c = sh_warp[w]; sh_warp[w] = tot; tot += c; }
+        *sh_base = tot ? atomicAdd(counter, (unsigned long long)tot) : 0ull;
+    }
+    __syncthreads();
+    long long slot = -1;
+    if (keep) slot = (long long)(*sh_base) + sh_warp[warp] + __popc(b & ((1u << lane) - 1u));
+    __syncthreads();
+    return slot;
+}
+
+// Warp-aggregated per-query counter add (all 32 lanes call; val 0 = no-op).
+__device__ __forceinline__ void warp_add_q(unsigned long long *arr, int q, unsigned val)
+{
+    unsigned peers = __match_any_sync(kFull, q);
+    unsigned s = __reduce_add_sync(peers, val);
+    if (s && lane_id() == __ffs(peers) - 1) atomicAdd(arr + q, (unsigned long long)s);
+}
+
+// One level of the descent (search.py:405-477).  Thread per (row, child).
+template <int MET>
+__global__ void __launch_bounds__(256) k_expand(IndexView ix, QueryView qv, const Row *__restrict__ in,
+                                                int64_t m, int own, int pruning, const float *__restrict__ r32,
+                                                Row *out, unsigned long long *counter,
+                                                unsigned long long *pruned_stat)
+{
+    __shared__ int sh_warp[32];
+    __shared__ unsigned long long sh_base;
+    const int nc = ix.nc;
+    const int64_t total = m * nc;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < total; base += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = base + threadIdx.x;
+        bool valid = i < total;
+        bool keep = false, nonempty = false;
+        int q = -1, child = 0;
+        float cd = 0.f;
+        if (valid) {
+            const int64_t row = i / nc;
+            const int j = (int)(i - row * nc);
+            const Row pr = in[row];
+            q = pr.q;
+            child = (pr.node - 1) * nc + 2 + j;
+            const NodeRec c = ix.node[child];
+            nonempty = c.size > 0;
+            keep = nonempty;
+            const float r = r32[q];
+            if (keep && !own && pruning) {
+                // internal children carry ranges to the parent pivot:
+                // keep iff dq + r >= min and dq - r <= max (search.py:425-433)
+                const float e = slack(ix, pr.dqp, r);
+                keep = (pr.dqp + r + e >= c.mn) && (pr.dqp - r - e <= c.mx);
+            }
+            if (keep) {
+                cd = dist32<MET>(ix, qv, q, c.piv);
+                if (own && pruning) {
+                    // leaves carry ranges to their own pivot (search.py:467-471)
+                    const float e = slack(ix, cd, r);
+                    keep = (cd + r + e >= c.mn) && (cd - r - e <= c.mx);
+                }
+            }
+        }
+        warp_add_q(pruned_stat, valid ? q : -1, (valid && nonempty && !keep) ? 1u : 0u);
+        long long slot = block_append(keep, counter, sh_warp, &sh_base);
+        if (keep) out[slot] = Row{q, child, cd, 0};
+    }
+}
+
+// Leaf verification (search.py:507-538), one warp per leaf row; emits
+// (query, entry, exact float64 distance) for every live entry with d <= r.
+template <int MET>
+__global__ void __launch_bounds__(256) k_verify(IndexView ix, QueryView qv, const Row *__restrict__ rows,
+                                                int64_t m, int pruning, const float *__restrict__ r32,
+                                                const double *__restrict__ r64, HitBuf out,
+                                                unsigned long long *verified_stat, int stats_on)
+{
+    const int lane = lane_id();
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < m; w += warps) {
+        const Row lr = rows[w];
+        const int q = lr.q;
+        const NodeRec leaf = ix.node[lr.node];
+        const int pos = ix.npos[lr.node];
+        const float r = r32[q];
+        const double rr = r64[q];
+        unsigned ver = 0;
+        for (int b = 0; b < leaf.size; b += kWarp) {
+            const int k = b + lane;
+            bool pass = false;
+            int e = pos + k;
+            if (k < leaf.size && is_alive(ix.alive, e)) {
+                if (!pruning) pass = true;
+                else {
+                    const float de = __ldg(ix.dis + e);
+                    pass = fabsf(de - lr.dqp) <= r + slack(ix, de, lr.dqp) + ix.rel * r;
+                }
+            }
+            ver += __popc(__ballot_sync(kFull, pass));
+            bool hit = false;
+            double d64 = 0.0;
+            if (pass) {
+                const float d = dist32<MET>(ix, qv, q, e);
+                if (MET == kMetricEdit) {
+                    hit = d <= r;
+                    d64 = (double)d;
+                } else if (d - slack(ix, d, 0.f) <= r) {
+                    d64 = vdist64<MET>(ix, qv, q, e);
+                    hit = d64 <= rr;
+                }
+            }
+            unsigned hb = __ballot_sync(kFull, hit);
+            if (hb) {
+                unsigned long long base = 0;
+                if (lane == 0) base = atomicAdd(out.counter, (unsigned long long)__popc(hb));
+                base = __shfl_sync(kFull, base, 0);
+                if (hit) {
+                    unsigned long long slot = base + __popc(hb & ((1u << lane) - 1u));
+                    if (slot < out.cap) { out.q[slot] = q; out.e[slot] = e; out.d[slot] = d64; }
+                }
+            }
+        }
+        if (stats_on && lane == 0 && ver) atomicAdd(verified_stat + q, (unsigned long long)ver);
+    }
+}
+
+// Rows (q, leaf) for every live leaf when pruning is disabled (search.py:338-355).
+__global__ void k_all_leaves(const int32_t *leaves, int nleaves, int q0, int nqc, Row *out)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (int64_t)nleaves * nqc) return;
+    int q = q0 + (int)(i / nleaves);
+    int l = (int)(i % nleaves);
+    out[i] = Row{q, leaves[l], 0.f, 0};
+}
+
+// k-th smallest (1-based) of n non-negative float bit patterns in smem.
+__device__ uint32_t block_kth(const uint32_t *vals, int n, int k, unsigned *hist, int *sh)
+{
+    uint32_t prefix = 0, mask = 0;
+    int kk = k;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+        __syncthreads();
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            uint32_t v = vals[i];
+            if ((v & mask) == prefix) atomicAdd(&hist[(v >> shift) & 255u], 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int c = 0, bsel = 255, rem = kk;
+            for (int b = 0; b < 256; b++) {
+                if (c + (int)hist[b] >= kk) { bsel = b; rem = kk - c; break; }
+                c += hist[b];
+            }
+            sh[0] = bsel;
+            sh[1] = rem;
+        }
+        __syncthreads();
+        prefix |= (uint32_t)sh[0] << shift;
+        mask |= 255u << shift;
+        kk = sh[1];
+        __syncthreads();
+    }
+    return prefix;
+}
+
+constexpr int kProbeCand = 4096;
+
+// kNN radius estimate: greedy descent to the parent of the query's nearest
+// leaves, exact distances to every live entry of its leaf children, radius
+// = k-th smallest (an upper bound on the true k-th distance), else +inf.
+template <int MET>
+__global__ void __launch_bounds__(256) k_probe(IndexView ix, QueryView qv, int nq, const int32_t *ks,
+                                               float *r32, double *r64)
+{
+    __shared__ uint32_t cand[kProbeCand];
+    __shared__ unsigned hist[256];
+    __shared__ int sh[4];
+    __shared__ float best_d[32];
+    __shared__ int best_j[32];
+    for (int q = blockIdx.x; q < nq; q += gridDim.x) {
+        const int nc = ix.nc;
+        int node = 1;
+        // descend levels-2 times (to the parent of the leaf level)
+        for (int lvl = 1; lvl + 1 < ix.levels; lvl++) {
+            float d = FLT_MAX;
+            int j = threadIdx.x;
+            if (j < nc) {
+                const NodeRec c = ix.node[(node - 1) * nc + 2 + j];
+                if (c.size > 0) d = dist32<MET>(ix, qv, q, c.piv);
+            }
+            // block argmin over the first nc threads (ties: smallest child)
+            float bd = d;
+            int bj = j;
+            for (int o = 16; o > 0; o >>= 1) {
+                float od = __shfl_down_sync(kFull, bd, o);
+                int oj = __shfl_down_sync(kFull, bj, o);
+                if (od < bd || (od == bd && oj < bj)) { bd = od; bj = oj; }
+            }
+            if (lane_id() == 0) { best_d[threadIdx.x >> 5] = bd; best_j[threadIdx.x >> 5] = bj; }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                float xd = best_d[0];
+                int xj = best_j[0];
+                for (int w = 1; w < (int)(blockDim.x >> 5); w++)
+                    if (best_d[w] < xd || (best_d[w] == xd && best_j[w] < xj)) { xd = best_d[w]; xj = best_j[w]; }
+                sh[2] = xj;
+            }
+            __syncthreads();
+            node = (node - 1) * nc + 2 + sh[2];
+            __syncthreads();
+        }
+        // candidate leaves: the root itself (one-level tree) or node's children
+        if (threadIdx.x == 0) sh[3] = 0;
+        __syncthreads();
+        const int first = ix.levels == 1 ? 1 : (node - 1) * nc + 2;
+        const int nleaf = ix.levels == 1 ? 1 : nc;
+        for (int l = 0; l < nleaf; l++) {
+            const NodeRec lf = ix.node[first + l];
+            const int pos = ix.npos[first + l];
+            for (int k = threadIdx.x; k < lf.size; k += blockDim.x) {
+                const int e = pos + k;
+                if (!is_alive(ix.alive, e)) continue;
+                int slot = atomicAdd(&sh[3], 1);
+                if (slot < kProbeCand) cand[slot] = __float_as_uint(dist32<MET>(ix, qv, q, e));
+            }
+        }
+        __syncthreads();
+        const int n = min(sh[3], kProbeCand);
+        const int k = ks[q];
+        __syncthreads();
+        if (n >= k && k >= 1) {
+            uint32_t kth = block_kth(cand, n, k, hist, sh);
+            if (threadIdx.x == 0) {
+                float t = __uint_as_float(kth);
+                if (MET == kMetricEdit) {
+                    r32[q] = t;
+                    r64[q] = (double)t;
+                } else {
+                    // every one of the k objects has d64 <= d32 + slack
+                    float up = t + slack(ix, t, 0.f);
+                    r32[q] = up;
+                    r64[q] = (double)up;
+                }
+            }
+        } else if (threadIdx.x == 0) {
+            r32[q] = INFINITY;
+            r64[q] = INFINITY;
+        }
+        __syncthreads();
+    }
+}
+
+// query preparation --------------------------------------------------------
+
+__global__ void k_map_symbols(const int32_t *codes, int64_t n, const int32_t *alpha, int A, uint8_t *out)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int32_t c = codes[i];
+    int lo = 0, hi = A;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (alpha[mid] < c) lo = mid + 1; else hi = mid;
+    }
+    out[i] = (lo < A && alpha[lo] == c) ? (uint8_t)lo : kNoSym;
+}
+
+// one thread per (query, symbol position): sets the Myers match bit
+__global__ void k_build_peq(const uint8_t *sym, const int64_t *soff, const int64_t *peq_off, int nq,
+                            int64_t nsym, uint32_t *peq)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nsym) return;
+    // find the query owning symbol i (binary search over soff)
+    int lo = 0, hi = nq;
+    while (hi - lo > 1) {
+        int mid = (lo + hi) >> 1;
+        if (soff[mid] <= i) lo = mid; else hi = mid;
+    }
+    const int q = lo;
+    const int pos = (int)(i - soff[q]);
+    const int m = (int)(soff[q + 1] - soff[q]);
+    const int W = (m + 31) >> 5;
+    const uint8_t c = sym[i];
+    if (c == kNoSym) return;
+    atomicOr(peq + peq_off[q] + (int64_t)c * W + (pos >> 5), 1u << (pos & 31));
+}
+
+__global__ void k_vec_prep(const double *v64, int64_t nq, int D, int Dp, float *v32, unsigned *maxabs_bits,
+                           int *inexact)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nq * Dp) return;
+    int64_t r = i / Dp;
+    int d = (int)(i - r * Dp);
+    float f = 0.f;
+    if (d < D) {
+        double x = v64[r * D + d];
+        f = (float)x;
+        if ((double)f != x) atomicOr(inexact, 1);
+        atomicMax(maxabs_bits, __float_as_uint(fabsf(f)));
+    }
+    v32[i] = f;
+}
+
+// collect -------------------------------------------------------------------
+
+__global__ void k_gather_id(const int32_t *e, int64_t n, const int64_t *ids, unsigned long long *key, int32_t *perm)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    key[i] = (unsigned long long)ids[e[i]];
+    perm[i] = (int32_t)i;
+}
+
+__global__ void k_gather_d(const double *d, const int32_t *perm, int64_t n, unsigned long long *key)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    key[i] = (unsigned long long)__double_as_longlong(d[perm[i]]);
+}
+
+__global__ void k_gather_q(const int32_t *q, const int32_t *perm, int64_t n, uint32_t *key)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    key[i] = (uint32_t)q[perm[i]];
+}
+
+__global__ void k_count(const int32_t *q, int64_t n, long long *counts)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    atomicAdd((unsigned long long *)(counts + q[i]), 1ull);
+}
+
+__global__ void k_clamp_counts(const long long *counts, const int32_t *ks, int nq, long long *out)
+{
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    long long c = counts[q];
+    out[q] = ks ? min(c, (long long)ks[q]) : c;
+}
+
+// Final scatter: sorted hit i of query q at rank r within its segment goes
+// to out_off[q] + r when r < out count (kNN truncation keeps the k first).
+__global__ void k_emit(const int32_t *perm, const int32_t *hq, const int32_t *he, const double *hd,
+                       const long long *in_off, const long long *out_off, const long long *out_cnt,
+                       const int64_t *ids, int64_t n, int64_t *out_ids, double *out_dis)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int32_t h = perm[i];
+    const int q = hq[h];
+    const long long r = i - in_off[q];
+    if (r < out_cnt[q]) {
+        out_ids[out_off[q] + r] = ids[he[h]];
+        out_dis[out_off[q] + r] = hd[h];
+    }
+}
+
+__global__ void k_pair_vec(int metric, int64_t np, int D, const double *a, const double *b, double *out)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= np) return;
+    double s = metric == kMetricL1 ? pw_sum64<kMetricL1>(nullptr, a + i * D, b + i * D, 0, D)
+                                   : pw_sum64<kMetricL2>(nullptr, a + i * D, b + i * D, 0, D);
+    out[i] = metric == kMetricL1 ? s : __dsqrt_rn(s);
+}
+
+// pairs (a_i, b_i): a is the pattern (query side), b the text
+__global__ void k_pair_edit(int64_t np, const uint8_t *bsym, const int64_t *boff, QueryView qa, double *out)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= np) return;
+    const int64_t o = boff[i];
+    out[i] = (double)edit_qt(qa, (int)i, bsym + o, (int)(boff[i + 1] - o));
+}
+
+}  // namespace gts
+
+// ===========================================================================
+// host side
+// ===========================================================================
+using namespace gts;
+
+struct gts_index {
+    int device = 0;
+    int metric = 0;
+    int64_t n = 0, nodes = 0;
+    int nc = 0, levels = 0, split_rounds = 0;
+    int D = 0, Dp = 0;
+    int A = 0;
+    int max_len = 0;
+    bool data_exact = true;
+    float data_maxabs = 0.f;
+    DBuf<NodeRec> node;
+    DBuf<int32_t> npos;
+    DBuf<float> dis;
+    DBuf<int64_t> ids;
+    DBuf<uint32_t> alive;
+    DBuf<float> vec32;
+    DBuf<double> vec64;
+    DBuf<uint8_t> str;
+    DBuf<int64_t> soff;
+    DBuf<int32_t> alpha;
+    DBuf<int32_t> live_leaves;
+    int n_live_leaves = 0;
+    std::vector<int32_t> h_alpha;
+};
+
+struct gts_queries {
+    int metric = 0;
+    int64_t nq = 0;
+    int D = 0, Dp = 0;
+    bool exact = true;
+    float maxabs = 0.f;
+    cudaStream_t stream = 0;
+    DBuf<float> vec32;
+    DBuf<double> vec64;
+    DBuf<uint8_t> str;
+    DBuf<int64_t> soff;
+    DBuf<uint32_t> peq;
+    DBuf<int64_t> peq_off;
+};
+
+struct gts_result {
+    int64_t nq = 0, total = 0, peak = 0;
+    int64_t limits[64] = {0};
+    cudaStream_t stream = 0;
+    DBuf<int64_t> offsets;
+    DBuf<int64_t> ids;
+    DBuf<double> dis;
+    DBuf<unsigned long long> verified, pruned;
+};
+
+namespace {
+
+IndexView make_view(const gts_index *ix, const gts_queries *q)
+{
+    IndexView v{};
+    v.node = ix->node.p;
+    v.npos = ix->npos.p;
+    v.dis = ix->dis.p;
+    v.alive = ix->alive.p;
+    v.vec32 = ix->vec32.p;
+    v.vec64 = ix->vec64.p;
+    v.str = ix->str.p;
+    v.soff = ix->soff.p;
+    v.D = ix->D;
+    v.Dp = ix->Dp;
+    v.nc = ix->nc;
+    v.levels = ix->levels;
+    if (ix->metric == GTS_EDIT) {
+        v.rel = 0.f;
+        v.abs_eps = 0.f;
+    } else {
+        // fp32 screening error model: relative (D+8)*2^-23 covers sequential
+        // fp32 accumulation of D terms with margin; inputs that are not
+        // exactly representable add an absolute 2*D*2^-24*(max|x|+max|q|).
+        v.rel = (float)(ix->D + 8) * ldexpf(1.f, -23);
+        v.abs_eps = 0.f;
+        if (!ix->data_exact || (q && !q->exact))
+            v.abs_eps = 2.f * (float)ix->D * ldexpf(1.f, -24) * (ix->data_maxabs + (q ? q->maxabs : 0.f)) * 2.f;
+    }
+    return v;
+}
+
+QueryView make_qview(const gts_index *ix, const gts_queries *q)
+{
+    QueryView v{};
+    v.vec32 = q->vec32.p;
+    v.vec64 = q->vec64.p;
+    v.soff = q->soff.p;
+    v.str = q->str.p;
+    v.peq = q->peq.p;
+    v.peq_off = q->peq_off.p;
+    v.A = ix->A;
+    return v;
+}
+
+int64_t level_size_limit(int64_t cap, int64_t nc, int64_t split, int64_t layer)
+{
+    int64_t share = cap / ((split - layer + 1) * nc);
+    return share > 1 ? share : 1;
+}
+
+float round_up_f32(double r)
+{
+    if (std::isinf(r)) return INFINITY;
+    float f = (float)r;
+    if ((double)f < r) f = std::nextafter(f, INFINITY);
+    return f;
+}
+
+// Per-thread pinned words for the few device->host counter reads.
+unsigned long long *pinned_counters()
+{
+    static thread_local unsigned long long *p = nullptr;
+    if (!p) CK(cudaMallocHost((void **)&p, 4 * sizeof(unsigned long long)));
+    return p;
+}
+
+// The per-call search driver.
+struct Search {
+    gts_index *ix;
+    const gts_queries *qs;
+    cudaStream_t st;
+    IndexView iv;
+    QueryView qv;
+    int mode;          // 0 range, 1 knn
+    int64_t cap;
+    int pruning;
+    int64_t nq;
+    DBuf<float> r32;
+    DBuf<double> r64;
+    DBuf<int32_t> ks;
+    DBuf<unsigned long long> verified, pruned;
+    DBuf<unsigned long long> counter;   // [0] expand rows, [1] hits
+    unsigned long long *h_counter = nullptr;
+    // hits
+    DBuf<int32_t> hq, he;
+    DBuf<double> hd;
+    unsigned long long hits = 0;
+    int64_t peak = 0;
+    int64_t limits[64] = {0};
+
+    Search(gts_index *ix_, const gts_queries *q_, cudaStream_t s, int mode_, int64_t cap_, int pruning_)
+        : ix(ix_), qs(q_), st(s), mode(mode_), cap(cap_), pruning(pruning_), nq(q_->nq)
+    {
+        iv = make_view(ix, qs);
+        qv = make_qview(ix, qs);
+        verified.alloc((size_t)nq, st);
+        pruned.alloc((size_t)nq, st);
+        CK(cudaMemsetAsync(verified.p, 0, sizeof(unsigned long long) * nq, st));
+        CK(cudaMemsetAsync(pruned.p, 0, sizeof(unsigned long long) * nq, st));
+        counter.alloc(2, st);
+        CK(cudaMemsetAsync(counter.p, 0, 2 * sizeof(unsigned long long), st));
+        h_counter = pinned_counters();
+        size_t hcap = (size_t)std::max<int64_t>(1 << 16, nq * 16);
+        hq.alloc(hcap, st);
+        he.alloc(hcap, st);
+        hd.alloc(hcap, st);
+    }
+
+    unsigned long long read_counter(int i)
+    {
+        CK(cudaMemcpyAsync(h_counter + i, counter.p + i, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        return h_counter[i];
+    }
+
+    template <int MET>
+    void launch_verify(const Row *rows, int64_t m, int stats_on)
+    {
+        HitBuf hb{hq.p, he.p, hd.p, (unsigned long long)hq.n, counter.p + 1};
+        unsigned grid = grid_for(m * 32, 256, 148u * 64u);
+        k_verify<MET><<<grid, 256, 0, st>>>(iv, qv, rows, m, pruning, r32.p, r64.p, hb, verified.p, stats_on);
+        LAUNCH_CHECK();
+    }
+
+    void verify(const Row *rows, int64_t m)
+    {
+        const unsigned long long before = hits;
+        dispatch_verify(rows, m, 1);
+        unsigned long long after = read_counter(1);
+        if (after > hq.n) {
+            // grow the hit buffer and redo this launch (stats already counted)
+            size_t ncap = (size_t)std::max<unsigned long long>(after * 2, hq.n * 2);
+            DBuf<int32_t> nq_(ncap, st), ne_(ncap, st);
+            DBuf<double> nd_(ncap, st);
+            if (before) {
+                CK(cudaMemcpyAsync(nq_.p, hq.p, before * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+                CK(cudaMemcpyAsync(ne_.p, he.p, before * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+                CK(cudaMemcpyAsync(nd_.p, hd.p, before * sizeof(double), cudaMemcpyDeviceToDevice, st));
+            }
+            hq = std::move(nq_);
+            he = std::move(ne_);
+            hd = std::move(nd_);
+            h_counter[1] = before;
+            CK(cudaMemcpyAsync(counter.p + 1, h_counter + 1, sizeof(unsigned long long), cudaMemcpyHostToDevice, st));
+            dispatch_verify(rows, m, 0);
+            after = read_counter(1);
+        }
+        hits = after;
+    }
+
+    void dispatch_verify(const Row *rows, int64_t m, int stats_on)
+    {
+        switch (ix->metric) {
+        case GTS_EDIT: launch_verify<kMetricEdit>(rows, m, stats_on); break;
+        case GTS_L1: launch_verify<kMetricL1>(rows, m, stats_on); break;
+        default: launch_verify<kMetricL2>(rows, m, stats_on); break;
+        }
+    }
+
+    template <int MET>
+    int64_t launch_expand(const Row *in, int64_t m, int own, Row *out)
+    {
+        CK(cudaMemsetAsync(counter.p, 0, sizeof(unsigned long long), st));
+        unsigned grid = grid_for(m * ix->nc, 256, 148u * 32u);
+        k_expand<MET><<<grid, 256, 0, st>>>(iv, qv, in, m, own, pruning, r32.p, out, counter.p, pruned.p);
+        LAUNCH_CHECK();
+        return (int64_t)read_counter(0);
+    }
+
+    int64_t expand(const Row *in, int64_t m, int layer, Row *out)
+    {
+        const int own = (layer + 1) == ix->levels;
+        switch (ix->metric) {
+        case GTS_EDIT: return launch_expand<kMetricEdit>(in, m, own, out);
+        case GTS_L1: return launch_expand<kMetricL1>(in, m, own, out);
+        default: return launch_expand<kMetricL2>(in, m, own, out);
+        }
+    }
+
+    // depth-first over layers in chunks of level_size_limit parent rows
+    void process(int layer, const Row *rows, int64_t m)
+    {
+        if (m == 0) return;
+        if (layer == ix->levels) { verify(rows, m); return; }
+        const int64_t s = level_size_limit(cap, ix->nc, ix->split_rounds, layer);
+        if (layer < 64 && limits[layer] == 0) limits[layer] = s;
+        for (int64_t off = 0; off < m; off += s) {
+            const int64_t mm = std::min<int64_t>(s, m - off);
+            DBuf<Row> child((size_t)(mm * ix->nc), st);
+            int64_t cnt = expand(rows + off, mm, layer, child.p);
+            peak = std::max(peak, cnt);
+            if (cnt > cap) fail(GTS_EBUDGET, "table of %lld rows overflows budget %lld", (long long)cnt, (long long)cap);
+            process(layer + 1, child.p, cnt);
+        }
+    }
+
+    template <int MET>
+    void launch_root(Row *out)
+    {
+        k_root<MET><<<grid_for(nq, 256), 256, 0, st>>>(iv, qv, (int)nq, out);
+        LAUNCH_CHECK();
+    }
+
+    template <int MET>
+    void launch_probe()
+    {
+        k_probe<MET><<<grid_for(nq, 1, 148u * 16u), 256, 0, st>>>(iv, qv, (int)nq, ks.p, r32.p, r64.p);
+        LAUNCH_CHECK();
+    }
+
+    void run()
+    {
+        if (ix->levels == 0 || ix->n == 0 || nq == 0) return;
+        if (mode == 1 && pruning) {
+            switch (ix->metric) {
+            case GTS_EDIT: launch_probe<kMetricEdit>(); break;
+            case GTS_L1: launch_probe<kMetricL1>(); break;
+            default: launch_probe<kMetricL2>(); break;
+            }
+        }
+        if (!pruning) {
+            // every live entry of every leaf is verified (search.py:338-355)
+            const int64_t nl = std::max(ix->n_live_leaves, 1);
+            const int64_t qchunk = std::max<int64_t>(1, cap / nl);
+            for (int64_t q0 = 0; q0 < nq; q0 += qchunk) {
+                const int64_t nqc = std::min<int64_t>(qchunk, nq - q0);
+                const int64_t m = nqc * ix->n_live_leaves;
+                if (m == 0) continue;
+                DBuf<Row> rows((size_t)m, st);
+                k_all_leaves<<<grid_for(m, 256), 256, 0, st>>>(ix->live_leaves.p, ix->n_live_leaves, (int)q0,
+                                                               (int)nqc, rows.p);
+                LAUNCH_CHECK();
+                verify(rows.p, m);
+            }
+            return;
+        }
+        DBuf<Row> root((size_t)nq, st);
+        switch (ix->metric) {
+        case GTS_EDIT: launch_root<kMetricEdit>(root.p); break;
+        case GTS_L1: launch_root<kMetricL1>(root.p); break;
+        default: launch_root<kMetricL2>(root.p); break;
+        }
+        process(1, root.p, nq);
+    }
+
+    // sort hits by (q, d, id) and build the CSR result (search.py:298-314)
+    void collect(gts_result *res)
+    {
+        const int64_t n = (int64_t)hits;
+        res->nq = nq;
+        res->peak = peak;
+        std::memcpy(res->limits, limits, sizeof(limits));
+        res->stream = st;
+        res->offsets.alloc((size_t)nq + 1, st);
+        res->verified = std::move(verified);
+        res->pruned = std::move(pruned);
+        DBuf<long long> counts((size_t)nq + 1, st), outcnt((size_t)nq + 1, st);
+        DBuf<long long> in_off((size_t)nq + 1, st), out_off((size_t)nq + 1, st);
+        CK(cudaMemsetAsync(counts.p, 0, sizeof(long long) * (nq + 1), st));
+        DBuf<int32_t> perm_a, perm_b;
+        if (n > 0) {
+            DBuf<unsigned long long> ka((size_t)n, st), kb((size_t)n, st);
+            perm_a.alloc((size_t)n, st);
+            perm_b.alloc((size_t)n, st);
+            const unsigned g = grid_for(n, 256);
+            k_gather_id<<<g, 256, 0, st>>>(he.p, n, ix->ids.p, ka.p, perm_a.p);
+            LAUNCH_CHECK();
+            size_t tmp_bytes = 0, t2 = 0;
+            cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, ka.p, kb.p, perm_a.p, perm_b.p, (int)n, 0, 64, st);
+            cub::DeviceRadixSort::SortPairs(nullptr, t2, (uint32_t *)nullptr, (uint32_t *)nullptr, perm_a.p,
+                                            perm_b.p, (int)n, 0, 32, st);
+            tmp_bytes = std::max(tmp_bytes, t2);
+            DBuf<uint8_t> tmp(tmp_bytes, st);
+            // 1) by id
+            CK(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, ka.p, kb.p, perm_a.p, perm_b.p, (int)n, 0, 64, st));
+            g_launches += 4;
+            // 2) stable by distance bits (non-negative doubles order as integers)
+            k_gather_d<<<g, 256, 0, st>>>(hd.p, perm_b.p, n, ka.p);
+            LAUNCH_CHECK();
+            CK(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, ka.p, kb.p, perm_b.p, perm_a.p, (int)n, 0, 64, st));
+            g_launches += 4;
+            // 3) stable by query
+            DBuf<uint32_t> qa((size_t)n, st), qb((size_t)n, st);
+            k_gather_q<<<g, 256, 0, st>>>(hq.p, perm_a.p, n, qa.p);
+            LAUNCH_CHECK();
+            int qbits = 1;
+            while ((1ll << qbits) < nq) qbits++;
+            CK(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, qa.p, qb.p, perm_a.p, perm_b.p, (int)n, 0, qbits, st));
+            g_launches += 2;
+            k_count<<<g, 256, 0, st>>>(hq.p, n, counts.p);
+            LAUNCH_CHECK();
+        }
+        k_clamp_counts<<<grid_for(nq, 256), 256, 0, st>>>(counts.p, mode == 1 ? ks.p : nullptr, (int)nq, outcnt.p);
+        LAUNCH_CHECK();
+        size_t sb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, sb, counts.p, in_off.p, (int)nq + 1, st);
+        DBuf<uint8_t> stmp(sb, st);
+        CK(cub::DeviceScan::ExclusiveSum(stmp.p, sb, counts.p, in_off.p, (int)nq + 1, st));
+        CK(cub::DeviceScan::ExclusiveSum(stmp.p, sb, outcnt.p, out_off.p, (int)nq + 1, st));
+        g_launches += 2;
+        long long total = 0;
+        CK(cudaMemcpyAsync(&total, out_off.p + nq, sizeof(long long), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        res->total = total;
+        res->ids.alloc((size_t)std::max<long long>(total, 1), st);
+        res->dis.alloc((size_t)std::max<long long>(total, 1), st);
+        CK(cudaMemcpyAsync(res->offsets.p, out_off.p, sizeof(long long) * (nq + 1), cudaMemcpyDeviceToDevice, st));
+        if (n > 0) {
+            k_emit<<<grid_for(n, 256), 256, 0, st>>>(perm_b.p, hq.p, he.p, hd.p, in_off.p, out_off.p, outcnt.p,
+                                                     ix->ids.p, n, res->ids.p, res->dis.p);
+            LAUNCH_CHECK();
+        }
+    }
+};
+
+void check_queries(const gts_index *ix, const gts_queries *q)
+{
+    if (!ix || !q) fail(GTS_EINVAL, "null index or queries");
+    if (q->metric != ix->metric) fail(GTS_EMETRIC, "query metric %d != index metric %d", q->metric, ix->metric);
+    if (ix->metric != GTS_EDIT && ix->n > 0 && q->D != ix->D)
+        fail(GTS_EMETRIC, "query dimensionality %d != dataset dimensionality %d", q->D, ix->D);
+}
+
+gts_queries *upload_queries(gts_index *ix, const gts_query_batch *qb, cudaStream_t st)
+{
+    if (!qb) fail(GTS_EINVAL, "null query batch");
+    if (qb->nq < 0 || qb->nq > (1ll << 31) - 2) fail(GTS_EINVAL, "bad query count");
+    if (qb->metric != ix->metric) fail(GTS_EMETRIC, "query metric %d != index metric %d", qb->metric, ix->metric);
+    CK(cudaSetDevice(ix->device));
+    auto *q = new gts_queries();
+    try {
+        q->metric = qb->metric;
+        q->nq = qb->nq;
+        q->stream = st;
+        const int64_t nq = qb->nq;
+        if (ix->metric == GTS_EDIT) {
+            const int64_t nsym = nq ? qb->offsets[nq] : 0;
+            std::vector<int64_t> peq_off((size_t)nq + 1, 0);
+            for (int64_t i = 0; i < nq; i++) {
+                int64_t m = qb->offsets[i + 1] - qb->offsets[i];
+                if (m < 0) fail(GTS_EINVAL, "query offsets not monotone");
+                if (m > 32 * kMaxWords) fail(GTS_EINVAL, "query string longer than %d symbols", 32 * kMaxWords);
+                peq_off[(size_t)i + 1] = peq_off[(size_t)i] + (int64_t)ix->A * ((m + 31) / 32);
+            }
+            q->soff.alloc((size_t)nq + 1, st);
+            h2d(q->soff.p, qb->offsets, (size_t)nq + 1, st);
+            q->peq_off.alloc((size_t)nq + 1, st);
+            h2d(q->peq_off.p, peq_off.data(), (size_t)nq + 1, st);
+            q->str.alloc((size_t)std::max<int64_t>(nsym, 1), st);
+            q->peq.alloc((size_t)std::max<int64_t>(peq_off[(size_t)nq], 1), st);
+            CK(cudaMemsetAsync(q->peq.p, 0, sizeof(uint32_t) * q->peq.n, st));
+            if (nsym) {
+                DBuf<int32_t> codes((size_t)nsym, st);
+                h2d(codes.p, qb->codes, (size_t)nsym, st);
+                k_map_symbols<<<grid_for(nsym, 256), 256, 0, st>>>(codes.p, nsym, ix->alpha.p, ix->A, q->str.p);
+                LAUNCH_CHECK();
+                k_build_peq<<<grid_for(nsym, 256), 256, 0, st>>>(q->str.p, q->soff.p, q->peq_off.p, (int)nq, nsym,
+                                                                 q->peq.p);
+                LAUNCH_CHECK();
+            }
+        } else {
+            q->D = (int)qb->dim;
+            q->Dp = (q->D + 3) & ~3;
+            if (ix->n > 0 && q->D != ix->D)
+                fail(GTS_EMETRIC, "query dimensionality %d != dataset dimensionality %d", q->D, ix->D);
+            q->vec64.alloc((size_t)std::max<int64_t>(nq * q->D, 1), st);
+            h2d(q->vec64.p, qb->vectors, (size_t)(nq * q->D), st);
+            q->vec32.alloc((size_t)std::max<int64_t>(nq * q->Dp, 1), st);
+            DBuf<unsigned> flags(2, st);
+            CK(cudaMemsetAsync(flags.p, 0, 2 * sizeof(unsigned), st));
+            if (nq * q->Dp) {
+                k_vec_prep<<<grid_for(nq * q->Dp, 256), 256, 0, st>>>(q->vec64.p, nq, q->D, q->Dp, q->vec32.p,
+                                                                      flags.p, (int *)(flags.p + 1));
+                LAUNCH_CHECK();
+            }
+            unsigned hf[2];
+            CK(cudaMemcpyAsync(hf, flags.p, sizeof(hf), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            float mx;
+            std::memcpy(&mx, &hf[0], 4);
+            q->maxabs = mx;
+            q->exact = hf[1] == 0;
+        }
+        return q;
+    } catch (...) {
+        delete q;
+        throw;
+    }
+}
+
+gts_result *run_search(gts_index *ix, const gts_queries *q, int mode, const double *radii, const int64_t *ks,
+                       int64_t memory_units, int pruning, cudaStream_t st)
+{
+    check_queries(ix, q);
+    CK(cudaSetDevice(ix->device));
+    const int64_t cap = memory_units > 0 ? memory_units : (1ll << 20);
+    if (ix->n > 0 && cap < ix->nc) fail(GTS_EBUDGET, "memory_units %lld below fan-out %d", (long long)cap, ix->nc);
+    const int64_t nq = q->nq;
+    Search s(ix, q, st, mode, cap, pruning);
+    s.r32.alloc((size_t)std::max<int64_t>(nq, 1), st);
+    s.r64.alloc((size_t)std::max<int64_t>(nq, 1), st);
+    if (mode == 0) {
+        std::vector<float> h32((size_t)nq);
+        for (int64_t i = 0; i < nq; i++) {
+            if (!(radii[i] >= 0)) fail(GTS_EINVAL, "radius must be >= 0");
+            if (ix->metric == GTS_EDIT) {
+                double f = std::floor(radii[i]);
+                h32[(size_t)i] = (float)std::min(f, 16777216.0);
+            } else {
+                h32[(size_t)i] = round_up_f32(radii[i]);
+            }
+        }
+        h2d(s.r32.p, h32.data(), (size_t)nq, st);
+        h2d(s.r64.p, radii, (size_t)nq, st);
+    } else {
+        std::vector<int32_t> hk((size_t)nq);
+        for (int64_t i = 0; i < nq; i++) {
+            if (ks[i] < 1) fail(GTS_EINVAL, "k must be >= 1");
+            hk[(size_t)i] = (int32_t)std::min<int64_t>(ks[i], (1ll << 31) - 1);
+        }
+        s.ks.alloc((size_t)std::max<int64_t>(nq, 1), st);
+        h2d(s.ks.p, hk.data(), (size_t)nq, st);
+        if (!pruning) {
+            std::vector<float> inf32((size_t)nq, INFINITY);
+            std::vector<double> inf64((size_t)nq, INFINITY);
+            h2d(s.r32.p, inf32.data(), (size_t)nq, st);
+            h2d(s.r64.p, inf64.data(), (size_t)nq, st);
+        }
+    }
+    s.run();
+    auto *res = new gts_result();
+    try {
+        s.collect(res);
+    } catch (...) {
+        delete res;
+        throw;
+    }
+    return res;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+#define ABI_BEGIN try {
+#define ABI_END                                                                          \
+    }                                                                                    \
+    catch (const Error &e) { return e.code; }                                            \
+    catch (const std::bad_alloc &) { return set_error(GTS_EOOM, "host allocation failed"); } \
+    catch (...) { return set_error(GTS_EINVAL, "unexpected C++ exception"); }
+
+extern "C" const char *gts_last_error(void) { return g_err; }
+extern "C" const char *gts_version(void) { return "gts-b200 0.1 sm_100a"; }
+extern "C" int64_t gts_launch_count(void) { return g_launches.load(); }
+
+extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int device, gts_index **out)
+{
+    ABI_BEGIN
+    if (!ds || !t || !out) fail(GTS_EINVAL, "null argument");
+    if (ds->metric != GTS_EDIT && ds->metric != GTS_L1 && ds->metric != GTS_L2)
+        fail(GTS_EMETRIC, "metric %d not supported on the device path (edit, l1, l2)", ds->metric);
+    if (ds->n > (1ll << 31) - 64) fail(GTS_EINVAL, "index larger than 2^31 entries; shard it");
+    CK(cudaSetDevice(device));
+    {
+        cudaMemPool_t pool;
+        CK(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t thr = UINT64_MAX;
+        CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    }
+    auto *ix = new gts_index();
+    try {
+        cudaStream_t st = 0;
+        ix->device = device;
+        ix->metric = ds->metric;
+        ix->n = ds->n;
+        ix->nc = (int)t->nc;
+        ix->levels = (int)t->levels;
+        ix->split_rounds = (int)t->split_rounds;
+        ix->nodes = t->nodes;
+        const int64_t n = ds->n;
+        if (n == 0 || t->levels == 0) { *out = ix; return GTS_OK; }
+        // inverse permutation: table position of each dataset row
+        std::vector<int32_t> tpos((size_t)n);
+        for (int64_t e = 0; e < n; e++) tpos[(size_t)t->rows[e]] = (int32_t)e;
+        std::vector<NodeRec> nodes((size_t)t->nodes + 1);
+        std::vector<int32_t> npos((size_t)t->nodes + 1);
+        for (int64_t i = 0; i <= t->nodes; i++) {
+            NodeRec r;
+            float mn = (float)t->min_dis[i], mx = (float)t->max_dis[i];
+            if ((double)mn > t->min_dis[i]) mn = std::nextafter(mn, -INFINITY);
+            if ((double)mx < t->max_dis[i]) mx = std::nextafter(mx, INFINITY);
+            r.mn = mn;
+            r.mx = mx;
+            r.size = (int32_t)t->size[i];
+            r.piv = t->pivot_row[i] >= 0 ? tpos[(size_t)t->pivot_row[i]] : -1;
+            nodes[(size_t)i] = r;
+            npos[(size_t)i] = (int32_t)t->pos[i];
+        }
+        ix->node.alloc(nodes.size(), st);
+        h2d(ix->node.p, nodes.data(), nodes.size(), st);
+        ix->npos.alloc(npos.size(), st);
+        h2d(ix->npos.p, npos.data(), npos.size(), st);
+        // live leaves (for pruning-disabled scans)
+        {
+            __int128 c = 1;
+            for (int l = 1; l < ix->levels; l++) c *= ix->nc;
+            const int64_t first = (int64_t)((c - 1) / (ix->nc - 1) + 1), count = (int64_t)c;
+            std::vector<int32_t> lv;
+            for (int64_t i = first; i < first + count; i++) if (t->size[i] > 0) lv.push_back((int32_t)i);
+            ix->n_live_leaves = (int)lv.size();
+            ix->live_leaves.alloc(std::max<size_t>(lv.size(), 1), st);
+            h2d(ix->live_leaves.p, lv.data(), lv.size(), st);
+        }
+        std::vector<float> dis((size_t)n);
+        std::vector<int64_t> ids((size_t)n);
+        std::vector<uint32_t> alive((size_t)((n + 31) / 32), 0u);
+        for (int64_t e = 0; e < n; e++) {
+            dis[(size_t)e] = (float)t->dis[e];
+            ids[(size_t)e] = ds->ids[t->rows[e]];
+            if (!t->tombstone || t->tombstone[e] == 0) alive[(size_t)(e >> 5)] |= 1u << (e & 31);
+        }
+        ix->dis.alloc((size_t)n, st);
+        h2d(ix->dis.p, dis.data(), (size_t)n, st);
+        ix->ids.alloc((size_t)n, st);
+        h2d(ix->ids.p, ids.data(), (size_t)n, st);
+        ix->alive.alloc(alive.size(), st);
+        h2d(ix->alive.p, alive.data(), alive.size(), st);
+        if (ds->metric == GTS_EDIT) {
+            const int64_t ncodes = ds->offsets[n];
+            std::vector<int32_t> alpha(ds->codes, ds->codes + ncodes);
+            std::sort(alpha.begin(), alpha.end());
+            alpha.erase(std::unique(alpha.begin(), alpha.end()), alpha.end());
+            if (alpha.size() > 254)
+                fail(GTS_EMETRIC, "string alphabet of %zu symbols exceeds the device's 254", alpha.size());
+            ix->A = (int)alpha.size();
+            ix->h_alpha = alpha;
+            std::vector<int64_t> soff((size_t)n + 1, 0);
+            for (int64_t e = 0; e < n; e++) {
+                int64_t r = t->rows[e];
+                int64_t len = ds->offsets[r + 1] - ds->offsets[r];
+                ix->max_len = std::max<int>(ix->max_len, (int)len);
+                soff[(size_t)e + 1] = soff[(size_t)e] + len;
+            }
+            std::vector<uint8_t> sym((size_t)std::max<int64_t>(soff[(size_t)n], 1));
+            for (int64_t e = 0; e < n; e++) {
+                int64_t r = t->rows[e];
+                for (int64_t k = ds->offsets[r], o = soff[(size_t)e]; k < ds->offsets[r + 1]; k++, o++)
+                    sym[(size_t)o] = (uint8_t)(std::lower_bound(alpha.begin(), alpha.end(), ds->codes[k]) - alpha.begin());
+            }
+            ix->alpha.alloc(std::max<size_t>(alpha.size(), 1), st);
+            h2d(ix->alpha.p, alpha.data(), alpha.size(), st);
+            ix->soff.alloc(soff.size(), st);
+            h2d(ix->soff.p, soff.data(), soff.size(), st);
+            ix->str.alloc(sym.size(), st);
+            h2d(ix->str.p, sym.data(), sym.size(), st);
+        } else {
+            ix->D = (int)ds->dim;
+            ix->Dp = (ix->D + 3) & ~3;
+            std::vector<float> v32((size_t)(n * ix->Dp), 0.f);
+            bool exact = true;
+            float mx = 0.f;
+            for (int64_t e = 0; e < n; e++) {
+                const double *src = ds->vectors + t->rows[e] * ix->D;
+                for (int d = 0; d < ix->D; d++) {
+                    float f = (float)src[d];
+                    if ((double)f != src[d]) exact = false;
+                    mx = std::max(mx, std::fabs(f));
+                    v32[(size_t)(e * ix->Dp + d)] = f;
+                }
+            }
+            ix->data_exact = exact;
+            ix->data_maxabs = mx;
+            ix->vec32.alloc(v32.size(), st);
+            h2d(ix->vec32.p, v32.data(), v32.size(), st);
+            if (!exact) {
+                std::vector<double> v64((size_t)(n * ix->D));
+                for (int64_t e = 0; e < n; e++)
+                    std::memcpy(v64.data() + e * ix->D, ds->vectors + t->rows[e] * ix->D, sizeof(double) * ix->D);
+                ix->vec64.alloc(v64.size(), st);
+                h2d(ix->vec64.p, v64.data(), v64.size(), st);
+            }
+        }
+        CK(cudaStreamSynchronize(st));
+        *out = ix;
+        return GTS_OK;
+    } catch (...) {
+        delete ix;
+        throw;
+    }
+    ABI_END
+}
+
+extern "C" int gts_index_destroy(gts_index *ix)
+{
+    ABI_BEGIN
+    if (ix) {
+        cudaSetDevice(ix->device);
+        cudaDeviceSynchronize();
+        delete ix;
+    }
+    return GTS_OK;
+    ABI_END
+}
+
+extern "C" int gts_index_set_tombstones(gts_index *ix, const uint8_t *tomb, void *stream)
+{
+    ABI_BEGIN
+    if (!ix || !tomb) fail(GTS_EINVAL, "null argument");
+    if (ix->n == 0) return GTS_OK;
+    CK(cudaSetDevice(ix->device));
+    std::vector<uint32_t> alive((size_t)((ix->n + 31) / 32), 0u);
+    for (int64_t e = 0; e < ix->n; e++)
+        if (tomb[e] == 0) alive[(size_t)(e >> 5)] |= 1u << (e & 31);
+    cudaStream_t st = (cudaStream_t)stream;
+    h2d(ix->alive.p, alive.data(), alive.size(), st);
+    CK(cudaStreamSynchronize(st));
+    return GTS_OK;
+    ABI_END
+}
+
+extern "C" int gts_queries_upload(gts_index *ix, const gts_query_batch *qb, void *stream, gts_queries **out)
+{
+    ABI_BEGIN
+    if (!ix || !out) fail(GTS_EINVAL, "null argument");
+    *out = upload_queries(ix, qb, (cudaStream_t)stream);
+    return GTS_OK;
+    ABI_END
+}
+
+extern "C" int gts_queries_free(gts_queries *q)
+{
+    ABI_BEGIN
+    delete q;
+    return GTS_OK;
+    ABI_END
+}
+
+extern "C" int gts_range_batch(gts_index *ix, const gts_queries *q, const double *radii, int64_t memory_units,
+                               int pruning, void *stream, gts_result **out)
+{
+    ABI_BEGIN
+    if (!out || (!radii && q && q->nq)) fail(GTS_EINVAL, "null argument");
+    *out = run_search(ix, q, 0, radii, nullptr, memory_units, pruning, (cudaStream_t)stream);
+    return GTS_OK;
+    ABI_END
+}
+
+extern "C" int gts_knn_batch(gts_index *ix, const gts_queries *q, const int64_t *ks, int64_t memory_units,
+                             int pruning, void *stream, gts_result **out)
+{
+    ABI_BEGIN
+    if (!out || (!ks && q && q->nq)) fail(GTS_EINVAL, "null argument");
+    *out = run_search(ix, q, 1, nullptr, ks, memory_units, pruning, (cudaStream_t)stream);
+    return GTS_OK;
+    ABI_END
+}
+
+extern "C" int gts_range_batch_host(gts_index *ix, const gts_query_batch *qb, const double *radii,
+                                    int64_t memory_units, int pruning, void *stream, gts_result **out)
+{
+    ABI_BEGIN
+    if (!ix || !out) fail(GTS_EINVAL, "null argument");
+    gts_queries *q = upload_queries(ix, qb, (cudaStream_t)stream);
+    try {
+        *out = run_search(ix, q, 0, radii, nullptr, memory_units, pruning, (cudaStream_t)stream);
+    } catch (...) {
+        delete q;
+        throw;
+    }
+    delete q;
+    return GTS_OK;
+    ABI_END
+}
+
+extern "C" int gts_knn_batch_host(gts_index *ix, const gts_query_batch *qb, const int64_t *ks,
+                                  int64_t memory_units, int pruning, void *stream, gts_result **out)
+{
+    ABI_BEGIN
+    if (!ix || !out) fail(GTS_EINVAL, "null argument");
+    gts_queries *q = upload_queries(ix, qb, (cudaStream_t)stream);
+    try {
+        *out = run_search(ix, q, 1, nullptr, ks, memory_units, pruning, (cudaStream_t)stream);
+    } catch (...) {
+        delete q;
+        throw;
+    }
+    delete q;
+    return GTS_OK;
+    ABI_END
+}
+
+extern "C" int gts_result_info(const gts_result *r, int64_t *nq, int64_t *total, int64_t *peak, int64_t *limits)
+{
+    ABI_BEGIN
+    if (!r) fail(GTS_EINVAL, "null result");
+    if (nq) *nq = r->nq;
+    if (total) *total = r->total;
+    if (peak) *peak = r->peak;
+    if (limits) std::memcpy(limits, r->limits, sizeof(r->limits));
+    return GTS_OK;
+    ABI_END
+}
+
+extern "C" int gts_result_copy(const gts_result *r, int64_t *offsets, int64_t *ids, double *dis, int64_t *verified,
+                               int64_t *pruned, void *stream)
+{
+    ABI_BEGIN
+    if (!r) fail(GTS_EINVAL, "null result");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (offsets) CK(cudaMemcpyAsync(offsets, r->offsets.p, sizeof(int64_t) * (r->nq + 1), cudaMemcpyDefault, st));
+    if (ids && r->total) CK(cudaMemcpyAsync(ids, r->ids.p, sizeof(int64_t) * r->total, cudaMemcpyDefault, st));
+    if (dis && r->total) CK(cudaMemcpyAsync(dis, r->dis.p, sizeof(double) * r->total, cudaMemcpyDefault, st));
+    if (verified && r->nq && r->verified.p)
+        CK(cudaMemcpyAsync(verified, r->verified.p, sizeof(int64_t) * r->nq, cudaMemcpyDefault, st));
+    if (pruned && r->nq && r->pruned.p)
+        CK(cudaMemcpyAsync(pruned, r->pruned.p, sizeof(int64_t) * r->nq, cudaMemcpyDefault, st));
+    if (verified && r->nq && !r->verified.p) std::memset(verified, 0, sizeof(int64_t) * r->nq);
+    if (pruned && r->nq && !r->pruned.p) std::memset(pruned, 0, sizeof(int64_t) * r->nq);
+    CK(cudaStreamSynchronize(st));
+    return GTS_OK;
+    ABI_END
+}
+
+extern "C" int gts_result_device(const gts_result *r, const int64_t **offsets, const int64_t **ids,
+                                 const double **dis)
+{
+    ABI_BEGIN
+    if (!r) fail(GTS_EINVAL, "null result");
+    if (offsets) *offsets = r->offsets.p;
+    if (ids) *ids = r->ids.p;
+    if (dis) *dis = r->dis.p;
+    return GTS_OK;
+    ABI_END
+}
+
+extern "C" int gts_result_free(gts_result *r)
+{
+    ABI_BEGIN
+    delete r;
+    return GTS_OK;
+    ABI_END
+}
+
+extern "C" int gts_pair_distances(int32_t metric, int64_t np, int64_t dim, const double *a_vec, const double *b_vec,
+                                  const int32_t *a_codes, const int64_t *a_off, const int32_t *b_codes,
+                                  const int64_t *b_off, double *out, void *stream)
+{
+    ABI_BEGIN
+    cudaStream_t st = (cudaStream_t)stream;
+    if (np == 0) return GTS_OK;
+    if (metric == GTS_L1 || metric == GTS_L2) {
+        DBuf<double> a((size_t)(np * dim), st), b((size_t)(np * dim), st), o((size_t)np, st);
+        h2d(a.p, a_vec, (size_t)(np * dim), st);
+        h2d(b.p, b_vec, (size_t)(np * dim), st);
+        k_pair_vec<<<grid_for(np, 128), 128, 0, st>>>(metric, np, (int)dim, a.p, b.p, o.p);
+        LAUNCH_CHECK();
+        CK(cudaMemcpyAsync(out, o.p, sizeof(double) * np, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        return GTS_OK;
+    }
+    if (metric != GTS_EDIT) fail(GTS_EMETRIC, "metric %d not supported", metric);
+    // shared dense alphabet of both sides
+    const int64_t na = a_off[np], nb = b_off[np];
+    std::vector<int32_t> alpha(a_codes, a_codes + na);
+    alpha.insert(alpha.end(), b_codes, b_codes + nb);
+    std::sort(alpha.begin(), alpha.end());
+    alpha.erase(std::unique(alpha.begin(), alpha.end()), alpha.end());
+    if (alpha.size() > 254) fail(GTS_EMETRIC, "alphabet too large");
+    const int A = (int)alpha.size();
+    std::vector<int64_t> peq_off((size_t)np + 1, 0);
+    for (int64_t i = 0; i < np; i++) {
+        int64_t m = a_off[i + 1] - a_off[i];
+        if (m > 32 * kMaxWords) fail(GTS_EINVAL, "string too long");
+        peq_off[(size_t)i + 1] = peq_off[(size_t)i] + (int64_t)A * ((m + 31) / 32);
+    }
+    DBuf<int32_t> dalpha(std::max<size_t>(alpha.size(), 1), st);
+    h2d(dalpha.p, alpha.data(), alpha.size(), st);
+    DBuf<int32_t> ca((size_t)std::max<int64_t>(na, 1), st), cb((size_t)std::max<int64_t>(nb, 1), st);
+    h2d(ca.p, a_codes, (size_t)na, st);
+    h2d(cb.p, b_codes, (size_t)nb, st);
+    DBuf<uint8_t> sa((size_t)std::max<int64_t>(na, 1), st), sb((size_t)std::max<int64_t>(nb, 1), st);
+    if (na) { k_map_symbols<<<grid_for(na, 256), 256, 0, st>>>(ca.p, na, dalpha.p, A, sa.p); LAUNCH_CHECK(); }
+    if (nb) { k_map_symbols<<<grid_for(nb, 256), 256, 0, st>>>(cb.p, nb, dalpha.p, A, sb.p); LAUNCH_CHECK(); }
+    DBuf<int64_t> aoff((size_t)np + 1, st), boff((size_t)np + 1, st), poff((size_t)np + 1, st);
+    h2d(aoff.p, a_off, (size_t)np + 1, st);
+    h2d(boff.p, b_off, (size_t)np + 1, st);
+    h2d(poff.p, peq_off.data(), (size_t)np + 1, st);
+    DBuf<uint32_t> peq((size_t)std::max<int64_t>(peq_off[(size_t)np], 1), st);
+    CK(cudaMemsetAsync(peq.p, 0, sizeof(uint32_t) * peq.n, st));
+    if (na) {
+        k_build_peq<<<grid_for(na, 256), 256, 0, st>>>(sa.p, aoff.p, poff.p, (int)np, na, peq.p);
+        LAUNCH_CHECK();
+    }
+    QueryView qa{};
+    qa.soff = aoff.p;
+    qa.str = sa.p;
+    qa.peq = peq.p;
+    qa.peq_off = poff.p;
+    qa.A = A;
+    DBuf<double> o((size_t)np, st);
+    k_pair_edit<<<grid_for(np, 128), 128, 0, st>>>(np, sb.p, boff.p, qa, o.p);
+    LAUNCH_CHECK();
+    CK(cudaMemcpyAsync(out, o.p, sizeof(double) * np, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return GTS_OK;
+    ABI_END
+}

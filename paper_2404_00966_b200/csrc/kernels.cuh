@@ -1,0 +1,243 @@
+// kernels.cuh -- sm_100a device code of the GTS batch search path.
+//
+// Device layout (all in HBM, built once per index by gts_index_create):
+//   node table   NodeRec[nodes+1] {min f32 (rounded down), max f32 (rounded
+//                up), size i32, pivot table-position i32}  16 B, one load
+//   node pos     i32[nodes+1]  first table entry of the node's segment
+//   object table dis f32[n] (entry -> own leaf pivot), ids i64[n],
+//                alive bitmask u32[n/32]   (all in table = leaf order)
+//   payloads     vectors: f32 [n][Dp] in table order (Dp = D rounded to 4),
+//                optional f64 [n][D] when the data is not fp32-exact;
+//                strings: dense u8 symbols in table order + i64 offsets.
+// Reference semantics being restated: search.py:28-57 (predicates),
+// 405-477 (_expand), 507-538 (_verify_range), metrics.py:54-133 (metrics).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace gts {
+
+constexpr int kWarp = 32;
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kMetricEdit = 0, kMetricL1 = 1, kMetricL2 = 2;
+constexpr int kMaxWords = 128;      // edit patterns up to 4096 symbols
+constexpr uint8_t kNoSym = 0xff;    // query symbol absent from the index alphabet
+
+struct NodeRec {
+    float mn, mx;
+    int32_t size, piv;
+};
+
+struct Row {            // one (query, node, d(q, node pivot)) frontier row
+    int32_t q, node;
+    float dqp;
+    int32_t pad;
+};
+
+struct IndexView {
+    const NodeRec *node;
+    const int32_t *npos;
+    const float *dis;
+    const uint32_t *alive;
+    const float *vec32;
+    const double *vec64;   // may be null (fp32-exact data: widen vec32)
+    const uint8_t *str;
+    const int64_t *soff;
+    int D, Dp, nc, levels;
+    float rel, abs_eps;    // fp32 slack model (vectors); 0 for edit
+};
+
+struct QueryView {
+    const float *vec32;    // [nq][Dp]
+    const double *vec64;   // [nq][D]
+    const int64_t *soff;   // [nq+1] symbol offsets
+    const uint8_t *str;    // dense symbols
+    const uint32_t *peq;   // Myers match masks, [A][W] per query
+    const int64_t *peq_off;
+    int A;
+};
+
+struct HitBuf {
+    int32_t *q;
+    int32_t *e;
+    double *d;
+    unsigned long long cap;
+    unsigned long long *counter;
+};
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+__device__ __forceinline__ bool is_alive(const uint32_t *alive, int e)
+{
+    return (__ldg(alive + (e >> 5)) >> (e & 31)) & 1u;
+}
+
+// ---------------------------------------------------------------------------
+// edit distance: Myers/Hyyro block bit-vector recurrence, pattern = query
+// (match masks precomputed per query), text = stored object.  Returns the
+// same integer as the reference DP (metrics.py:54-84).
+// ---------------------------------------------------------------------------
+template <int W>
+__device__ __forceinline__ int myers_fixed(const uint32_t *__restrict__ peq, int m,
+                                           const uint8_t *__restrict__ t, int n)
+{
+    uint32_t P[W], M[W];
+#pragma unroll
+    for (int b = 0; b < W; b++) { P[b] = ~0u; M[b] = 0u; }
+    const uint32_t last = 1u << ((m - 1) & 31);
+    int score = m;
+    for (int j = 0; j < n; j++) {
+        const uint32_t *eq = peq + (int)__ldg(t + j) * W;
+        int hin = 1;
+#pragma unroll
+        for (int b = 0; b < W; b++) {
+            uint32_t Eq = __ldg(eq + b), Pv = P[b], Mv = M[b];
+            uint32_t Xv = Eq | Mv;
+            if (hin < 0) Eq |= 1u;
+            uint32_t Xh = (((Eq & Pv) + Pv) ^ Pv) | Eq;
+            uint32_t Ph = Mv | ~(Xh | Pv);
+            uint32_t Mh = Pv & Xh;
+            const uint32_t hb = (b == W - 1) ? last : 0x80000000u;
+            int hout = (Ph & hb) ? 1 : ((Mh & hb) ? -1 : 0);
+            Ph = (Ph << 1) | (uint32_t)(hin > 0);
+            Mh = (Mh << 1) | (uint32_t)(hin < 0);
+            P[b] = Mh | ~(Xv | Ph);
+            M[b] = Ph & Xv;
+            hin = hout;
+        }
+        score += hin;
+    }
+    return score;
+}
+
+__device__ __noinline__ int myers_generic(const uint32_t *__restrict__ peq, int W, int m,
+                                          const uint8_t *__restrict__ t, int n)
+{
+    uint32_t P[kMaxWords], M[kMaxWords];
+    for (int b = 0; b < W; b++) { P[b] = ~0u; M[b] = 0u; }
+    const uint32_t last = 1u << ((m - 1) & 31);
+    int score = m;
+    for (int j = 0; j < n; j++) {
+        const uint32_t *eq = peq + (int)t[j] * W;
+        int hin = 1;
+        for (int b = 0; b < W; b++) {
+            uint32_t Eq = eq[b], Pv = P[b], Mv = M[b];
+            uint32_t Xv = Eq | Mv;
+            if (hin < 0) Eq |= 1u;
+            uint32_t Xh = (((Eq & Pv) + Pv) ^ Pv) | Eq;
+            uint32_t Ph = Mv | ~(Xh | Pv);
+            uint32_t Mh = Pv & Xh;
+            const uint32_t hb = (b == W - 1) ? last : 0x80000000u;
+            int hout = (Ph & hb) ? 1 : ((Mh & hb) ? -1 : 0);
+            Ph = (Ph << 1) | (uint32_t)(hin > 0);
+            Mh = (Mh << 1) | (uint32_t)(hin < 0);
+            P[b] = Mh | ~(Xv | Ph);
+            M[b] = Ph & Xv;
+            hin = hout;
+        }
+        score += hin;
+    }
+    return score;
+}
+
+__device__ __forceinline__ int edit_qt(const QueryView &qv, int q, const uint8_t *t, int n)
+{
+    const int64_t qo = qv.soff[q];
+    const int m = (int)(qv.soff[q + 1] - qo);
+    if (m == 0) return n;
+    if (n == 0) return m;
+    const uint32_t *peq = qv.peq + qv.peq_off[q];
+    const int W = (m + 31) >> 5;
+    switch (W) {
+    case 1: return myers_fixed<1>(peq, m, t, n);
+    case 2: return myers_fixed<2>(peq, m, t, n);
+    case 3: return myers_fixed<3>(peq, m, t, n);
+    case 4: return myers_fixed<4>(peq, m, t, n);
+    default: return myers_generic(peq, W, m, t, n);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// vectors: fp32 screening distance (float4 loads) and the exact float64
+// distance in numpy's pairwise row-sum order (bit-identical to the
+// reference's l1/l2_one_to_many, metrics.py:127-133).
+// ---------------------------------------------------------------------------
+template <int MET>
+__device__ __forceinline__ float vdist32(const float *__restrict__ a, const float *__restrict__ b, int Dp)
+{
+    float acc = 0.f;
+    const float4 *a4 = reinterpret_cast<const float4 *>(a);
+    const float4 *b4 = reinterpret_cast<const float4 *>(b);
+    for (int i = 0; i < (Dp >> 2); i++) {
+        float4 x = __ldg(a4 + i), y = __ldg(b4 + i);
+        float d0 = x.x - y.x, d1 = x.y - y.y, d2 = x.z - y.z, d3 = x.w - y.w;
+        if (MET == kMetricL1) acc += (fabsf(d0) + fabsf(d1)) + (fabsf(d2) + fabsf(d3));
+        else acc += (d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3);
+    }
+    return MET == kMetricL1 ? acc : sqrtf(acc);
+}
+
+template <int MET>
+__device__ __forceinline__ double term64(double x, double y)
+{
+    double d = __dadd_rn(x, -y);
+    return MET == kMetricL1 ? fabs(d) : __dmul_rn(d, d);
+}
+
+template <int MET>
+__device__ double pw_sum64(const float *o32, const double *o64, const double *q, int s, int n)
+{
+#define GTS_X(i) (o64 ? o64[(i)] : (double)o32[(i)])
+    if (n < 8) {
+        double r = 0.0;
+        for (int i = 0; i < n; i++) r = __dadd_rn(r, term64<MET>(GTS_X(s + i), q[s + i]));
+        return r;
+    }
+    if (n <= 128) {
+        double r[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) r[j] = term64<MET>(GTS_X(s + j), q[s + j]);
+        int i;
+        for (i = 8; i < n - (n % 8); i += 8) {
+#pragma unroll
+            for (int j = 0; j < 8; j++) r[j] = __dadd_rn(r[j], term64<MET>(GTS_X(s + i + j), q[s + i + j]));
+        }
+        double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                               __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+        for (; i < n; i++) res = __dadd_rn(res, term64<MET>(GTS_X(s + i), q[s + i]));
+        return res;
+    }
+#undef GTS_X
+    int n2 = n / 2;
+    n2 -= n2 % 8;
+    return __dadd_rn(pw_sum64<MET>(o32, o64, q, s, n2), pw_sum64<MET>(o32, o64, q, s + n2, n - n2));
+}
+
+template <int MET>
+__device__ __forceinline__ double vdist64(const IndexView &ix, const QueryView &qv, int q, int e)
+{
+    const float *o32 = ix.vec64 ? nullptr : ix.vec32 + (size_t)e * ix.Dp;
+    const double *o64 = ix.vec64 ? ix.vec64 + (size_t)e * ix.D : nullptr;
+    double s = pw_sum64<MET>(o32, o64, qv.vec64 + (size_t)q * ix.D, 0, ix.D);
+    return MET == kMetricL1 ? s : __dsqrt_rn(s);
+}
+
+// screening distance query q -> table entry e (exact integer for edit)
+template <int MET>
+__device__ __forceinline__ float dist32(const IndexView &ix, const QueryView &qv, int q, int e)
+{
+    if (MET == kMetricEdit) {
+        const int64_t o = ix.soff[e];
+        return (float)edit_qt(qv, q, ix.str + o, (int)(ix.soff[e + 1] - o));
+    } else {
+        return vdist32<MET>(ix.vec32 + (size_t)e * ix.Dp, qv.vec32 + (size_t)q * ix.Dp, ix.Dp);
+    }
+}
+
+// fp32 error slack for comparisons involving magnitudes a and b
+__device__ __forceinline__ float slack(const IndexView &ix, float a, float b)
+{
+    return ix.rel * (fabsf(a) + fabsf(b)) + ix.abs_eps;
+}
+
+}  // namespace gts
