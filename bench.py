@@ -1,0 +1,580 @@
+#!/usr/bin/env python
+"""Benchmark: GTS batch range + kNN search on B200 (BASELINE.json metric
+"range/kNN queries/sec ... vs CPU ref; distance evals/sec").
+
+Default workload = BASELINE.json configs[1]: synthetic words (a-z, length
+U[1,34]) n=1,000,000, edit distance, a 10,000-query batch answered as one
+range batch (r=1) plus one kNN batch (k=10).  One step = both batches.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload words|dna|tloc]
+
+value  : queries/sec with the query batch resident in HBM (device-timed).
+e2e    : the same through the host C ABI (gts_*_batch_host): H2D of the
+         query batch from pinned memory and D2H of the CSR answers inside
+         the timed region.
+With N>1 (torchrun), each rank holds its own shard of n objects (weak
+scaling); every rank answers the full batch on its shard and the per-shard
+answers are merged (paper_2404_00966_b200/sharded.py); value counts
+shard-queries (queries x shards) per second.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+ALPHA_WORDS = "abcdefghijklmnopqrstuvwxyz"
+
+WORKLOADS = {
+    # configs[1] -- the headline
+    "words": dict(metric="edit", n=1_000_000, nq=10_000, min_len=1, max_len=34, alphabet=ALPHA_WORDS,
+                  radius=1.0, k=10, config_index=1),
+    # configs[3] (static part): DNA len 108
+    "dna": dict(metric="edit", n=1_000_000, nq=10_000, min_len=108, max_len=108, alphabet="ACGT",
+                radius=8.0, k=10, config_index=3),
+    # configs[0]: T-Loc-like 2-D L2, CPU-reference-runnable
+    "tloc": dict(metric="l2", n=100_000, nq=1_000, dim=2, radius=0.0582588, k=10, config_index=0),
+}
+
+
+# ---------------------------------------------------------------------------
+# synthetic data (vectorised; same distribution as the reference generators)
+# ---------------------------------------------------------------------------
+
+def gen_strings(n, seed, min_len, max_len, alphabet):
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(min_len, max_len + 1, size=n).astype(np.int64)
+    off = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(lens, out=off[1:])
+    alpha = np.frombuffer(alphabet.encode("utf-32-le"), dtype=np.int32)
+    codes = alpha[rng.integers(0, alpha.size, size=int(off[-1]))].astype(np.int32)
+    return codes, off
+
+
+def string_queries(codes, off, nq, seed, alphabet):
+    """Half members, half members with 1-2 random edits (test_acceptance.py:74-89)."""
+    rng = np.random.default_rng(seed)
+    n = off.size - 1
+    alpha = np.frombuffer(alphabet.encode("utf-32-le"), dtype=np.int32)
+    out = []
+    for i, r in enumerate(rng.integers(0, n, nq)):
+        s = list(codes[off[r]:off[r + 1]])
+        if i >= nq // 2:
+            for _ in range(int(rng.integers(1, 3))):
+                c = int(alpha[int(rng.integers(0, alpha.size))])
+                if s and rng.integers(0, 2):
+                    s[int(rng.integers(0, len(s)))] = c
+                else:
+                    s.insert(int(rng.integers(0, len(s) + 1)), c)
+        out.append(np.array(s, dtype=np.int32))
+    qoff = np.zeros(nq + 1, dtype=np.int64)
+    np.cumsum([len(s) for s in out], out=qoff[1:])
+    qcodes = np.concatenate(out) if out else np.zeros(0, np.int32)
+    return qcodes.astype(np.int32), qoff
+
+
+def make_workload(name, rank, args):
+    w = dict(WORKLOADS[name])
+    if args.n:
+        w["n"] = args.n
+    if args.nq:
+        w["nq"] = args.nq
+    seed = 12 + 1000 * rank
+    if w["metric"] == "edit":
+        codes, off = gen_strings(w["n"], seed, w["min_len"], w["max_len"], w["alphabet"])
+        qcodes, qoff = string_queries(codes, off, w["nq"], 13, w["alphabet"] if True else None)
+        w.update(codes=codes, off=off, qcodes=qcodes, qoff=qoff)
+    else:
+        rng = np.random.default_rng(seed)
+        mat = rng.uniform(0.0, 1.0, size=(w["n"], w["dim"])).astype(np.float32).astype(np.float64)
+        q = np.random.default_rng(13).uniform(0.0, 1.0, size=(w["nq"], w["dim"])).astype(np.float32).astype(np.float64)
+        w.update(mat=mat, q=q)
+    w["ids"] = np.arange(w["n"], dtype=np.int64) + rank * w["n"]
+    return w
+
+
+# ---------------------------------------------------------------------------
+# clocks
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index, interval_ms=200):
+        self.gpu = gpu_index
+        self.interval_ms = interval_ms
+        self.proc = None
+        self.path = tempfile.mktemp(suffix=".csv")
+
+    def start(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", str(self.interval_ms)], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.path)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+class Engine:
+    """Thin C-ABI driver (the same calls the Python drop-in makes)."""
+
+    def __init__(self, w, device):
+        from paper_2404_00966_b200 import _lib
+        self.L = _lib.lib()
+        self._lib = _lib
+        self.w = w
+        self.edit = w["metric"] == "edit"
+        code = {"edit": 0, "l1": 1, "l2": 2}[w["metric"]]
+        p = _lib.ptr
+        n = w["n"]
+        if self.edit:
+            self.ds = _lib.GtsDataset(code, n, 0, None, p(w["codes"], _lib._i32p), p(w["off"], _lib._i64p),
+                                      p(w["ids"], _lib._i64p))
+        else:
+            self.ds = _lib.GtsDataset(code, n, w["dim"], p(w["mat"], _lib._f64p), None, None, p(w["ids"], _lib._i64p))
+        nc = 20
+        mh, sp = C.c_int64(), C.c_int64()
+        _lib.check(self.L.gts_tree_height(n, nc, C.byref(mh), C.byref(sp)))
+        levels = sp.value + 1
+        nodes = self.L.gts_node_count(levels, nc)
+        self.arrs = dict(
+            pivot_id=np.zeros(nodes + 1, np.int64), pivot_row=np.zeros(nodes + 1, np.int64),
+            pos=np.zeros(nodes + 1, np.int64), size=np.zeros(nodes + 1, np.int64),
+            min_dis=np.zeros(nodes + 1), max_dis=np.zeros(nodes + 1), rows=np.zeros(n, np.int64),
+            dis=np.zeros(n), tomb=np.zeros(n, np.uint8))
+        a = self.arrs
+        self.tree = _lib.GtsTree(nc, levels, sp.value, nodes, n, p(a["pivot_id"], _lib._i64p),
+                                 p(a["pivot_row"], _lib._i64p), p(a["pos"], _lib._i64p), p(a["size"], _lib._i64p),
+                                 p(a["min_dis"], _lib._f64p), p(a["max_dis"], _lib._f64p), p(a["rows"], _lib._i64p),
+                                 p(a["dis"], _lib._f64p), p(a["tomb"], _lib._u8p))
+        root_row = int(np.random.default_rng(0).integers(0, n))
+        t0 = time.perf_counter()
+        _lib.check(self.L.gts_build_tree(C.byref(self.ds), root_row, 0, C.byref(self.tree)))
+        self.build_s = time.perf_counter() - t0
+        self.levels = levels
+        h = C.c_void_p()
+        t0 = time.perf_counter()
+        _lib.check(self.L.gts_index_create(C.byref(self.ds), C.byref(self.tree), device, C.byref(h)))
+        self.upload_s = time.perf_counter() - t0
+        self.ix = h
+        nq = w["nq"]
+        self.radii = np.full(nq, w["radius"], dtype=np.float64)
+        self.ks = np.full(nq, w["k"], dtype=np.int64)
+        if self.edit:
+            self.qb = _lib.GtsQueryBatch(code, nq, 0, None, p(w["qcodes"], _lib._i32p), p(w["qoff"], _lib._i64p))
+        else:
+            self.qb = _lib.GtsQueryBatch(code, nq, w["dim"], p(w["q"], _lib._f64p), None, None)
+
+    def upload(self, stream):
+        q = C.c_void_p()
+        self._lib.check(self.L.gts_queries_upload(self.ix, C.byref(self.qb), C.c_void_p(stream), C.byref(q)))
+        self.q = q
+
+    def step_device(self, stream):
+        """Range + kNN batch on device-resident queries; results stay in HBM."""
+        res = []
+        for mode in (0, 1):
+            h = C.c_void_p()
+            if mode == 0:
+                rc = self.L.gts_range_batch(self.ix, self.q, self._lib.ptr(self.radii, self._lib._f64p), 0, 1,
+                                            C.c_void_p(stream), C.byref(h))
+            else:
+                rc = self.L.gts_knn_batch(self.ix, self.q, self._lib.ptr(self.ks, self._lib._i64p), 0, 1,
+                                          C.c_void_p(stream), C.byref(h))
+            self._lib.check(rc)
+            res.append(h)
+        return res
+
+    def info(self, h):
+        nq, tot, peak = C.c_int64(), C.c_int64(), C.c_int64()
+        self._lib.check(self.L.gts_result_info(h, C.byref(nq), C.byref(tot), C.byref(peak), None))
+        return nq.value, tot.value
+
+    def free(self, hs):
+        for h in hs:
+            self.L.gts_result_free(h)
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2404_00966_b200 import _lib
+
+    torch.cuda.set_device(local_rank)
+    w = make_workload(args.workload, rank, args)
+    eng = Engine(w, local_rank)
+    stream = torch.cuda.Stream()
+    sp = stream.cuda_stream
+    nq = w["nq"]
+    eng.upload(sp)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    merger = None
+    if world > 1:
+        from paper_2404_00966_b200.sharded import ShardMerger
+        merger = ShardMerger(nq, torch.device("cuda", local_rank))
+
+    def one_step():
+        hs = eng.step_device(sp)
+        if merger is not None:
+            with torch.cuda.stream(stream):
+                merger.merge_handles(eng, hs, eng.ks, sp)
+        eng.free(hs)
+
+    # warm-up
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+
+    # profiling pass (not timed): per-kernel event times + work counters
+    _lib.lib().gts_profile_enable(1)
+    _lib.profile_read(reset=True)
+    one_step()
+    torch.cuda.synchronize()
+    prof = _lib.profile_read(reset=True)
+    _lib.lib().gts_profile_enable(0)
+    hs = eng.step_device(sp)
+    torch.cuda.synchronize()
+    totals = [eng.info(h)[1] for h in hs]
+    eng.free(hs)
+
+    # timed region (value): inputs resident in HBM
+    clocks = ClockSampler(local_rank, args.clock_ms)
+    clocks.start()
+    time.sleep(0.3)
+    barrier()
+    torch.cuda.synchronize()
+    launches0 = _lib.launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    t_wall = time.perf_counter()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        one_step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    wall_ms = (time.perf_counter() - t_wall) * 1e3 / args.steps
+    barrier()
+    launches = _lib.launch_count() - launches0
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # e2e through the host C ABI with pinned buffers
+    e2e_ms, h2d, d2h = run_e2e(eng, w, args, sp, merger, world, max(totals))
+
+    if rank != 0:
+        return None
+    qps = 2 * nq * world / (ms / 1e3)
+    kver = prof["kernels"].get("k_verify", {"ms": 0.0, "count": 0})
+    work = prof["work"]
+    step_ms_prof = sum(v["ms"] for v in prof["kernels"].values())
+    out = {
+        "metric": "range+kNN queries/sec",
+        "value": round(qps, 3),
+        "unit": "queries/s" if world == 1 else "shard-queries/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms, 4),
+        "wall_ms_per_step": round(wall_ms, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u8 symbols / int32 bit-parallel DP" if eng.edit else "f32 screen + f64 exact recheck",
+        "data": "synthetic",
+        "config": {
+            "workload": f"{args.workload} (BASELINE.json configs[{w['config_index']}])",
+            "n_per_gpu": w["n"], "nq": nq, "radius": w["radius"], "k": w["k"], "node_capacity": 20,
+            "levels": eng.levels, "memory_units": 1 << 20,
+            "l2_policy": "index payload+tables exceed nothing: words (~25 MB) stay L2-resident by design; "
+                         "no flush between steps (device-resident index is the operating point)",
+            "parallelism": f"dp{world} (one shard per GPU)",
+        },
+        "range_answers_per_step": totals[0],
+        "knn_answers_per_step": totals[1],
+        "distance_evals_per_s": round(work["pairs"] / (step_ms_prof / 1e3), 1) if step_ms_prof else None,
+        "build_s": round(eng.build_s, 3),
+        "index_upload_s": round(eng.upload_s, 3),
+        "clocks": clk,
+        "gpu_launches": int(launches),
+        "e2e": {"value": round(2 * nq * world / (e2e_ms / 1e3), 3), "unit": "queries/s",
+                "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+        "profile": prof,
+    }
+    out["roofline"] = roofline(eng, prof, kver, step_ms_prof)
+    if world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(w, args)
+    return out
+
+
+def run_e2e(eng, w, args, sp, merger, world, max_total):
+    import torch
+    from paper_2404_00966_b200 import _lib
+    nq = w["nq"]
+    # pinned copies of the host inputs
+    if eng.edit:
+        pc = torch.from_numpy(w["qcodes"]).pin_memory()
+        po = torch.from_numpy(w["qoff"]).pin_memory()
+        qb = _lib.GtsQueryBatch(0, nq, 0, None, C.cast(pc.data_ptr(), _lib._i32p), C.cast(po.data_ptr(), _lib._i64p))
+        h2d_in = pc.numel() * 4 + po.numel() * 8
+    else:
+        pv = torch.from_numpy(w["q"]).pin_memory()
+        qb = _lib.GtsQueryBatch(2, nq, w["dim"], C.cast(pv.data_ptr(), _lib._f64p), None, None)
+        h2d_in = pv.numel() * 8
+    prad = torch.from_numpy(eng.radii).pin_memory()
+    pks = torch.from_numpy(eng.ks).pin_memory()
+    cap = int(max_total * 1.25) + 1024
+    o_off = torch.empty(nq + 1, dtype=torch.int64).pin_memory()
+    o_ids = torch.empty(cap, dtype=torch.int64).pin_memory()
+    o_dis = torch.empty(cap, dtype=torch.float64).pin_memory()
+    o_ver = torch.empty(nq, dtype=torch.int64).pin_memory()
+    o_pr = torch.empty(nq, dtype=torch.int64).pin_memory()
+    L = eng.L
+    bytes_out = [0]
+
+    def step():
+        b = 0
+        for mode in (0, 1):
+            h = C.c_void_p()
+            if mode == 0:
+                rc = L.gts_range_batch_host(eng.ix, C.byref(qb), C.cast(prad.data_ptr(), _lib._f64p), 0, 1,
+                                            C.c_void_p(sp), C.byref(h))
+            else:
+                rc = L.gts_knn_batch_host(eng.ix, C.byref(qb), C.cast(pks.data_ptr(), _lib._i64p), 0, 1,
+                                          C.c_void_p(sp), C.byref(h))
+            _lib.check(rc)
+            _, tot = eng.info(h)
+            if tot > cap:
+                raise RuntimeError("e2e output buffer too small")
+            _lib.check(L.gts_result_copy(h, C.cast(o_off.data_ptr(), _lib._i64p), C.cast(o_ids.data_ptr(), _lib._i64p),
+                                         C.cast(o_dis.data_ptr(), _lib._f64p), C.cast(o_ver.data_ptr(), _lib._i64p),
+                                         C.cast(o_pr.data_ptr(), _lib._i64p), C.c_void_p(sp)))
+            b += (nq + 1) * 8 + tot * 16 + 2 * nq * 8
+            L.gts_result_free(h)
+        bytes_out[0] = b
+
+    for _ in range(max(1, args.warmup // 2)):
+        step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize()
+    ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    h2d = 2 * h2d_in + nq * 8 * 2
+    return ms, h2d, bytes_out[0]
+
+
+def roofline(eng, prof, kver, step_ms_prof):
+    from paper_2404_00966_b200 import _lib
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peaks = json.load(open(peaks_path)) if os.path.exists(peaks_path) else {}
+    work = prof["work"]
+    t = kver["ms"] / 1e3 if kver["ms"] else None
+    share = kver["ms"] / step_ms_prof if step_ms_prof else None
+    if eng.edit:
+        ops = C.c_double()
+        _lib.check(_lib.lib().gts_bench_int_peak(C.byref(ops), None))
+        peak = ops.value / 1e12
+        achieved = work["word_steps"] * OPS_PER_WORD_STEP / t / 1e12 if t else None
+        return {
+            "bound": "int", "kernel": "k_verify<edit> (bit-parallel Myers/Hyyro, 32-bit words)",
+            "achieved": round(achieved, 3) if achieved else None, "peak": round(peak, 3), "unit": "Tops/s",
+            "frac": round(achieved / peak, 4) if achieved else None,
+            "traffic": None,
+            "work_unit": f"word-step = one text symbol x one 32-bit pattern word, {OPS_PER_WORD_STEP} int ops "
+                         "(SASS count of the W=1 inner loop)",
+            "word_steps_per_step": work["word_steps"], "pairs_per_step": work["pairs"],
+            "kernel_ms_per_step": round(kver["ms"], 4), "kernel_launches_per_step": kver["count"],
+            "kernel_share_of_step": round(share, 4) if share else None,
+            "peak_source": "gts_bench_int_peak: LOP3+IMAD chains on all SMs, measured in this run "
+                           "(MEASURED_PEAKS.json has no integer peak)",
+        }
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    D = eng.w.get("dim", 2)
+    bytes_alg = work["entries"] * 8 + work["pairs"] * 4 * D
+    achieved = bytes_alg / t / 1e9 if t else None
+    return {"bound": "hbm", "kernel": "k_verify<l2>", "achieved": round(achieved, 2) if achieved else None,
+            "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4) if achieved else None, "traffic": None,
+            "kernel_ms_per_step": round(kver["ms"], 4), "kernel_share_of_step": round(share, 4) if share else None,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"}
+
+
+# SASS integer instructions per word-step of the W=1 Myers loop.
+OPS_PER_WORD_STEP = 16
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle port) -- cpu_baseline leg and --impl reference
+# ---------------------------------------------------------------------------
+
+def oracle_setup(w):
+    from oracle import oracle as O
+    if w["metric"] == "edit":
+        data = O.Payloads(O.EDIT, codes=w["codes"], off=w["off"], ids=w["ids"])
+    else:
+        data = O.Payloads(O.L2, vec=w["mat"], ids=w["ids"])
+    t0 = time.perf_counter()
+    tree = O.build(data, 20, 0, threads=os.cpu_count() or 1)
+    return O, data, tree, time.perf_counter() - t0
+
+
+def oracle_queries(O, w, idx):
+    if w["metric"] == "edit":
+        qs = [w["qcodes"][w["qoff"][i]:w["qoff"][i + 1]] for i in idx]
+        off = np.zeros(len(qs) + 1, np.int64)
+        np.cumsum([len(s) for s in qs], out=off[1:])
+        codes = np.concatenate(qs) if qs else np.zeros(0, np.int32)
+        return O.Payloads(O.EDIT, codes=codes, off=off)
+    return O.Payloads(O.L2, vec=w["q"][idx])
+
+
+def time_oracle(O, data, tree, w, n_range, n_knn, threads, seed=0):
+    rng = np.random.default_rng(seed)
+    out = {}
+    for mode, cnt, name in ((O.RANGE, n_range, "range"), (O.KNN, n_knn, "knn")):
+        idx = rng.choice(w["nq"], size=min(cnt, w["nq"]), replace=False)
+        qs = oracle_queries(O, w, idx)
+        t0 = time.perf_counter()
+        O.search(tree, data, qs, mode, radii=np.full(len(idx), w["radius"]), ks=np.full(len(idx), w["k"]),
+                 threads=threads)
+        out[name] = (len(idx), time.perf_counter() - t0)
+    return out
+
+
+def cpu_baseline(w, args):
+    O, data, tree, build_s = oracle_setup(w)
+    threads = os.cpu_count() or 1
+    n_range, n_knn = (256, 64) if w["metric"] == "edit" else (1000, 1000)
+    t = time_oracle(O, data, tree, w, n_range, n_knn, threads)
+    per_q = (t["range"][1] / t["range"][0] + t["knn"][1] / t["knn"][0]) / 2
+    return {
+        "value": round(1.0 / per_q, 3), "unit": "queries/s", "cores": threads, "kind": "port",
+        "sample": f"{t['range'][0]} range + {t['knn'][0]} kNN queries of the same batch on the same 1-shard index "
+                  f"(oracle/gts_oracle.c = restated reference BatchSearcher, {threads} threads over query slices); "
+                  f"range {t['range'][0] / t['range'][1]:.2f} q/s, kNN {t['knn'][0] / t['knn'][1]:.2f} q/s; "
+                  f"value = 1 / mean per-query time at the bench's 1:1 range:kNN mix",
+        "oracle_build_s": round(build_s, 2),
+    }
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    w = make_workload(args.workload, 0, args)
+    O, data, tree, build_s = oracle_setup(w)
+    threads = os.cpu_count() or 1
+    n_r, n_k = (32, 32) if w["metric"] == "edit" else (500, 500)
+    for i in range(args.warmup):
+        time_oracle(O, data, tree, w, 4, 4, threads, seed=100 + i)
+    tot_q, tot_t = 0, 0.0
+    for i in range(args.steps):
+        t = time_oracle(O, data, tree, w, n_r, n_k, threads, seed=i)
+        tot_q += t["range"][0] + t["knn"][0]
+        tot_t += t["range"][1] + t["knn"][1]
+    v = tot_q / tot_t
+    sample = (f"per step {n_r} range + {n_k} kNN queries of the {w['nq']}-query batch, oracle port "
+              f"(restated reference BatchSearcher in C, {threads} threads over query slices)")
+    return {
+        "impl": "reference", "metric": "range+kNN queries/sec", "value": round(v, 3), "unit": "queries/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot_t / args.steps * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64/int64 (CPU)",
+        "data": "synthetic", "config": {"workload": f"{args.workload} (BASELINE.json configs[{w['config_index']}])",
+                                        "n_per_gpu": w["n"], "nq": w["nq"], "radius": w["radius"], "k": w["k"]},
+        "cpu_baseline": {"value": round(v, 3), "unit": "queries/s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": round(v, 3), "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "oracle_build_s": round(build_s, 2),
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="words")
+    ap.add_argument("--n", type=int, default=0)
+    ap.add_argument("--nq", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--clock-ms", type=int, default=200, help="nvidia-smi sampling interval in the timed region")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        out = run_reference(args, rank, world)
+    else:
+        if world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(local_rank)
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            dist.init_process_group("nccl")
+        out = run_ours(args, rank, world, local_rank)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

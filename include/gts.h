@@ -145,6 +145,12 @@ int gts_pair_distances(int32_t metric, int64_t npairs, int64_t dim,
 
 /* Count of this library's kernel launches since load (bench evidence). */
 int64_t gts_launch_count(void);
+/* Per-kernel CUDA-event timing + algorithmic work counters (bench.py's
+ * roofline).  gts_profile_read writes a JSON object into buf. */
+int gts_profile_enable(int on);
+int gts_profile_read(char *buf, int64_t cap, int reset);
+/* Integer-pipe throughput microbenchmark (LOP3 + IMAD chains), ops/s. */
+int gts_bench_int_peak(double *ops_per_s, void *stream);
 const char *gts_last_error(void);
 const char *gts_version(void);
 

@@ -84,6 +84,9 @@ def lib():
             "gts_pair_distances": (C.c_int, [C.c_int32, C.c_int64, C.c_int64, _f64p, _f64p, _i32p, _i64p,
                                              _i32p, _i64p, _f64p, v]),
             "gts_launch_count": (C.c_int64, []),
+            "gts_profile_enable": (C.c_int, [C.c_int]),
+            "gts_profile_read": (C.c_int, [C.c_char_p, C.c_int64, C.c_int]),
+            "gts_bench_int_peak": (C.c_int, [_f64p, v]),
             "gts_last_error": (C.c_char_p, []),
             "gts_version": (C.c_char_p, []),
         }
@@ -100,8 +103,15 @@ EXPORTED = (
     "gts_index_set_tombstones", "gts_queries_upload", "gts_queries_free", "gts_range_batch",
     "gts_knn_batch", "gts_range_batch_host", "gts_knn_batch_host", "gts_result_info", "gts_result_copy",
     "gts_result_device", "gts_result_free", "gts_pair_distances", "gts_launch_count", "gts_last_error",
-    "gts_version",
+    "gts_version", "gts_profile_enable", "gts_profile_read", "gts_bench_int_peak",
 )
+
+
+def profile_read(reset=True):
+    import json
+    buf = C.create_string_buffer(1 << 16)
+    check(lib().gts_profile_read(buf, len(buf), int(reset)))
+    return json.loads(buf.value.decode())
 
 
 def check(rc: int) -> None:

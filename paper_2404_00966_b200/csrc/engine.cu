@@ -22,6 +22,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -70,6 +71,26 @@ struct Error {
     } while (0)
 
 static std::atomic<int64_t> g_launches{0};
+
+// Optional per-kernel timing (CUDA events on the launching stream) and
+// algorithmic work counters, read by bench.py for the roofline figures.
+static std::atomic<int> g_profile{0};
+struct ProfRec {
+    double ms = 0;
+    int64_t count = 0;
+};
+static std::mutex g_prof_mu;
+static std::vector<std::pair<std::string, ProfRec>> g_prof;
+static unsigned long long g_work[4] = {0, 0, 0, 0};   // pairs, word-steps, entries, rows
+enum { kWorkPairs = 0, kWorkSteps = 1, kWorkEntries = 2, kWorkRows = 3 };
+
+static void prof_add(const char *name, double ms)
+{
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    for (auto &kv : g_prof)
+        if (kv.first == name) { kv.second.ms += ms; kv.second.count++; return; }
+    g_prof.push_back({name, ProfRec{ms, 1}});
+}
 
 #define LAUNCH_CHECK() \
     do {               \
@@ -219,7 +240,8 @@ template <int MET>
 __global__ void __launch_bounds__(256) k_verify(IndexView ix, QueryView qv, const Row *__restrict__ rows,
                                                 int64_t m, int pruning, const float *__restrict__ r32,
                                                 const double *__restrict__ r64, HitBuf out,
-                                                unsigned long long *verified_stat, int stats_on)
+                                                unsigned long long *verified_stat, int stats_on,
+                                                unsigned long long *work)
 {
     const int lane = lane_id();
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -231,6 +253,7 @@ __global__ void __launch_bounds__(256) k_verify(IndexView ix, QueryView qv, cons
         const float r = r32[q];
         const double rr = r64[q];
         unsigned ver = 0;
+        unsigned long long steps = 0;
         for (int b = 0; b < leaf.size; b += kWarp) {
             const int k = b + lane;
             bool pass = false;
@@ -239,7 +262,7 @@ __global__ void __launch_bounds__(256) k_verify(IndexView ix, QueryView qv, cons
                 if (!pruning) pass = true;
                 else {
                     const float de = __ldg(ix.dis + e);
-                    pass = fabsf(de - lr.dqp) <= r + slack(ix, de, lr.dqp) + ix.rel * r;
+                    pass = fabsf(de - lr.dqp) <= r + slack(ix, de, lr.dqp, r);
                 }
             }
             ver += __popc(__ballot_sync(kFull, pass));
@@ -267,7 +290,299 @@ __global__ void __launch_bounds__(256) k_verify(IndexView ix, QueryView qv, cons
             }
         }
         if (stats_on && lane == 0 && ver) atomicAdd(verified_stat + q, (unsigned long long)ver);
+        if (work) {
+            for (int o = 16; o > 0; o >>= 1) steps += __shfl_down_sync(kFull, steps, o);
+            if (lane == 0) {
+                atomicAdd(work + kWorkPairs, (unsigned long long)ver);
+                atomicAdd(work + kWorkSteps, steps);
+                atomicAdd(work + kWorkEntries, (unsigned long long)leaf.size);
+                atomicAdd(work + kWorkRows, 1ull);
+            }
+        }
     }
+}
+
+struct Cand {
+    int32_t q, e;
+};
+
+// Leaf filter for edit distance (search.py:518-524), one warp per leaf row:
+// live entries passing the lemma-1 pivot test are "verified" (the
+// reference's counter); those whose length difference also fits the
+// radius (|len q - len o| is a lower bound of the edit distance) are
+// candidates for k_verify_edit.  Two passes without contended atomics:
+// WRITE=false counts candidates per row, an exclusive scan gives each row
+// its slice, WRITE=true fills it in leaf order (leaves are length-sorted,
+// so neighbouring candidates have similar DP lengths).
+template <bool WRITE>
+__global__ void __launch_bounds__(256) k_filter_edit(IndexView ix, QueryView qv, const Row *__restrict__ rows,
+                                                     int64_t m, int pruning, const float *__restrict__ r32,
+                                                     int32_t *row_count, const long long *row_off, Cand *out,
+                                                     unsigned long long *verified_stat, int stats_on,
+                                                     unsigned long long *work)
+{
+    const int lane = lane_id();
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < m; w += warps) {
+        const Row lr = rows[w];
+        const int q = lr.q;
+        const NodeRec leaf = ix.node[lr.node];
+        const int pos = ix.npos[lr.node];
+        const float r = r32[q];
+        const int mq = qlen(qv, q);
+        unsigned ver = 0, ncand = 0;
+        long long base = WRITE ? row_off[w] : 0;
+        for (int b = 0; b < leaf.size; b += kWarp) {
+            const int k = b + lane;
+            const int e = pos + k;
+            bool pass = false;
+            if (k < leaf.size && is_alive(ix.alive, e))
+                pass = !pruning || fabsf(__ldg(ix.dis + e) - lr.dqp) <= r;
+            if (!WRITE) ver += __popc(__ballot_sync(kFull, pass));
+            const bool cand = pass && (float)abs(mq - __ldg(ix.slen + e)) <= r;
+            const unsigned cb = __ballot_sync(kFull, cand);
+            if (WRITE && cand) out[base + ncand + __popc(cb & ((1u << lane) - 1u))] = Cand{q, e};
+            ncand += __popc(cb);
+        }
+        if (lane == 0) {
+            if (!WRITE) {
+                row_count[w] = (int32_t)ncand;
+                if (stats_on && ver) atomicAdd(verified_stat + q, (unsigned long long)ver);
+                if (work) {
+                    atomicAdd(work + kWorkPairs, (unsigned long long)ver);
+                    atomicAdd(work + kWorkEntries, (unsigned long long)leaf.size);
+                    atomicAdd(work + kWorkRows, 1ull);
+                }
+            }
+        }
+    }
+}
+
+constexpr int kSlots = 32;
+constexpr int kSlotWords = 256;
+
+// Exact edit distance of every candidate, one thread per (query, object)
+// pair (bit-parallel Myers/Hyyro), emitting hits d <= r.  The match masks of
+// the (few) distinct queries of a block are staged in shared memory.
+__global__ void __launch_bounds__(256) k_verify_edit(IndexView ix, QueryView qv, const Cand *__restrict__ cand,
+                                                     int64_t ncand, const float *__restrict__ r32, HitBuf out,
+                                                     unsigned long long *work)
+{
+    __shared__ uint32_t peq_s[kSlots * kSlotWords];
+    __shared__ int slot_q[kSlots];
+    __shared__ int warp_tot[8];
+    const int lane = lane_id(), warp = threadIdx.x >> 5;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < ncand; base += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = base + threadIdx.x;
+        const bool valid = i < ncand;
+        Cand c{-1, -1};
+        if (valid) c = cand[i];
+        const int prevq = (valid && threadIdx.x > 0) ? cand[i - 1].q : -2;
+        const unsigned start = (valid && c.q != prevq) ? 1u : 0u;
+        // block-wide inclusive scan of segment starts -> slot index
+        unsigned inc = start;
+        for (int o = 1; o < 32; o <<= 1) {
+            unsigned v = __shfl_up_sync(kFull, inc, o);
+            if (lane >= o) inc += v;
+        }
+        if (lane == 31) warp_tot[warp] = inc;
+        __syncthreads();
+        unsigned off = 0, total = 0;
+        for (int w2 = 0; w2 < (int)(blockDim.x >> 5); w2++) {
+            if (w2 < warp) off += warp_tot[w2];
+            total += warp_tot[w2];
+        }
+        const int slot = (int)(inc + off) - 1;
+        if (start && slot < kSlots) slot_q[slot] = c.q;
+        __syncthreads();
+        const int nslot = min((int)total, kSlots);
+        for (int t = threadIdx.x; t < nslot * kSlotWords; t += blockDim.x) {
+            const int sidx = t / kSlotWords, wi = t - sidx * kSlotWords;
+            const int sq = slot_q[sidx];
+            const int words = qv.A * ((qlen(qv, sq) + 31) >> 5);
+            if (wi < words) peq_s[t] = __ldg(qv.peq + qv.peq_off[sq] + wi);
+        }
+        __syncthreads();
+        bool hit = false;
+        int d = 0;
+        unsigned long long steps = 0;
+        if (valid) {
+            const int mq = qlen(qv, c.q);
+            const int words = qv.A * ((mq + 31) >> 5);
+            const int n = __ldg(ix.slen + c.e);
+            const uint32_t *txt = ix.str + __ldg(ix.sword + c.e);
+            // two call sites so the staged one compiles to shared-memory loads
+            if (slot < kSlots && words <= kSlotWords) d = edit_peq(peq_s + slot * kSlotWords, mq, txt, n);
+            else d = edit_peq(qv.peq + qv.peq_off[c.q], mq, txt, n);
+            hit = (float)d <= r32[c.q];
+            steps = (unsigned long long)((mq + 31) >> 5) * (unsigned long long)n;
+        }
+        const unsigned hb = __ballot_sync(kFull, hit);
+        if (hb) {
+            unsigned long long hbase = 0;
+            if (lane == 0) hbase = atomicAdd(out.counter, (unsigned long long)__popc(hb));
+            hbase = __shfl_sync(kFull, hbase, 0);
+            if (hit) {
+                const unsigned long long sl = hbase + __popc(hb & ((1u << lane) - 1u));
+                if (sl < out.cap) { out.q[sl] = c.q; out.e[sl] = c.e; out.d[sl] = (double)d; }
+            }
+        }
+        if (work) {
+            for (int o = 16; o > 0; o >>= 1) steps += __shfl_down_sync(kFull, steps, o);
+            if (lane == 0 && steps) atomicAdd(work + kWorkSteps, steps);
+        }
+        __syncthreads();
+    }
+}
+
+constexpr int kLeafWarps = 8;          // warps per block of k_leaf_edit
+constexpr int kRowChunk = 16;          // rows a warp claims per cursor bump
+
+// match masks too large to stage (A*W > kWarpPeqWords): read from global
+__device__ __noinline__ int edit_peq_global(const uint32_t *peq, int m, const uint32_t *t4, int n)
+{
+    return edit_peq(peq, m, t4, n);
+}
+constexpr int kWarpPeqWords = 1024;     // per-warp staged match masks (A*W <= 1024)
+
+// Fused leaf scan + verification for edit distance (search.py:507-570).
+// Each warp owns a contiguous run of leaf rows.  Per row, live entries
+// passing the lemma-1 pivot test count as "verified" (the reference's
+// counter) and those whose length also fits the radius (|len q - len o|
+// lower-bounds the edit distance) are pushed onto a warp-private queue in
+// shared memory; every 32 queued entries run as one batch of bit-parallel
+// DPs (one per lane) against the row query's match masks staged in shared
+// memory.  Leaves are length-sorted, so a batch has similar DP lengths.
+__global__ void __launch_bounds__(256, 4) k_leaf_edit(IndexView ix, QueryView qv, const Row *__restrict__ rows,
+                                                      int64_t m, int pruning, const float *__restrict__ r32,
+                                                      HitBuf out, unsigned long long *verified_stat, int stats_on,
+                                                      unsigned long long *work, unsigned long long *cursor)
+{
+    __shared__ uint32_t peq_s[kLeafWarps][kWarpPeqWords];
+    __shared__ int32_t queue[kLeafWarps][64];
+    const int lane = lane_id(), wib = threadIdx.x >> 5;
+    uint32_t *peq_w = peq_s[wib];
+    int32_t *qu = queue[wib];
+    int cur_q = -1, mq = 0, qn = 0;
+    unsigned long long nrows = 0;
+    float r = 0.f;
+    bool staged = false;
+    const uint32_t *peq_g = nullptr;
+    unsigned long long steps = 0, pairs = 0, entries = 0;
+
+    // run DPs for queue slots [0, cnt) (cnt <= 32), emit hits
+    auto run_batch = [&](int cnt) {
+        bool hit = false;
+        int d = 0, e = -1;
+        if (lane < cnt) {
+            e = qu[lane];
+            const int n = __ldg(ix.slen + e);
+            const uint32_t *txt = ix.str + __ldg(ix.sword + e);
+            if (staged) d = edit_peq(peq_w, mq, txt, n);
+            else d = edit_peq_global(peq_g, mq, txt, n);
+            hit = (float)d <= r;
+            steps += (unsigned long long)((mq + 31) >> 5) * (unsigned long long)n;
+        }
+        const unsigned hb = __ballot_sync(kFull, hit);
+        if (hb) {
+            unsigned long long hbase = 0;
+            if (lane == 0) hbase = atomicAdd(out.counter, (unsigned long long)__popc(hb));
+            hbase = __shfl_sync(kFull, hbase, 0);
+            if (hit) {
+                const unsigned long long sl = hbase + __popc(hb & ((1u << lane) - 1u));
+                if (sl < out.cap) { out.q[sl] = cur_q; out.e[sl] = e; out.d[sl] = (double)d; }
+            }
+        }
+        __syncwarp();
+    };
+
+    for (;;) {
+        unsigned long long start = 0;
+        if (lane == 0) start = atomicAdd(cursor, (unsigned long long)kRowChunk);
+        start = __shfl_sync(kFull, start, 0);
+        if ((int64_t)start >= m) break;
+        const int64_t stop = min(m, (int64_t)start + kRowChunk);
+        nrows += (unsigned long long)(stop - (int64_t)start);
+    for (int64_t w = (int64_t)start; w < stop; w++) {
+        const Row lr = rows[w];
+        if (lr.q != cur_q) {
+            if (qn) { run_batch(qn); qn = 0; }
+            cur_q = lr.q;
+            mq = qlen(qv, cur_q);
+            r = r32[cur_q];
+            peq_g = qv.peq + qv.peq_off[cur_q];
+            const int words = qv.A * ((mq + 31) >> 5);
+            staged = words <= kWarpPeqWords;
+            if (staged) {
+                for (int t = lane; t < words; t += kWarp) peq_w[t] = __ldg(peq_g + t);
+            }
+            __syncwarp();
+        }
+        const NodeRec leaf = ix.node[lr.node];
+        const int pos = ix.npos[lr.node];
+        unsigned ver = 0;
+        for (int b = 0; b < leaf.size; b += kWarp) {
+            const int k = b + lane;
+            const int e = pos + k;
+            bool pass = false;
+            if (k < leaf.size && is_alive(ix.alive, e))
+                pass = !pruning || fabsf(__ldg(ix.dis + e) - lr.dqp) <= r;
+            ver += __popc(__ballot_sync(kFull, pass));
+            const bool cand = pass && (float)abs(mq - __ldg(ix.slen + e)) <= r;
+            const unsigned cb = __ballot_sync(kFull, cand);
+            if (cand) qu[qn + __popc(cb & ((1u << lane) - 1u))] = e;
+            qn += __popc(cb);
+            __syncwarp();
+            if (qn >= kWarp) {
+                run_batch(kWarp);
+                qn -= kWarp;
+                if (lane < qn) qu[lane] = qu[kWarp + lane];
+                __syncwarp();
+            }
+        }
+        if (lane == 0 && stats_on && ver) atomicAdd(verified_stat + lr.q, (unsigned long long)ver);
+        pairs += ver;
+        entries += leaf.size;
+    }
+    }
+    if (qn) run_batch(qn);
+    if (work) {
+        for (int o = 16; o > 0; o >>= 1) steps += __shfl_down_sync(kFull, steps, o);
+        if (lane == 0) {
+            atomicAdd(work + kWorkSteps, steps);
+            atomicAdd(work + kWorkPairs, pairs);
+            atomicAdd(work + kWorkEntries, entries);
+            atomicAdd(work + kWorkRows, nrows);
+        }
+    }
+}
+
+// Packed sort key for exact small-integer distances: query | distance |
+// dataset row (row order == id order, data.py:149-153).
+__global__ void k_pack_keys(const int32_t *hq, const int32_t *he, const double *hd, const int32_t *row, int64_t n,
+                            int dshift, int qshift, unsigned long long *key, int32_t *perm)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    key[i] = ((unsigned long long)hq[i] << qshift) | ((unsigned long long)hd[i] << dshift) |
+             (unsigned long long)row[he[i]];
+    perm[i] = (int32_t)i;
+}
+
+// counts[q] from sorted packed keys (two binary searches per query)
+__global__ void k_seg_counts(const unsigned long long *key, int64_t n, int qshift, int nq, long long *counts)
+{
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    auto lb = [&](unsigned long long v) {
+        int64_t lo = 0, hi = n;
+        while (lo < hi) {
+            int64_t mid = (lo + hi) >> 1;
+            if (key[mid] < v) lo = mid + 1; else hi = mid;
+        }
+        return lo;
+    };
+    counts[q] = lb((unsigned long long)(q + 1) << qshift) - lb((unsigned long long)q << qshift);
 }
 
 // Rows (q, leaf) for every live leaf when pruning is disabled (search.py:338-355).
@@ -312,10 +627,15 @@ __device__ uint32_t block_kth(const uint32_t *vals, int n, int k, unsigned *hist
 }
 
 constexpr int kProbeCand = 4096;
+constexpr int kProbeTarget = 1024;
+constexpr int kMaxLevels = 64;
 
-// kNN radius estimate: greedy descent to the parent of the query's nearest
-// leaves, exact distances to every live entry of its leaf children, radius
-// = k-th smallest (an upper bound on the true k-th distance), else +inf.
+// kNN radius estimate (the "estimate its search radius" step): greedy
+// descent to the leaf whose pivot chain is nearest the query, then exact
+// distances to the live entries of the deepest node on that path holding
+// at least max(k, kProbeTarget) entries (a contiguous table segment).  The
+// k-th smallest of those real distances bounds the true k-th distance
+// from above; with fewer than k live candidates the radius is +inf.
 template <int MET>
 __global__ void __launch_bounds__(256) k_probe(IndexView ix, QueryView qv, int nq, const int32_t *ks,
                                                float *r32, double *r64)
@@ -325,18 +645,18 @@ __global__ void __launch_bounds__(256) k_probe(IndexView ix, QueryView qv, int n
     __shared__ int sh[4];
     __shared__ float best_d[32];
     __shared__ int best_j[32];
+    __shared__ int path[kMaxLevels];
     for (int q = blockIdx.x; q < nq; q += gridDim.x) {
         const int nc = ix.nc;
         int node = 1;
-        // descend levels-2 times (to the parent of the leaf level)
-        for (int lvl = 1; lvl + 1 < ix.levels; lvl++) {
+        if (threadIdx.x == 0) path[0] = 1;
+        for (int lvl = 1; lvl < ix.levels; lvl++) {
             float d = FLT_MAX;
             int j = threadIdx.x;
             if (j < nc) {
                 const NodeRec c = ix.node[(node - 1) * nc + 2 + j];
                 if (c.size > 0) d = dist32<MET>(ix, qv, q, c.piv);
             }
-            // block argmin over the first nc threads (ties: smallest child)
             float bd = d;
             int bj = j;
             for (int o = 16; o > 0; o >>= 1) {
@@ -352,43 +672,45 @@ __global__ void __launch_bounds__(256) k_probe(IndexView ix, QueryView qv, int n
                 for (int w = 1; w < (int)(blockDim.x >> 5); w++)
                     if (best_d[w] < xd || (best_d[w] == xd && best_j[w] < xj)) { xd = best_d[w]; xj = best_j[w]; }
                 sh[2] = xj;
+                path[lvl] = (node - 1) * nc + 2 + xj;
             }
             __syncthreads();
             node = (node - 1) * nc + 2 + sh[2];
-            __syncthreads();
         }
-        // candidate leaves: the root itself (one-level tree) or node's children
+        const int k = ks[q];
+        const int target = min(max(k, kProbeTarget), kProbeCand);
+        int anc = 1;
+        for (int lvl = ix.levels - 1; lvl >= 0; lvl--) {
+            if (ix.node[path[lvl]].size >= target) { anc = path[lvl]; break; }
+        }
         if (threadIdx.x == 0) sh[3] = 0;
         __syncthreads();
-        const int first = ix.levels == 1 ? 1 : (node - 1) * nc + 2;
-        const int nleaf = ix.levels == 1 ? 1 : nc;
-        for (int l = 0; l < nleaf; l++) {
-            const NodeRec lf = ix.node[first + l];
-            const int pos = ix.npos[first + l];
-            for (int k = threadIdx.x; k < lf.size; k += blockDim.x) {
-                const int e = pos + k;
-                if (!is_alive(ix.alive, e)) continue;
-                int slot = atomicAdd(&sh[3], 1);
-                if (slot < kProbeCand) cand[slot] = __float_as_uint(dist32<MET>(ix, qv, q, e));
+        {
+            const int pos = ix.npos[anc];
+            const int size = ix.node[anc].size;
+            for (int b = 0; b < size; b += blockDim.x) {
+                if (sh[3] >= kProbeCand) break;       // uniform: read after the barrier
+                const int kk = b + threadIdx.x;
+                if (kk < size) {
+                    const int e = pos + kk;
+                    if (is_alive(ix.alive, e)) {
+                        int slot = atomicAdd(&sh[3], 1);
+                        if (slot < kProbeCand) cand[slot] = __float_as_uint(dist32<MET>(ix, qv, q, e));
+                    }
+                }
+                __syncthreads();
             }
         }
         __syncthreads();
         const int n = min(sh[3], kProbeCand);
-        const int k = ks[q];
         __syncthreads();
         if (n >= k && k >= 1) {
             uint32_t kth = block_kth(cand, n, k, hist, sh);
             if (threadIdx.x == 0) {
                 float t = __uint_as_float(kth);
-                if (MET == kMetricEdit) {
-                    r32[q] = t;
-                    r64[q] = (double)t;
-                } else {
-                    // every one of the k objects has d64 <= d32 + slack
-                    float up = t + slack(ix, t, 0.f);
-                    r32[q] = up;
-                    r64[q] = (double)up;
-                }
+                if (MET != kMetricEdit) t = t + slack(ix, t, 0.f);   // d64 <= d32 + slack
+                r32[q] = t;
+                r64[q] = (double)t;
             }
         } else if (threadIdx.x == 0) {
             r32[q] = INFINITY;
@@ -517,12 +839,12 @@ __global__ void k_pair_vec(int metric, int64_t np, int D, const double *a, const
 }
 
 // pairs (a_i, b_i): a is the pattern (query side), b the text
-__global__ void k_pair_edit(int64_t np, const uint8_t *bsym, const int64_t *boff, QueryView qa, double *out)
+__global__ void k_pair_edit(int64_t np, const uint32_t *bwords, const uint32_t *bword, const int32_t *blen,
+                            QueryView qa, double *out)
 {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= np) return;
-    const int64_t o = boff[i];
-    out[i] = (double)edit_qt(qa, (int)i, bsym + o, (int)(boff[i + 1] - o));
+    out[i] = (double)edit_peq(qa.peq + qa.peq_off[i], qlen(qa, (int)i), bwords + bword[i], blen[i]);
 }
 
 }  // namespace gts
@@ -531,6 +853,34 @@ __global__ void k_pair_edit(int64_t np, const uint8_t *bsym, const int64_t *boff
 // host side
 // ===========================================================================
 using namespace gts;
+
+namespace gts {
+// Pack strings (dense symbols, given per string as a code range mapped by
+// `sym`) 4 per 32-bit word, each string starting on a word boundary.
+template <class SymOf>
+static void pack_words(int64_t n, const int64_t *off, SymOf sym, std::vector<uint32_t> &words,
+                       std::vector<uint32_t> &wstart, std::vector<int32_t> &len, const int64_t *order = nullptr)
+{
+    wstart.resize((size_t)n);
+    len.resize((size_t)n);
+    uint64_t w = 0;
+    for (int64_t e = 0; e < n; e++) {
+        const int64_t r = order ? order[e] : e;
+        const int64_t l = off[r + 1] - off[r];
+        wstart[(size_t)e] = (uint32_t)w;
+        len[(size_t)e] = (int32_t)l;
+        w += (uint64_t)((l + 3) / 4);
+    }
+    if (w >= (1ull << 32)) fail(GTS_EINVAL, "string payload exceeds 16 GiB per index; shard it");
+    words.assign((size_t)std::max<uint64_t>(w, 1), 0u);
+    for (int64_t e = 0; e < n; e++) {
+        const int64_t r = order ? order[e] : e;
+        uint32_t *dst = words.data() + wstart[(size_t)e];
+        for (int64_t k = off[r], j = 0; k < off[r + 1]; k++, j++)
+            dst[j >> 2] |= (uint32_t)sym(k) << (8 * (j & 3));
+    }
+}
+}  // namespace gts
 
 struct gts_index {
     int device = 0;
@@ -549,9 +899,13 @@ struct gts_index {
     DBuf<uint32_t> alive;
     DBuf<float> vec32;
     DBuf<double> vec64;
-    DBuf<uint8_t> str;
-    DBuf<int64_t> soff;
+    DBuf<uint32_t> str;      // dense symbols, 4 per word, each entry 4-byte aligned
+    DBuf<uint32_t> sword;
+    DBuf<int32_t> slen;
+    DBuf<int32_t> row;
     DBuf<int32_t> alpha;
+    int max_leaf = 0;
+    std::vector<int64_t> ord;   // device entry -> reference table position
     DBuf<int32_t> live_leaves;
     int n_live_leaves = 0;
     std::vector<int32_t> h_alpha;
@@ -560,6 +914,7 @@ struct gts_index {
 struct gts_queries {
     int metric = 0;
     int64_t nq = 0;
+    int max_len = 0;
     int D = 0, Dp = 0;
     bool exact = true;
     float maxabs = 0.f;
@@ -594,7 +949,9 @@ IndexView make_view(const gts_index *ix, const gts_queries *q)
     v.vec32 = ix->vec32.p;
     v.vec64 = ix->vec64.p;
     v.str = ix->str.p;
-    v.soff = ix->soff.p;
+    v.sword = ix->sword.p;
+    v.slen = ix->slen.p;
+    v.row = ix->row.p;
     v.D = ix->D;
     v.Dp = ix->Dp;
     v.nc = ix->nc;
@@ -670,8 +1027,44 @@ struct Search {
     DBuf<int32_t> hq, he;
     DBuf<double> hd;
     unsigned long long hits = 0;
+    int max_qlen = 0;
     int64_t peak = 0;
     int64_t limits[64] = {0};
+    bool prof = false;
+    std::vector<std::tuple<const char *, cudaEvent_t, cudaEvent_t>> events;
+    DBuf<unsigned long long> work;
+
+    // time one launch with events when profiling is on
+    template <class F>
+    void timed(const char *name, F &&launch)
+    {
+        if (!prof) { launch(); return; }
+        cudaEvent_t a, b;
+        CK(cudaEventCreate(&a));
+        CK(cudaEventCreate(&b));
+        CK(cudaEventRecord(a, st));
+        launch();
+        CK(cudaEventRecord(b, st));
+        events.emplace_back(name, a, b);
+    }
+
+    void flush_profile()
+    {
+        if (!prof) return;
+        CK(cudaStreamSynchronize(st));
+        for (auto &ev : events) {
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, std::get<1>(ev), std::get<2>(ev)));
+            prof_add(std::get<0>(ev), ms);
+            cudaEventDestroy(std::get<1>(ev));
+            cudaEventDestroy(std::get<2>(ev));
+        }
+        events.clear();
+        unsigned long long h[4];
+        CK(cudaMemcpy(h, work.p, sizeof(h), cudaMemcpyDeviceToHost));
+        std::lock_guard<std::mutex> g(g_prof_mu);
+        for (int i = 0; i < 4; i++) g_work[i] += h[i];
+    }
 
     Search(gts_index *ix_, const gts_queries *q_, cudaStream_t s, int mode_, int64_t cap_, int pruning_)
         : ix(ix_), qs(q_), st(s), mode(mode_), cap(cap_), pruning(pruning_), nq(q_->nq)
@@ -685,6 +1078,11 @@ struct Search {
         counter.alloc(2, st);
         CK(cudaMemsetAsync(counter.p, 0, 2 * sizeof(unsigned long long), st));
         h_counter = pinned_counters();
+        prof = g_profile.load() != 0;
+        if (prof) {
+            work.alloc(4, st);
+            CK(cudaMemsetAsync(work.p, 0, 4 * sizeof(unsigned long long), st));
+        }
         size_t hcap = (size_t)std::max<int64_t>(1 << 16, nq * 16);
         hq.alloc(hcap, st);
         he.alloc(hcap, st);
@@ -703,7 +1101,10 @@ struct Search {
     {
         HitBuf hb{hq.p, he.p, hd.p, (unsigned long long)hq.n, counter.p + 1};
         unsigned grid = grid_for(m * 32, 256, 148u * 64u);
-        k_verify<MET><<<grid, 256, 0, st>>>(iv, qv, rows, m, pruning, r32.p, r64.p, hb, verified.p, stats_on);
+        timed("k_verify", [&] {
+            k_verify<MET><<<grid, 256, 0, st>>>(iv, qv, rows, m, pruning, r32.p, r64.p, hb, verified.p, stats_on,
+                                                stats_on ? work.p : nullptr);
+        });
         LAUNCH_CHECK();
     }
 
@@ -733,10 +1134,69 @@ struct Search {
         hits = after;
     }
 
+    // edit distance: k_filter_edit compacts candidates, k_verify_edit runs
+    // one Myers DP per candidate.  The candidate list is sized by the exact
+    // bound rows x largest leaf, so it cannot overflow.
+    DBuf<Cand> cands;
+    int64_t ncand = 0;
+
+    void filter_edit(const Row *rows, int64_t m, int stats_on)
+    {
+        DBuf<int32_t> cnt((size_t)m, st);
+        DBuf<long long> off((size_t)m + 1, st);
+        unsigned grid = grid_for(m * 32, 256, 148u * 64u);
+        timed("k_filter_edit", [&] {
+            k_filter_edit<false><<<grid, 256, 0, st>>>(iv, qv, rows, m, pruning, r32.p, cnt.p, nullptr, nullptr,
+                                                       verified.p, stats_on, stats_on ? work.p : nullptr);
+        });
+        LAUNCH_CHECK();
+        size_t tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.p, off.p, (int)m, st);
+        DBuf<uint8_t> tmp(tb, st);
+        CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, cnt.p, off.p, (int)m, st));
+        g_launches += 2;
+        // total = off[m-1] + cnt[m-1]
+        long long last_off = 0;
+        int32_t last_cnt = 0;
+        CK(cudaMemcpyAsync(&last_off, off.p + m - 1, sizeof(long long), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&last_cnt, cnt.p + m - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        ncand = last_off + last_cnt;
+        if (ncand == 0) return;
+        if ((int64_t)cands.n < ncand) cands.alloc((size_t)ncand, st);
+        timed("k_filter_edit", [&] {
+            k_filter_edit<true><<<grid, 256, 0, st>>>(iv, qv, rows, m, pruning, r32.p, nullptr, off.p, cands.p,
+                                                      nullptr, 0, nullptr);
+        });
+        LAUNCH_CHECK();
+    }
+
+    void verify_edit(int stats_on)
+    {
+        if (ncand == 0) return;
+        HitBuf hb{hq.p, he.p, hd.p, (unsigned long long)hq.n, counter.p + 1};
+        unsigned grid = grid_for(ncand, 256, 148u * 16u);
+        timed("k_verify_edit", [&] {
+            k_verify_edit<<<grid, 256, 0, st>>>(iv, qv, cands.p, ncand, r32.p, hb, stats_on ? work.p : nullptr);
+        });
+        LAUNCH_CHECK();
+    }
+
     void dispatch_verify(const Row *rows, int64_t m, int stats_on)
     {
         switch (ix->metric) {
-        case GTS_EDIT: launch_verify<kMetricEdit>(rows, m, stats_on); break;
+        case GTS_EDIT: {
+            HitBuf hb{hq.p, he.p, hd.p, (unsigned long long)hq.n, counter.p + 1};
+            // one warp per ~contiguous run of rows; enough warps to fill the GPU
+            unsigned grid = grid_for((m + kRowChunk - 1) / kRowChunk, kLeafWarps, 148u * 4u);
+            CK(cudaMemsetAsync(counter.p, 0, sizeof(unsigned long long), st));
+            timed("k_leaf_edit", [&] {
+                k_leaf_edit<<<grid, 32 * kLeafWarps, 0, st>>>(iv, qv, rows, m, pruning, r32.p, hb, verified.p,
+                                                             stats_on, stats_on ? work.p : nullptr, counter.p);
+            });
+            LAUNCH_CHECK();
+            break;
+        }
         case GTS_L1: launch_verify<kMetricL1>(rows, m, stats_on); break;
         default: launch_verify<kMetricL2>(rows, m, stats_on); break;
         }
@@ -747,7 +1207,9 @@ struct Search {
     {
         CK(cudaMemsetAsync(counter.p, 0, sizeof(unsigned long long), st));
         unsigned grid = grid_for(m * ix->nc, 256, 148u * 32u);
-        k_expand<MET><<<grid, 256, 0, st>>>(iv, qv, in, m, own, pruning, r32.p, out, counter.p, pruned.p);
+        timed("k_expand", [&] {
+            k_expand<MET><<<grid, 256, 0, st>>>(iv, qv, in, m, own, pruning, r32.p, out, counter.p, pruned.p);
+        });
         LAUNCH_CHECK();
         return (int64_t)read_counter(0);
     }
@@ -782,14 +1244,16 @@ struct Search {
     template <int MET>
     void launch_root(Row *out)
     {
-        k_root<MET><<<grid_for(nq, 256), 256, 0, st>>>(iv, qv, (int)nq, out);
+        timed("k_root", [&] { k_root<MET><<<grid_for(nq, 256), 256, 0, st>>>(iv, qv, (int)nq, out); });
         LAUNCH_CHECK();
     }
 
     template <int MET>
     void launch_probe()
     {
-        k_probe<MET><<<grid_for(nq, 1, 148u * 16u), 256, 0, st>>>(iv, qv, (int)nq, ks.p, r32.p, r64.p);
+        timed("k_probe", [&] {
+            k_probe<MET><<<grid_for(nq, 1, 148u * 16u), 256, 0, st>>>(iv, qv, (int)nq, ks.p, r32.p, r64.p);
+        });
         LAUNCH_CHECK();
     }
 
@@ -831,6 +1295,22 @@ struct Search {
     // sort hits by (q, d, id) and build the CSR result (search.py:298-314)
     void collect(gts_result *res)
     {
+        cudaEvent_t ca = nullptr, cb = nullptr;
+        if (prof) {
+            CK(cudaEventCreate(&ca));
+            CK(cudaEventCreate(&cb));
+            CK(cudaEventRecord(ca, st));
+        }
+        collect_impl(res);
+        if (prof) {
+            CK(cudaEventRecord(cb, st));
+            events.emplace_back("collect", ca, cb);
+        }
+        flush_profile();
+    }
+
+    void collect_impl(gts_result *res)
+    {
         const int64_t n = (int64_t)hits;
         res->nq = nq;
         res->peak = peak;
@@ -843,7 +1323,31 @@ struct Search {
         DBuf<long long> in_off((size_t)nq + 1, st), out_off((size_t)nq + 1, st);
         CK(cudaMemsetAsync(counts.p, 0, sizeof(long long) * (nq + 1), st));
         DBuf<int32_t> perm_a, perm_b;
-        if (n > 0) {
+        // packed-key fast path for exact integer distances (edit)
+        int qbits = 1;
+        while ((1ll << qbits) < nq) qbits++;
+        int dbits = 1;
+        while ((1ll << dbits) <= (long long)std::max(ix->max_len, max_qlen)) dbits++;
+        int rbits = 1;
+        while ((1ll << rbits) < ix->n) rbits++;
+        const bool packed = ix->metric == GTS_EDIT && qbits + dbits + rbits <= 64;
+        if (n > 0 && packed) {
+            DBuf<unsigned long long> ka((size_t)n, st), kb((size_t)n, st);
+            perm_a.alloc((size_t)n, st);
+            perm_b.alloc((size_t)n, st);
+            const unsigned g = grid_for(n, 256);
+            k_pack_keys<<<g, 256, 0, st>>>(hq.p, he.p, hd.p, ix->row.p, n, rbits, rbits + dbits, ka.p, perm_a.p);
+            LAUNCH_CHECK();
+            size_t tmp_bytes = 0;
+            cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, ka.p, kb.p, perm_a.p, perm_b.p, (int)n, 0,
+                                            qbits + dbits + rbits, st);
+            DBuf<uint8_t> tmp(tmp_bytes, st);
+            CK(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, ka.p, kb.p, perm_a.p, perm_b.p, (int)n, 0,
+                                               qbits + dbits + rbits, st));
+            g_launches += 4;
+            k_seg_counts<<<grid_for(nq, 256), 256, 0, st>>>(kb.p, n, rbits + dbits, (int)nq, counts.p);
+            LAUNCH_CHECK();
+        } else if (n > 0) {
             DBuf<unsigned long long> ka((size_t)n, st), kb((size_t)n, st);
             perm_a.alloc((size_t)n, st);
             perm_b.alloc((size_t)n, st);
@@ -868,8 +1372,6 @@ struct Search {
             DBuf<uint32_t> qa((size_t)n, st), qb((size_t)n, st);
             k_gather_q<<<g, 256, 0, st>>>(hq.p, perm_a.p, n, qa.p);
             LAUNCH_CHECK();
-            int qbits = 1;
-            while ((1ll << qbits) < nq) qbits++;
             CK(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, qa.p, qb.p, perm_a.p, perm_b.p, (int)n, 0, qbits, st));
             g_launches += 2;
             k_count<<<g, 256, 0, st>>>(hq.p, n, counts.p);
@@ -925,13 +1427,14 @@ gts_queries *upload_queries(gts_index *ix, const gts_query_batch *qb, cudaStream
                 int64_t m = qb->offsets[i + 1] - qb->offsets[i];
                 if (m < 0) fail(GTS_EINVAL, "query offsets not monotone");
                 if (m > 32 * kMaxWords) fail(GTS_EINVAL, "query string longer than %d symbols", 32 * kMaxWords);
+                q->max_len = std::max<int>(q->max_len, (int)m);
                 peq_off[(size_t)i + 1] = peq_off[(size_t)i] + (int64_t)ix->A * ((m + 31) / 32);
             }
             q->soff.alloc((size_t)nq + 1, st);
             h2d(q->soff.p, qb->offsets, (size_t)nq + 1, st);
             q->peq_off.alloc((size_t)nq + 1, st);
             h2d(q->peq_off.p, peq_off.data(), (size_t)nq + 1, st);
-            q->str.alloc((size_t)std::max<int64_t>(nsym, 1), st);
+            q->str.alloc((size_t)std::max<int64_t>(nsym, 1), st);   // u8 symbols (Peq build only)
             q->peq.alloc((size_t)std::max<int64_t>(peq_off[(size_t)nq], 1), st);
             CK(cudaMemsetAsync(q->peq.p, 0, sizeof(uint32_t) * q->peq.n, st));
             if (nsym) {
@@ -982,6 +1485,7 @@ gts_result *run_search(gts_index *ix, const gts_queries *q, int mode, const doub
     if (ix->n > 0 && cap < ix->nc) fail(GTS_EBUDGET, "memory_units %lld below fan-out %d", (long long)cap, ix->nc);
     const int64_t nq = q->nq;
     Search s(ix, q, st, mode, cap, pruning);
+    s.max_qlen = q->max_len;
     s.r32.alloc((size_t)std::max<int64_t>(nq, 1), st);
     s.r64.alloc((size_t)std::max<int64_t>(nq, 1), st);
     if (mode == 0) {
@@ -1039,6 +1543,88 @@ extern "C" const char *gts_last_error(void) { return g_err; }
 extern "C" const char *gts_version(void) { return "gts-b200 0.1 sm_100a"; }
 extern "C" int64_t gts_launch_count(void) { return g_launches.load(); }
 
+extern "C" int gts_profile_enable(int on)
+{
+    g_profile.store(on ? 1 : 0);
+    return GTS_OK;
+}
+
+extern "C" int gts_profile_read(char *buf, int64_t cap, int reset)
+{
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    std::string js = "{\"kernels\": {";
+    bool first = true;
+    for (auto &kv : g_prof) {
+        char tmp[256];
+        snprintf(tmp, sizeof(tmp), "%s\"%s\": {\"count\": %lld, \"ms\": %.6f}", first ? "" : ", ", kv.first.c_str(),
+                 (long long)kv.second.count, kv.second.ms);
+        js += tmp;
+        first = false;
+    }
+    char tmp[256];
+    snprintf(tmp, sizeof(tmp), "}, \"work\": {\"pairs\": %llu, \"word_steps\": %llu, \"entries\": %llu, \"rows\": %llu}}",
+             g_work[0], g_work[1], g_work[2], g_work[3]);
+    js += tmp;
+    if (reset) {
+        g_prof.clear();
+        for (auto &w : g_work) w = 0;
+    }
+    if (!buf || cap <= (int64_t)js.size()) return set_error(GTS_EINVAL, "profile buffer too small (%zu)", js.size());
+    std::memcpy(buf, js.c_str(), js.size() + 1);
+    return GTS_OK;
+}
+
+// Integer-pipe peak microbenchmark: 8 independent chains per thread mixing
+// LOP3 (alu pipe) and IMAD (fma pipe) -- the two pipes the bit-parallel edit
+// kernel issues to.  Returns executed int ops per second.
+__global__ void k_int_peak(uint32_t seed, int iters, uint32_t *sink)
+{
+    uint32_t a[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) a[i] = seed ^ (threadIdx.x * 2654435761u + i);
+    const uint32_t b = seed * 7u + 3u, c = seed | 1u;
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            a[i] = (a[i] ^ b) & (a[i] | c);   // 1 LOP3
+            a[i] = a[i] * 3u + b;             // 1 IMAD
+        }
+    }
+    uint32_t r = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) r ^= a[i];
+    if (r == 0x9e3779b9u) sink[0] = r;
+}
+
+extern "C" int gts_bench_int_peak(double *ops_per_s, void *stream)
+{
+    ABI_BEGIN
+    cudaStream_t st = (cudaStream_t)stream;
+    int dev = 0, sms = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    DBuf<uint32_t> sink(1, st);
+    const int iters = 4096, block = 256, blocks = sms * 8;
+    k_int_peak<<<blocks, block, 0, st>>>(1u, 64, sink.p);   // warm-up
+    LAUNCH_CHECK();
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    CK(cudaEventRecord(a, st));
+    k_int_peak<<<blocks, block, 0, st>>>(1u, iters, sink.p);
+    LAUNCH_CHECK();
+    CK(cudaEventRecord(b, st));
+    CK(cudaEventSynchronize(b));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    const double ops = (double)blocks * block * iters * 8 * 2;
+    *ops_per_s = ops / (ms * 1e-3);
+    return GTS_OK;
+    ABI_END
+}
+
 extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int device, gts_index **out)
 {
     ABI_BEGIN
@@ -1067,7 +1653,29 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
         if (n == 0 || t->levels == 0) { *out = ix; return GTS_OK; }
         // inverse permutation: table position of each dataset row
         std::vector<int32_t> tpos((size_t)n);
-        for (int64_t e = 0; e < n; e++) tpos[(size_t)t->rows[e]] = (int32_t)e;
+        // Device table order: the reference table order, except that string
+        // entries are stably sorted by length inside each leaf (leaves are
+        // scanned, never ordered, search.py:518-524), so DP lanes of a warp
+        // see similar lengths.  ord[e] = reference position of device entry e.
+        std::vector<int64_t> ord((size_t)n);
+        for (int64_t e = 0; e < n; e++) ord[(size_t)e] = e;
+        if (ds->metric == GTS_EDIT) {
+            __int128 c = 1;
+            for (int l = 1; l < ix->levels; l++) c *= ix->nc;
+            const int64_t lfirst = (int64_t)((c - 1) / (ix->nc - 1) + 1), lcount = (int64_t)c;
+            for (int64_t i = lfirst; i < lfirst + lcount; i++) {
+                const int64_t p0 = t->pos[i], sz = t->size[i];
+                if (sz <= 1) continue;
+                std::stable_sort(ord.begin() + p0, ord.begin() + p0 + sz, [&](int64_t a, int64_t b) {
+                    const int64_t ra = t->rows[a], rb = t->rows[b];
+                    return ds->offsets[ra + 1] - ds->offsets[ra] < ds->offsets[rb + 1] - ds->offsets[rb];
+                });
+            }
+        }
+        std::vector<int64_t> drow((size_t)n);
+        for (int64_t e = 0; e < n; e++) drow[(size_t)e] = t->rows[ord[(size_t)e]];
+        ix->ord = ord;
+        for (int64_t e = 0; e < n; e++) tpos[(size_t)drow[(size_t)e]] = (int32_t)e;
         std::vector<NodeRec> nodes((size_t)t->nodes + 1);
         std::vector<int32_t> npos((size_t)t->nodes + 1);
         for (int64_t i = 0; i <= t->nodes; i++) {
@@ -1096,14 +1704,22 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
             ix->n_live_leaves = (int)lv.size();
             ix->live_leaves.alloc(std::max<size_t>(lv.size(), 1), st);
             h2d(ix->live_leaves.p, lv.data(), lv.size(), st);
+            for (int64_t i = first; i < first + count; i++) ix->max_leaf = std::max<int>(ix->max_leaf, (int)t->size[i]);
+        }
+        {
+            std::vector<int32_t> row((size_t)n);
+            for (int64_t e = 0; e < n; e++) row[(size_t)e] = (int32_t)drow[(size_t)e];
+            ix->row.alloc((size_t)n, st);
+            h2d(ix->row.p, row.data(), (size_t)n, st);
         }
         std::vector<float> dis((size_t)n);
         std::vector<int64_t> ids((size_t)n);
         std::vector<uint32_t> alive((size_t)((n + 31) / 32), 0u);
         for (int64_t e = 0; e < n; e++) {
-            dis[(size_t)e] = (float)t->dis[e];
-            ids[(size_t)e] = ds->ids[t->rows[e]];
-            if (!t->tombstone || t->tombstone[e] == 0) alive[(size_t)(e >> 5)] |= 1u << (e & 31);
+            const int64_t o = ord[(size_t)e];
+            dis[(size_t)e] = (float)t->dis[o];
+            ids[(size_t)e] = ds->ids[drow[(size_t)e]];
+            if (!t->tombstone || t->tombstone[o] == 0) alive[(size_t)(e >> 5)] |= 1u << (e & 31);
         }
         ix->dis.alloc((size_t)n, st);
         h2d(ix->dis.p, dis.data(), (size_t)n, st);
@@ -1120,25 +1736,21 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
                 fail(GTS_EMETRIC, "string alphabet of %zu symbols exceeds the device's 254", alpha.size());
             ix->A = (int)alpha.size();
             ix->h_alpha = alpha;
-            std::vector<int64_t> soff((size_t)n + 1, 0);
-            for (int64_t e = 0; e < n; e++) {
-                int64_t r = t->rows[e];
-                int64_t len = ds->offsets[r + 1] - ds->offsets[r];
-                ix->max_len = std::max<int>(ix->max_len, (int)len);
-                soff[(size_t)e + 1] = soff[(size_t)e] + len;
-            }
-            std::vector<uint8_t> sym((size_t)std::max<int64_t>(soff[(size_t)n], 1));
-            for (int64_t e = 0; e < n; e++) {
-                int64_t r = t->rows[e];
-                for (int64_t k = ds->offsets[r], o = soff[(size_t)e]; k < ds->offsets[r + 1]; k++, o++)
-                    sym[(size_t)o] = (uint8_t)(std::lower_bound(alpha.begin(), alpha.end(), ds->codes[k]) - alpha.begin());
-            }
+            std::vector<uint32_t> words, wstart;
+            std::vector<int32_t> lens;
+            auto symof = [&](int64_t k) {
+                return (uint32_t)(std::lower_bound(alpha.begin(), alpha.end(), ds->codes[k]) - alpha.begin());
+            };
+            pack_words(n, ds->offsets, symof, words, wstart, lens, drow.data());
+            for (auto l : lens) ix->max_len = std::max<int>(ix->max_len, l);
             ix->alpha.alloc(std::max<size_t>(alpha.size(), 1), st);
             h2d(ix->alpha.p, alpha.data(), alpha.size(), st);
-            ix->soff.alloc(soff.size(), st);
-            h2d(ix->soff.p, soff.data(), soff.size(), st);
-            ix->str.alloc(sym.size(), st);
-            h2d(ix->str.p, sym.data(), sym.size(), st);
+            ix->str.alloc(words.size(), st);
+            h2d(ix->str.p, words.data(), words.size(), st);
+            ix->sword.alloc(wstart.size(), st);
+            h2d(ix->sword.p, wstart.data(), wstart.size(), st);
+            ix->slen.alloc(lens.size(), st);
+            h2d(ix->slen.p, lens.data(), lens.size(), st);
         } else {
             ix->D = (int)ds->dim;
             ix->Dp = (ix->D + 3) & ~3;
@@ -1146,7 +1758,7 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
             bool exact = true;
             float mx = 0.f;
             for (int64_t e = 0; e < n; e++) {
-                const double *src = ds->vectors + t->rows[e] * ix->D;
+                const double *src = ds->vectors + drow[(size_t)e] * ix->D;
                 for (int d = 0; d < ix->D; d++) {
                     float f = (float)src[d];
                     if ((double)f != src[d]) exact = false;
@@ -1161,7 +1773,7 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
             if (!exact) {
                 std::vector<double> v64((size_t)(n * ix->D));
                 for (int64_t e = 0; e < n; e++)
-                    std::memcpy(v64.data() + e * ix->D, ds->vectors + t->rows[e] * ix->D, sizeof(double) * ix->D);
+                    std::memcpy(v64.data() + e * ix->D, ds->vectors + drow[(size_t)e] * ix->D, sizeof(double) * ix->D);
                 ix->vec64.alloc(v64.size(), st);
                 h2d(ix->vec64.p, v64.data(), v64.size(), st);
             }
@@ -1196,7 +1808,7 @@ extern "C" int gts_index_set_tombstones(gts_index *ix, const uint8_t *tomb, void
     CK(cudaSetDevice(ix->device));
     std::vector<uint32_t> alive((size_t)((ix->n + 31) / 32), 0u);
     for (int64_t e = 0; e < ix->n; e++)
-        if (tomb[e] == 0) alive[(size_t)(e >> 5)] |= 1u << (e & 31);
+        if (tomb[ix->ord[(size_t)e]] == 0) alive[(size_t)(e >> 5)] |= 1u << (e & 31);
     cudaStream_t st = (cudaStream_t)stream;
     h2d(ix->alive.p, alive.data(), alive.size(), st);
     CK(cudaStreamSynchronize(st));
@@ -1364,9 +1976,18 @@ extern "C" int gts_pair_distances(int32_t metric, int64_t np, int64_t dim, const
     DBuf<int32_t> ca((size_t)std::max<int64_t>(na, 1), st), cb((size_t)std::max<int64_t>(nb, 1), st);
     h2d(ca.p, a_codes, (size_t)na, st);
     h2d(cb.p, b_codes, (size_t)nb, st);
-    DBuf<uint8_t> sa((size_t)std::max<int64_t>(na, 1), st), sb((size_t)std::max<int64_t>(nb, 1), st);
+    DBuf<uint8_t> sa((size_t)std::max<int64_t>(na, 1), st);
     if (na) { k_map_symbols<<<grid_for(na, 256), 256, 0, st>>>(ca.p, na, dalpha.p, A, sa.p); LAUNCH_CHECK(); }
-    if (nb) { k_map_symbols<<<grid_for(nb, 256), 256, 0, st>>>(cb.p, nb, dalpha.p, A, sb.p); LAUNCH_CHECK(); }
+    std::vector<uint32_t> bw, bstart;
+    std::vector<int32_t> blen;
+    pack_words(np, b_off, [&](int64_t k) {
+        return (uint32_t)(std::lower_bound(alpha.begin(), alpha.end(), b_codes[k]) - alpha.begin());
+    }, bw, bstart, blen);
+    DBuf<uint32_t> dbw(bw.size(), st), dbs(bstart.size(), st);
+    DBuf<int32_t> dbl(blen.size(), st);
+    h2d(dbw.p, bw.data(), bw.size(), st);
+    h2d(dbs.p, bstart.data(), bstart.size(), st);
+    h2d(dbl.p, blen.data(), blen.size(), st);
     DBuf<int64_t> aoff((size_t)np + 1, st), boff((size_t)np + 1, st), poff((size_t)np + 1, st);
     h2d(aoff.p, a_off, (size_t)np + 1, st);
     h2d(boff.p, b_off, (size_t)np + 1, st);
@@ -1384,7 +2005,7 @@ extern "C" int gts_pair_distances(int32_t metric, int64_t np, int64_t dim, const
     qa.peq_off = poff.p;
     qa.A = A;
     DBuf<double> o((size_t)np, st);
-    k_pair_edit<<<grid_for(np, 128), 128, 0, st>>>(np, sb.p, boff.p, qa, o.p);
+    k_pair_edit<<<grid_for(np, 128), 128, 0, st>>>(np, dbw.p, dbs.p, dbl.p, qa, o.p);
     LAUNCH_CHECK();
     CK(cudaMemcpyAsync(out, o.p, sizeof(double) * np, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));

@@ -41,8 +41,10 @@ struct IndexView {
     const uint32_t *alive;
     const float *vec32;
     const double *vec64;   // may be null (fp32-exact data: widen vec32)
-    const uint8_t *str;
-    const int64_t *soff;
+    const uint32_t *str;     // dense symbols, 4 per word, each object 4-byte aligned
+    const uint32_t *sword;   // [n] first word of each entry's symbols
+    const int32_t *slen;     // [n] symbols per entry
+    const int32_t *row;      // [n] dataset row of each entry (row order = id order)
     int D, Dp, nc, levels;
     float rel, abs_eps;    // fp32 slack model (vectors); 0 for edit
 };
@@ -74,88 +76,120 @@ __device__ __forceinline__ bool is_alive(const uint32_t *alive, int e)
 
 // ---------------------------------------------------------------------------
 // edit distance: Myers/Hyyro block bit-vector recurrence, pattern = query
-// (match masks precomputed per query), text = stored object.  Returns the
-// same integer as the reference DP (metrics.py:54-84).
+// (match masks Peq[A][W] precomputed per query), text = stored object
+// (dense symbols, 4 per 32-bit word, 4-byte aligned).  The horizontal carry
+// between 32-bit blocks travels as two bits (hp: +1, hm: -1); the score is
+// read off the final column, D[m][n] = n + popc(Pv) - popc(Mv), so the loop
+// carries no per-column score.  Same integer as the reference DP
+// (metrics.py:54-84).
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ void myers_step1(uint32_t Eq, uint32_t &Pv, uint32_t &Mv)
+{
+    // single block: the top boundary row adds +1 per column (hin = +1)
+    const uint32_t Xv = Eq | Mv;
+    const uint32_t Xh = (((Eq & Pv) + Pv) ^ Pv) | Eq;
+    uint32_t Ph = Mv | ~(Xh | Pv);
+    uint32_t Mh = Pv & Xh;
+    Ph = (Ph << 1) | 1u;
+    Mh = Mh << 1;
+    Pv = Mh | ~(Xv | Ph);
+    Mv = Ph & Xv;
+}
+
+__device__ __forceinline__ void myers_stepb(uint32_t Eq, uint32_t &Pv, uint32_t &Mv, uint32_t &hp, uint32_t &hm)
+{
+    const uint32_t Xv = Eq | Mv;
+    Eq |= hm;
+    const uint32_t Xh = (((Eq & Pv) + Pv) ^ Pv) | Eq;
+    uint32_t Ph = Mv | ~(Xh | Pv);
+    uint32_t Mh = Pv & Xh;
+    const uint32_t op = Ph >> 31, om = Mh >> 31;
+    Ph = (Ph << 1) | hp;
+    Mh = (Mh << 1) | hm;
+    Pv = Mh | ~(Xv | Ph);
+    Mv = Ph & Xv;
+    hp = op;
+    hm = om;
+}
+
 template <int W>
-__device__ __forceinline__ int myers_fixed(const uint32_t *__restrict__ peq, int m,
-                                           const uint8_t *__restrict__ t, int n)
+__device__ __forceinline__ void myers_char(const uint32_t *peq, uint32_t c, uint32_t (&P)[W], uint32_t (&M)[W])
+{
+    if (W == 1) {
+        myers_step1(peq[c], P[0], M[0]);
+    } else {
+        uint32_t hp = 1u, hm = 0u;
+#pragma unroll
+        for (int b = 0; b < W; b++) myers_stepb(peq[c * W + b], P[b], M[b], hp, hm);
+    }
+}
+
+// peq: [A][W] masks of the query (shared or global); t4: text words.
+// Full words are unrolled four symbols at a time; the tail word is last.
+template <int W>
+__device__ __forceinline__ int myers_fixed(const uint32_t *peq, int m, const uint32_t *__restrict__ t4, int n)
 {
     uint32_t P[W], M[W];
 #pragma unroll
     for (int b = 0; b < W; b++) { P[b] = ~0u; M[b] = 0u; }
-    const uint32_t last = 1u << ((m - 1) & 31);
-    int score = m;
-    for (int j = 0; j < n; j++) {
-        const uint32_t *eq = peq + (int)__ldg(t + j) * W;
-        int hin = 1;
+    const int nfull = n >> 2;
+    for (int jw = 0; jw < nfull; jw++) {
+        const uint32_t w = __ldg(t4 + jw);
+        myers_char<W>(peq, w & 0xffu, P, M);
+        myers_char<W>(peq, (w >> 8) & 0xffu, P, M);
+        myers_char<W>(peq, (w >> 16) & 0xffu, P, M);
+        myers_char<W>(peq, w >> 24, P, M);
+    }
+    const int rem = n & 3;
+    if (rem) {
+        const uint32_t w = __ldg(t4 + nfull);
+        myers_char<W>(peq, w & 0xffu, P, M);
+        if (rem > 1) myers_char<W>(peq, (w >> 8) & 0xffu, P, M);
+        if (rem > 2) myers_char<W>(peq, (w >> 16) & 0xffu, P, M);
+    }
+    const uint32_t lastmask = (m & 31) ? ((1u << (m & 31)) - 1u) : ~0u;
+    int score = n;
 #pragma unroll
-        for (int b = 0; b < W; b++) {
-            uint32_t Eq = __ldg(eq + b), Pv = P[b], Mv = M[b];
-            uint32_t Xv = Eq | Mv;
-            if (hin < 0) Eq |= 1u;
-            uint32_t Xh = (((Eq & Pv) + Pv) ^ Pv) | Eq;
-            uint32_t Ph = Mv | ~(Xh | Pv);
-            uint32_t Mh = Pv & Xh;
-            const uint32_t hb = (b == W - 1) ? last : 0x80000000u;
-            int hout = (Ph & hb) ? 1 : ((Mh & hb) ? -1 : 0);
-            Ph = (Ph << 1) | (uint32_t)(hin > 0);
-            Mh = (Mh << 1) | (uint32_t)(hin < 0);
-            P[b] = Mh | ~(Xv | Ph);
-            M[b] = Ph & Xv;
-            hin = hout;
-        }
-        score += hin;
+    for (int b = 0; b < W; b++) {
+        const uint32_t mk = (b == W - 1) ? lastmask : ~0u;
+        score += __popc(P[b] & mk) - __popc(M[b] & mk);
     }
     return score;
 }
 
-__device__ __noinline__ int myers_generic(const uint32_t *__restrict__ peq, int W, int m,
-                                          const uint8_t *__restrict__ t, int n)
+__device__ __noinline__ int myers_generic(const uint32_t *peq, int W, int m, const uint32_t *__restrict__ t4, int n)
 {
     uint32_t P[kMaxWords], M[kMaxWords];
     for (int b = 0; b < W; b++) { P[b] = ~0u; M[b] = 0u; }
-    const uint32_t last = 1u << ((m - 1) & 31);
-    int score = m;
     for (int j = 0; j < n; j++) {
-        const uint32_t *eq = peq + (int)t[j] * W;
-        int hin = 1;
-        for (int b = 0; b < W; b++) {
-            uint32_t Eq = eq[b], Pv = P[b], Mv = M[b];
-            uint32_t Xv = Eq | Mv;
-            if (hin < 0) Eq |= 1u;
-            uint32_t Xh = (((Eq & Pv) + Pv) ^ Pv) | Eq;
-            uint32_t Ph = Mv | ~(Xh | Pv);
-            uint32_t Mh = Pv & Xh;
-            const uint32_t hb = (b == W - 1) ? last : 0x80000000u;
-            int hout = (Ph & hb) ? 1 : ((Mh & hb) ? -1 : 0);
-            Ph = (Ph << 1) | (uint32_t)(hin > 0);
-            Mh = (Mh << 1) | (uint32_t)(hin < 0);
-            P[b] = Mh | ~(Xv | Ph);
-            M[b] = Ph & Xv;
-            hin = hout;
-        }
-        score += hin;
+        const uint32_t c = (__ldg(t4 + (j >> 2)) >> (8 * (j & 3))) & 0xffu;
+        uint32_t hp = 1u, hm = 0u;
+        for (int b = 0; b < W; b++) myers_stepb(peq[c * W + b], P[b], M[b], hp, hm);
+    }
+    const uint32_t lastmask = (m & 31) ? ((1u << (m & 31)) - 1u) : ~0u;
+    int score = n;
+    for (int b = 0; b < W; b++) {
+        const uint32_t mk = (b == W - 1) ? lastmask : ~0u;
+        score += __popc(P[b] & mk) - __popc(M[b] & mk);
     }
     return score;
 }
 
-__device__ __forceinline__ int edit_qt(const QueryView &qv, int q, const uint8_t *t, int n)
+// edit distance between pattern (m symbols, masks peq) and text (n symbols)
+__device__ __forceinline__ int edit_peq(const uint32_t *peq, int m, const uint32_t *t4, int n)
 {
-    const int64_t qo = qv.soff[q];
-    const int m = (int)(qv.soff[q + 1] - qo);
     if (m == 0) return n;
     if (n == 0) return m;
-    const uint32_t *peq = qv.peq + qv.peq_off[q];
-    const int W = (m + 31) >> 5;
-    switch (W) {
-    case 1: return myers_fixed<1>(peq, m, t, n);
-    case 2: return myers_fixed<2>(peq, m, t, n);
-    case 3: return myers_fixed<3>(peq, m, t, n);
-    case 4: return myers_fixed<4>(peq, m, t, n);
-    default: return myers_generic(peq, W, m, t, n);
+    switch ((m + 31) >> 5) {
+    case 1: return myers_fixed<1>(peq, m, t4, n);
+    case 2: return myers_fixed<2>(peq, m, t4, n);
+    case 3: return myers_fixed<3>(peq, m, t4, n);
+    case 4: return myers_fixed<4>(peq, m, t4, n);
+    default: return myers_generic(peq, (m + 31) >> 5, m, t4, n);
     }
 }
+
+__device__ __forceinline__ int qlen(const QueryView &qv, int q) { return (int)(qv.soff[q + 1] - qv.soff[q]); }
 
 // ---------------------------------------------------------------------------
 // vectors: fp32 screening distance (float4 loads) and the exact float64
@@ -227,17 +261,18 @@ template <int MET>
 __device__ __forceinline__ float dist32(const IndexView &ix, const QueryView &qv, int q, int e)
 {
     if (MET == kMetricEdit) {
-        const int64_t o = ix.soff[e];
-        return (float)edit_qt(qv, q, ix.str + o, (int)(ix.soff[e + 1] - o));
+        return (float)edit_peq(qv.peq + qv.peq_off[q], qlen(qv, q), ix.str + ix.sword[e], ix.slen[e]);
     } else {
         return vdist32<MET>(ix.vec32 + (size_t)e * ix.Dp, qv.vec32 + (size_t)q * ix.Dp, ix.Dp);
     }
 }
 
-// fp32 error slack for comparisons involving magnitudes a and b
-__device__ __forceinline__ float slack(const IndexView &ix, float a, float b)
+// fp32 error slack for comparisons involving magnitudes a, b (and c);
+// exact metrics (rel == 0) never touch the magnitudes, so an infinite
+// radius cannot turn the slack into NaN.
+__device__ __forceinline__ float slack(const IndexView &ix, float a, float b, float c = 0.f)
 {
-    return ix.rel * (fabsf(a) + fabsf(b)) + ix.abs_eps;
+    return ix.rel > 0.f ? ix.rel * (fabsf(a) + fabsf(b) + fabsf(c)) + ix.abs_eps : ix.abs_eps;
 }
 
 }  // namespace gts
