@@ -459,10 +459,12 @@ __global__ void __launch_bounds__(256, 4) k_leaf_edit(IndexView ix, QueryView qv
                                                       unsigned long long *work, unsigned long long *cursor)
 {
     __shared__ uint32_t peq_s[kLeafWarps][kWarpPeqWords];
-    __shared__ int32_t queue[kLeafWarps][64];
+    __shared__ int32_t queue[kLeafWarps][3][64];   // entry, first text word, length
     const int lane = lane_id(), wib = threadIdx.x >> 5;
     uint32_t *peq_w = peq_s[wib];
-    int32_t *qu = queue[wib];
+    int32_t *qu = queue[wib][0];
+    int32_t *qw = queue[wib][1];
+    int32_t *ql = queue[wib][2];
     int cur_q = -1, mq = 0, qn = 0;
     unsigned long long nrows = 0;
     float r = 0.f;
@@ -476,8 +478,8 @@ __global__ void __launch_bounds__(256, 4) k_leaf_edit(IndexView ix, QueryView qv
         int d = 0, e = -1;
         if (lane < cnt) {
             e = qu[lane];
-            const int n = __ldg(ix.slen + e);
-            const uint32_t *txt = ix.str + __ldg(ix.sword + e);
+            const int n = ql[lane];
+            const uint32_t *txt = ix.str + (uint32_t)qw[lane];
             if (staged) d = edit_peq(peq_w, mq, txt, n);
             else d = edit_peq_global(peq_g, mq, txt, n);
             hit = (float)d <= r;
@@ -503,8 +505,21 @@ __global__ void __launch_bounds__(256, 4) k_leaf_edit(IndexView ix, QueryView qv
         if ((int64_t)start >= m) break;
         const int64_t stop = min(m, (int64_t)start + kRowChunk);
         nrows += (unsigned long long)(stop - (int64_t)start);
+        // lanes fetch the chunk's row and leaf records in one parallel batch
+        Row pr{0, 0, 0.f, 0};
+        NodeRec pn{0.f, 0.f, 0, 0};
+        int ppos = 0;
+        if ((int64_t)start + lane < stop) {
+            pr = rows[start + lane];
+            pn = ix.node[pr.node];
+            ppos = ix.npos[pr.node];
+        }
     for (int64_t w = (int64_t)start; w < stop; w++) {
-        const Row lr = rows[w];
+        const int src = (int)(w - (int64_t)start);
+        Row lr;
+        lr.q = __shfl_sync(kFull, pr.q, src);
+        lr.node = __shfl_sync(kFull, pr.node, src);
+        lr.dqp = __shfl_sync(kFull, pr.dqp, src);
         if (lr.q != cur_q) {
             if (qn) { run_batch(qn); qn = 0; }
             cur_q = lr.q;
@@ -518,8 +533,9 @@ __global__ void __launch_bounds__(256, 4) k_leaf_edit(IndexView ix, QueryView qv
             }
             __syncwarp();
         }
-        const NodeRec leaf = ix.node[lr.node];
-        const int pos = ix.npos[lr.node];
+        NodeRec leaf;
+        leaf.size = __shfl_sync(kFull, pn.size, src);
+        const int pos = __shfl_sync(kFull, ppos, src);
         unsigned ver = 0;
         for (int b = 0; b < leaf.size; b += kWarp) {
             const int k = b + lane;
@@ -528,15 +544,22 @@ __global__ void __launch_bounds__(256, 4) k_leaf_edit(IndexView ix, QueryView qv
             if (k < leaf.size && is_alive(ix.alive, e))
                 pass = !pruning || fabsf(__ldg(ix.dis + e) - lr.dqp) <= r;
             ver += __popc(__ballot_sync(kFull, pass));
-            const bool cand = pass && (float)abs(mq - __ldg(ix.slen + e)) <= r;
+            int len = 0;
+            if (pass) len = __ldg(ix.slen + e);
+            const bool cand = pass && (float)abs(mq - len) <= r;
             const unsigned cb = __ballot_sync(kFull, cand);
-            if (cand) qu[qn + __popc(cb & ((1u << lane) - 1u))] = e;
+            if (cand) {
+                const int slot = qn + __popc(cb & ((1u << lane) - 1u));
+                qu[slot] = e;
+                qw[slot] = (int32_t)__ldg(ix.sword + e);
+                ql[slot] = len;
+            }
             qn += __popc(cb);
             __syncwarp();
             if (qn >= kWarp) {
                 run_batch(kWarp);
                 qn -= kWarp;
-                if (lane < qn) qu[lane] = qu[kWarp + lane];
+                if (lane < qn) { qu[lane] = qu[kWarp + lane]; qw[lane] = qw[kWarp + lane]; ql[lane] = ql[kWarp + lane]; }
                 __syncwarp();
             }
         }
@@ -856,7 +879,7 @@ using namespace gts;
 
 namespace gts {
 // Pack strings (dense symbols, given per string as a code range mapped by
-// `sym`) 4 per 32-bit word, each string starting on a word boundary.
+// `sym`) 4 per 32-bit word, each string starting on a 16-byte boundary.
 template <class SymOf>
 static void pack_words(int64_t n, const int64_t *off, SymOf sym, std::vector<uint32_t> &words,
                        std::vector<uint32_t> &wstart, std::vector<int32_t> &len, const int64_t *order = nullptr)
@@ -869,10 +892,11 @@ static void pack_words(int64_t n, const int64_t *off, SymOf sym, std::vector<uin
         const int64_t l = off[r + 1] - off[r];
         wstart[(size_t)e] = (uint32_t)w;
         len[(size_t)e] = (int32_t)l;
-        w += (uint64_t)((l + 3) / 4);
+        w += (uint64_t)((l + 15) / 16) * 4;    // 16-byte aligned objects
     }
+    w += 8;                                    // the DP prefetches one uint4 past an object
     if (w >= (1ull << 32)) fail(GTS_EINVAL, "string payload exceeds 16 GiB per index; shard it");
-    words.assign((size_t)std::max<uint64_t>(w, 1), 0u);
+    words.assign((size_t)w, 0u);
     for (int64_t e = 0; e < n; e++) {
         const int64_t r = order ? order[e] : e;
         uint32_t *dst = words.data() + wstart[(size_t)e];
@@ -906,6 +930,7 @@ struct gts_index {
     DBuf<int32_t> alpha;
     int max_leaf = 0;
     std::vector<int64_t> ord;   // device entry -> reference table position
+    std::atomic<unsigned long long> hit_hint[2] = {{0}, {0}};   // hits of the last range / kNN call
     DBuf<int32_t> live_leaves;
     int n_live_leaves = 0;
     std::vector<int32_t> h_alpha;
@@ -1084,6 +1109,7 @@ struct Search {
             CK(cudaMemsetAsync(work.p, 0, 4 * sizeof(unsigned long long), st));
         }
         size_t hcap = (size_t)std::max<int64_t>(1 << 16, nq * 16);
+        hcap = std::max<size_t>(hcap, (size_t)ix->hit_hint[mode].load());
         hq.alloc(hcap, st);
         he.alloc(hcap, st);
         hd.alloc(hcap, st);
@@ -1517,6 +1543,11 @@ gts_result *run_search(gts_index *ix, const gts_queries *q, int mode, const doub
         }
     }
     s.run();
+    {
+        const unsigned long long want = s.hits + s.hits / 4;
+        unsigned long long cur = ix->hit_hint[mode].load();
+        while (want > cur && !ix->hit_hint[mode].compare_exchange_weak(cur, want)) {}
+    }
     auto *res = new gts_result();
     try {
         s.collect(res);
@@ -1574,10 +1605,11 @@ extern "C" int gts_profile_read(char *buf, int64_t cap, int reset)
     return GTS_OK;
 }
 
-// Integer-pipe peak microbenchmark: 8 independent chains per thread mixing
-// LOP3 (alu pipe) and IMAD (fma pipe) -- the two pipes the bit-parallel edit
-// kernel issues to.  Returns executed int ops per second.
-__global__ void k_int_peak(uint32_t seed, int iters, uint32_t *sink)
+// Integer peak microbenchmark: 8 independent chains per thread, each one
+// LOP3 (alu pipe) + one IMAD (fma pipe) -- the two pipes the bit-parallel
+// edit kernel issues to -- so the measured rate is the issue-limited
+// integer throughput (SASS checked: 1 LOP3 + 1 IMAD per chain step).
+__global__ void k_int_peak(uint32_t seed, uint32_t mul, int iters, uint32_t *sink)
 {
     uint32_t a[8];
 #pragma unroll
@@ -1586,8 +1618,8 @@ __global__ void k_int_peak(uint32_t seed, int iters, uint32_t *sink)
     for (int it = 0; it < iters; it++) {
 #pragma unroll
         for (int i = 0; i < 8; i++) {
-            a[i] = (a[i] ^ b) & (a[i] | c);   // 1 LOP3
-            a[i] = a[i] * 3u + b;             // 1 IMAD
+            a[i] = (a[i] ^ b) | c;            // 1 LOP3 (alu pipe)
+            a[i] = a[i] * mul + b;            // 1 IMAD (fma pipe; runtime multiplier)
         }
     }
     uint32_t r = 0;
@@ -1605,13 +1637,13 @@ extern "C" int gts_bench_int_peak(double *ops_per_s, void *stream)
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     DBuf<uint32_t> sink(1, st);
     const int iters = 4096, block = 256, blocks = sms * 8;
-    k_int_peak<<<blocks, block, 0, st>>>(1u, 64, sink.p);   // warm-up
+    k_int_peak<<<blocks, block, 0, st>>>(1u, 0x9e3779b1u, 64, sink.p);   // warm-up
     LAUNCH_CHECK();
     cudaEvent_t a, b;
     CK(cudaEventCreate(&a));
     CK(cudaEventCreate(&b));
     CK(cudaEventRecord(a, st));
-    k_int_peak<<<blocks, block, 0, st>>>(1u, iters, sink.p);
+    k_int_peak<<<blocks, block, 0, st>>>(1u, 0x9e3779b1u, iters, sink.p);
     LAUNCH_CHECK();
     CK(cudaEventRecord(b, st));
     CK(cudaEventSynchronize(b));

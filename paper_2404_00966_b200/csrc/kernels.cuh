@@ -85,15 +85,16 @@ __device__ __forceinline__ bool is_alive(const uint32_t *alive, int e)
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void myers_step1(uint32_t Eq, uint32_t &Pv, uint32_t &Mv)
 {
-    // single block: the top boundary row adds +1 per column (hin = +1)
-    const uint32_t Xv = Eq | Mv;
-    const uint32_t Xh = (((Eq & Pv) + Pv) ^ Pv) | Eq;
-    uint32_t Ph = Mv | ~(Xh | Pv);
-    uint32_t Mh = Pv & Xh;
-    Ph = (Ph << 1) | 1u;
-    Mh = Mh << 1;
-    Pv = Mh | ~(Xv | Ph);
-    Mv = Ph & Xv;
+    // single block, top boundary row +1 per column.  Hyyro's form: with
+    // X = Eq | Mv, D0 = (((X & Pv) + Pv) ^ Pv) | X (Pv & Mv == 0 makes it
+    // the textbook Xh | Mv), 10 integer ops per text symbol.
+    const uint32_t X = Eq | Mv;
+    const uint32_t D0 = (((X & Pv) + Pv) ^ Pv) | X;
+    const uint32_t HN = Pv & D0;
+    const uint32_t HP = Mv | ~(Pv | D0);
+    const uint32_t Xs = (HP << 1) | 1u;
+    Mv = Xs & D0;
+    Pv = (HN << 1) | ~(Xs | D0);
 }
 
 __device__ __forceinline__ void myers_stepb(uint32_t Eq, uint32_t &Pv, uint32_t &Mv, uint32_t &hp, uint32_t &hm)
@@ -124,8 +125,18 @@ __device__ __forceinline__ void myers_char(const uint32_t *peq, uint32_t c, uint
     }
 }
 
-// peq: [A][W] masks of the query (shared or global); t4: text words.
-// Full words are unrolled four symbols at a time; the tail word is last.
+// peq: [A][W] masks of the query (shared or global); t4: text (storage is
+// padded, so reading one word past the end is safe).  Four symbols per
+// 32-bit word, unrolled; the next word is loaded while this one computes.
+template <int W>
+__device__ __forceinline__ void myers_word(const uint32_t *peq, uint32_t w, uint32_t (&P)[W], uint32_t (&M)[W])
+{
+    myers_char<W>(peq, w & 0xffu, P, M);
+    myers_char<W>(peq, (w >> 8) & 0xffu, P, M);
+    myers_char<W>(peq, (w >> 16) & 0xffu, P, M);
+    myers_char<W>(peq, w >> 24, P, M);
+}
+
 template <int W>
 __device__ __forceinline__ int myers_fixed(const uint32_t *peq, int m, const uint32_t *__restrict__ t4, int n)
 {
@@ -133,16 +144,14 @@ __device__ __forceinline__ int myers_fixed(const uint32_t *peq, int m, const uin
 #pragma unroll
     for (int b = 0; b < W; b++) { P[b] = ~0u; M[b] = 0u; }
     const int nfull = n >> 2;
+    uint32_t w = __ldg(t4);
     for (int jw = 0; jw < nfull; jw++) {
-        const uint32_t w = __ldg(t4 + jw);
-        myers_char<W>(peq, w & 0xffu, P, M);
-        myers_char<W>(peq, (w >> 8) & 0xffu, P, M);
-        myers_char<W>(peq, (w >> 16) & 0xffu, P, M);
-        myers_char<W>(peq, w >> 24, P, M);
+        const uint32_t nxt = __ldg(t4 + jw + 1);
+        myers_word<W>(peq, w, P, M);
+        w = nxt;
     }
     const int rem = n & 3;
     if (rem) {
-        const uint32_t w = __ldg(t4 + nfull);
         myers_char<W>(peq, w & 0xffu, P, M);
         if (rem > 1) myers_char<W>(peq, (w >> 8) & 0xffu, P, M);
         if (rem > 2) myers_char<W>(peq, (w >> 16) & 0xffu, P, M);
