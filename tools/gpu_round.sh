@@ -11,6 +11,6 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $o
 (timeout 1200 python bench.py 2>&1 | tail -3) > $out/bench_words_$tag.json
 (timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches_words_$tag.csv \
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $out/ncu_launch_stdout_$tag.txt 2>&1)
-(timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_verify_edit -s 6 -c 1 \
+(timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_leaf_edit -s 6 -c 1 \
     -o $out/prof_verify_words_$tag python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $out/ncu_full_stdout_$tag.txt 2>&1)
 ls -la $out

@@ -1,0 +1,111 @@
+#!/usr/bin/env python
+"""Summarise gpurun_out ncu artefacts into a markdown file under profiles/.
+
+    python tools/ncu_summary.py --tag r01d --out profiles/r01_words.md
+
+Reads gpurun_out/launches_words_<tag>.csv (gpu__time_duration launch list,
+cold-cache and serialised: compare shares, not absolutes) and
+gpurun_out/prof_*_<tag>.ncu-rep (one `--set full` capture of the top kernel).
+"""
+
+from __future__ import annotations
+
+import argparse
+import collections
+import csv
+import glob
+import io
+import json
+import os
+import subprocess
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "gpurun_out")
+
+METRICS = [
+    ("gpu__time_duration.sum", "duration (us)"),
+    ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput % of peak"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue slots active %"),
+    ("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "ALU pipe %"),
+    ("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "FMA pipe %"),
+    ("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "LSU pipe %"),
+    ("smsp__thread_inst_executed_per_inst_executed.ratio", "active threads / warp instr"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
+    ("launch__registers_per_thread", "registers / thread"),
+    ("smsp__inst_executed.sum", "warp instructions"),
+    ("dram__bytes_read.sum", "DRAM bytes read"),
+    ("dram__bytes_write.sum", "DRAM bytes written"),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput %"),
+    ("lts__t_sector_hit_rate.pct", "L2 hit rate %"),
+    ("l1tex__t_sector_hit_rate.pct", "L1 hit rate %"),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe %"),
+]
+
+
+def launch_table(path):
+    rows = list(csv.reader(open(path)))
+    hdr = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+    h = rows[hdr]
+    ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    agg = collections.OrderedDict()
+    for r in rows[hdr + 1:]:
+        name = r[ki].split("(")[0].replace("void ", "").strip()
+        v = float(r[vi].replace(",", ""))
+        scale = {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0}[r[ui]]
+        a = agg.setdefault(name, [0, 0.0])
+        a[0] += 1
+        a[1] += v * scale
+    tot = sum(v[1] for v in agg.values())
+    lines = ["| kernel | launches | total ms | share |", "|---|---:|---:|---:|"]
+    for k, (n, ms) in sorted(agg.items(), key=lambda x: -x[1][1])[:14]:
+        lines.append(f"| `{k[:70]}` | {n} | {ms:.3f} | {ms / tot:.3f} |")
+    lines.append(f"| **total** | {sum(v[0] for v in agg.values())} | {tot:.3f} | 1.000 |")
+    return "\n".join(lines)
+
+
+def full_capture(path):
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    r = list(csv.reader(io.StringIO(raw)))
+    h, v = r[0], r[2] if len(r) > 2 else r[1]
+    name = v[h.index("Kernel Name")] if "Kernel Name" in h else "?"
+    lines = [f"kernel: `{name[:120]}`", "", "| metric | value |", "|---|---:|"]
+    for m, label in METRICS:
+        if m in h:
+            lines.append(f"| {label} (`{m}`) | {v[h.index(m)]} |")
+    st = [(x, float(v[h.index(x)])) for x in h
+          if x.startswith("smsp__average_warps_issue_stalled") and x.endswith("per_issue_active.ratio")]
+    lines += ["", "top stall reasons (warps stalled per issued instruction):", "",
+              "| reason | ratio |", "|---|---:|"]
+    for x, y in sorted(st, key=lambda t: -t[1])[:6]:
+        lines.append(f"| {x.replace('smsp__average_warps_issue_stalled_', '').replace('_per_issue_active.ratio', '')} | {y:.3f} |")
+    return "\n".join(lines)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--tag", required=True)
+    ap.add_argument("--workload", default="words")
+    ap.add_argument("--out", required=True)
+    ap.add_argument("--title", default="")
+    a = ap.parse_args()
+    parts = [f"# ncu summary {a.title or a.tag} ({a.workload})", ""]
+    bench = os.path.join(OUT, f"bench_{a.workload}_{a.tag}.json")
+    if os.path.exists(bench):
+        d = json.loads(open(bench).read().strip().splitlines()[-1])
+        d.pop("profile", None)
+        parts += ["## bench line (same box, same build)", "", "```json", json.dumps(d, indent=1), "```", ""]
+    lp = os.path.join(OUT, f"launches_{a.workload}_{a.tag}.csv")
+    if os.path.exists(lp):
+        parts += ["## launch list (ncu --metrics gpu__time_duration.sum --clock-control none; cold, serialised;"
+                  " shares are what to compare)", "", launch_table(lp), ""]
+    for rep in sorted(glob.glob(os.path.join(OUT, f"prof_*{a.workload}*_{a.tag}.ncu-rep"))
+                    + sorted(glob.glob(os.path.join(OUT, f"prof_leaf_{a.tag}.ncu-rep")))):
+        parts += [f"## full capture `{os.path.basename(rep)}` (ncu --set full --clock-control none)", "",
+                  full_capture(rep), ""]
+    os.makedirs(os.path.dirname(os.path.abspath(a.out)), exist_ok=True)
+    open(a.out, "w").write("\n".join(parts))
+    print(a.out)
+
+
+if __name__ == "__main__":
+    main()
