@@ -16,6 +16,8 @@
 // truncation to the k smallest (distance, id) (oracle.py:30-36).
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdlib>
 #include <cfloat>
 #include <cmath>
 #include <cstdarg>
@@ -453,13 +455,16 @@ constexpr int kWarpPeqWords = 1024;     // per-warp staged match masks (A*W <= 1
 // shared memory; every 32 queued entries run as one batch of bit-parallel
 // DPs (one per lane) against the row query's match masks staged in shared
 // memory.  Leaves are length-sorted, so a batch has similar DP lengths.
+constexpr int kHistBins = 256;   // kNN shrinking-bound histogram: exact distances 0..255
+
 __global__ void __launch_bounds__(256, 4) k_leaf_edit(IndexView ix, QueryView qv, const Row *__restrict__ rows,
-                                                      int64_t m, int pruning, const float *__restrict__ r32,
+                                                      int64_t m, int pruning, float *r32,
                                                       HitBuf out, unsigned long long *verified_stat, int stats_on,
-                                                      unsigned long long *work, unsigned long long *cursor)
+                                                      unsigned long long *work, unsigned long long *cursor,
+                                                      unsigned *hist, const int32_t *__restrict__ ks)
 {
     __shared__ uint32_t peq_s[kLeafWarps][kWarpPeqWords];
-    __shared__ int32_t queue[kLeafWarps][3][64];   // entry, first text word, length
+    __shared__ int32_t queue[kLeafWarps][3][96];   // entry, first text word, length
     const int lane = lane_id(), wib = threadIdx.x >> 5;
     uint32_t *peq_w = peq_s[wib];
     int32_t *qu = queue[wib][0];
@@ -467,24 +472,52 @@ __global__ void __launch_bounds__(256, 4) k_leaf_edit(IndexView ix, QueryView qv
     int32_t *ql = queue[wib][2];
     int cur_q = -1, mq = 0, qn = 0;
     unsigned long long nrows = 0;
+    uint4 qh0 = make_uint4(0u, 0u, 0u, 0u), qh1 = qh0;
     float r = 0.f;
     bool staged = false;
     const uint32_t *peq_g = nullptr;
     unsigned long long steps = 0, pairs = 0, entries = 0;
 
-    // run DPs for queue slots [0, cnt) (cnt <= 32), emit hits
-    auto run_batch = [&](int cnt) {
-        bool hit = false;
-        int d = 0, e = -1;
-        if (lane < cnt) {
-            e = qu[lane];
-            const int n = ql[lane];
-            const uint32_t *txt = ix.str + (uint32_t)qw[lane];
-            if (staged) d = edit_peq(peq_w, mq, txt, n);
-            else d = edit_peq_global(peq_g, mq, txt, n);
-            hit = (float)d <= r;
-            steps += (unsigned long long)((mq + 31) >> 5) * (unsigned long long)n;
+    // kNN shrinking bound (hist != null): count every emitted candidate's
+    // exact distance per query; the k-th smallest found so far is an upper
+    // bound on the query's k-th distance, so the radius only ever shrinks
+    // to values that still admit every true answer (and its ties).
+    auto shrink = [&](bool ha, int dA, bool hb2, int dB) {
+        const unsigned any = __ballot_sync(kFull, ha || hb2);
+        if (!hist || !any) return;
+        unsigned *hq_ = hist + (size_t)cur_q * kHistBins;
+        if (ha && dA < kHistBins) atomicAdd(hq_ + dA, 1u);
+        if (hb2 && dB < kHistBins) atomicAdd(hq_ + dB, 1u);
+        __syncwarp();
+        __threadfence_block();
+        // warp prefix over the 256 bins (8 per lane) -> smallest t with count(d <= t) >= k
+        const int kq = ks[cur_q];
+        unsigned c[8], tot = 0;
+#pragma unroll
+        for (int i = 0; i < 8; i++) { c[i] = __ldcg(hq_ + lane * 8 + i); tot += c[i]; }
+        unsigned inc = tot;
+        for (int o = 1; o < 32; o <<= 1) {
+            unsigned v = __shfl_up_sync(kFull, inc, o);
+            if (lane >= o) inc += v;
         }
+        const unsigned before = inc - tot;
+        int t = kHistBins;
+        if (before < (unsigned)kq && inc >= (unsigned)kq) {
+            unsigned run = before;
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                run += c[i];
+                if (run >= (unsigned)kq) { t = lane * 8 + i; break; }
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) t = min(t, __shfl_xor_sync(kFull, t, o));
+        if (t < kHistBins && (float)t < r) {
+            r = (float)t;
+            if (lane == 0) atomicMin(reinterpret_cast<int *>(r32 + cur_q), __float_as_int((float)t));
+        }
+    };
+    // emit one hit per lane (warp-aggregated slot claim)
+    auto emit = [&](bool hit, int e, int d) {
         const unsigned hb = __ballot_sync(kFull, hit);
         if (hb) {
             unsigned long long hbase = 0;
@@ -495,6 +528,39 @@ __global__ void __launch_bounds__(256, 4) k_leaf_edit(IndexView ix, QueryView qv
                 if (sl < out.cap) { out.q[sl] = cur_q; out.e[sl] = e; out.d[sl] = (double)d; }
             }
         }
+    };
+    // run DPs for queue slots [0, cnt) (cnt <= 64): lane takes slots lane
+    // and lane + 32; with a single-word pattern both run interleaved
+    auto run_batch = [&](int cnt) {
+        const bool va = lane < cnt, vb = lane + 32 < cnt;
+        int ea = -1, eb = -1, da = 0, db = 0;
+        if (va) {
+            ea = qu[lane];
+            const int na = ql[lane];
+            const uint32_t *tA = ix.str + (uint32_t)qw[lane];
+            if (vb) {
+                eb = qu[lane + 32];
+                const int nb = ql[lane + 32];
+                const uint32_t *tB = ix.str + (uint32_t)qw[lane + 32];
+                if (staged && mq <= 32) {
+                    myers2_w1(peq_w, mq, tA, na, tB, nb, da, db);
+                } else if (staged) {
+                    da = edit_peq(peq_w, mq, tA, na);
+                    db = edit_peq(peq_w, mq, tB, nb);
+                } else {
+                    da = edit_peq_global(peq_g, mq, tA, na);
+                    db = edit_peq_global(peq_g, mq, tB, nb);
+                }
+                steps += (unsigned long long)((mq + 31) >> 5) * (unsigned long long)nb;
+            } else {
+                da = staged ? edit_peq(peq_w, mq, tA, na) : edit_peq_global(peq_g, mq, tA, na);
+            }
+            steps += (unsigned long long)((mq + 31) >> 5) * (unsigned long long)na;
+        }
+        const bool ha = va && (float)da <= r, hb2 = vb && (float)db <= r;
+        emit(ha, ea, da);
+        emit(hb2, eb, db);
+        shrink(ha, da, hb2, db);
         __syncwarp();
     };
 
@@ -524,7 +590,8 @@ __global__ void __launch_bounds__(256, 4) k_leaf_edit(IndexView ix, QueryView qv
             if (qn) { run_batch(qn); qn = 0; }
             cur_q = lr.q;
             mq = qlen(qv, cur_q);
-            r = r32[cur_q];
+            r = __ldcg(r32 + cur_q);
+            if (ix.ehist) { qh0 = qv.qhist[2 * cur_q]; qh1 = qv.qhist[2 * cur_q + 1]; }
             peq_g = qv.peq + qv.peq_off[cur_q];
             const int words = qv.A * ((mq + 31) >> 5);
             staged = words <= kWarpPeqWords;
@@ -533,33 +600,54 @@ __global__ void __launch_bounds__(256, 4) k_leaf_edit(IndexView ix, QueryView qv
             }
             __syncwarp();
         }
+        if (hist) r = fminf(r, __ldcg(r32 + cur_q));   // another warp may have shrunk it
         NodeRec leaf;
         leaf.size = __shfl_sync(kFull, pn.size, src);
         const int pos = __shfl_sync(kFull, ppos, src);
         unsigned ver = 0;
+        // the chunk's records and alive bits are loaded one chunk ahead
+        uint4 nrec = make_uint4(0u, 0u, 0u, 0u);
+        uint32_t nal = 0u;
+        if (lane < leaf.size) {
+            nrec = __ldg(ix.erec + pos + lane);
+            nal = __ldg(ix.alive + ((pos + lane) >> 5));
+        }
         for (int b = 0; b < leaf.size; b += kWarp) {
             const int k = b + lane;
             const int e = pos + k;
+            const uint4 rec = nrec;
+            const uint32_t al = nal;
+            if (b + kWarp + lane < leaf.size) {
+                nrec = __ldg(ix.erec + e + kWarp);
+                nal = __ldg(ix.alive + ((e + kWarp) >> 5));
+            }
             bool pass = false;
-            if (k < leaf.size && is_alive(ix.alive, e))
-                pass = !pruning || fabsf(__ldg(ix.dis + e) - lr.dqp) <= r;
+            if (k < leaf.size && ((al >> (e & 31)) & 1u))
+                pass = !pruning || fabsf(__uint_as_float(rec.x) - lr.dqp) <= r;
             ver += __popc(__ballot_sync(kFull, pass));
-            int len = 0;
-            if (pass) len = __ldg(ix.slen + e);
-            const bool cand = pass && (float)abs(mq - len) <= r;
+            const int len = (int)rec.y;
+            bool cand = pass && (float)abs(mq - len) <= r;
+            if (cand && ix.ehist) {
+                const uint4 h0 = __ldg(ix.ehist + 2 * e), h1 = __ldg(ix.ehist + 2 * e + 1);
+                cand = (float)hist_lb(qh0, qh1, h0, h1, mq - len) <= r;
+            }
             const unsigned cb = __ballot_sync(kFull, cand);
             if (cand) {
                 const int slot = qn + __popc(cb & ((1u << lane) - 1u));
                 qu[slot] = e;
-                qw[slot] = (int32_t)__ldg(ix.sword + e);
+                qw[slot] = (int32_t)rec.z;
                 ql[slot] = len;
             }
             qn += __popc(cb);
             __syncwarp();
-            if (qn >= kWarp) {
-                run_batch(kWarp);
-                qn -= kWarp;
-                if (lane < qn) { qu[lane] = qu[kWarp + lane]; qw[lane] = qw[kWarp + lane]; ql[lane] = ql[kWarp + lane]; }
+            if (qn >= 2 * kWarp) {
+                run_batch(2 * kWarp);
+                qn -= 2 * kWarp;
+                if (lane < qn) {
+                    qu[lane] = qu[2 * kWarp + lane];
+                    qw[lane] = qw[2 * kWarp + lane];
+                    ql[lane] = ql[2 * kWarp + lane];
+                }
                 __syncwarp();
             }
         }
@@ -779,6 +867,23 @@ __global__ void k_build_peq(const uint8_t *sym, const int64_t *soff, const int64
     atomicOr(peq + peq_off[q] + (int64_t)c * W + (pos >> 5), 1u << (pos & 31));
 }
 
+// per-query 32-bucket symbol histogram (kNoSym goes to bucket 31: a valid
+// merge, since no indexed object contains that symbol)
+__global__ void k_query_hist(const uint8_t *sym, const int64_t *soff, int nq, uint4 *qhist)
+{
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int64_t i = soff[q]; i < soff[q + 1]; i++) {
+        const uint8_t c = sym[i];
+        const int b = (c == kNoSym) ? 31 : (c & 31);
+        const uint32_t cur = (w[b >> 2] >> (8 * (b & 3))) & 0xffu;
+        if (cur < 255u) w[b >> 2] += 1u << (8 * (b & 3));
+    }
+    qhist[2 * q] = make_uint4(w[0], w[1], w[2], w[3]);
+    qhist[2 * q + 1] = make_uint4(w[4], w[5], w[6], w[7]);
+}
+
 __global__ void k_vec_prep(const double *v64, int64_t nq, int D, int Dp, float *v32, unsigned *maxabs_bits,
                            int *inexact)
 {
@@ -878,6 +983,7 @@ __global__ void k_pair_edit(int64_t np, const uint32_t *bwords, const uint32_t *
 using namespace gts;
 
 namespace gts {
+constexpr int kHistMinAlphabet = 8;   // symbol-histogram bound only pays on larger alphabets
 // Pack strings (dense symbols, given per string as a code range mapped by
 // `sym`) 4 per 32-bit word, each string starting on a 16-byte boundary.
 template <class SymOf>
@@ -927,6 +1033,8 @@ struct gts_index {
     DBuf<uint32_t> sword;
     DBuf<int32_t> slen;
     DBuf<int32_t> row;
+    DBuf<uint4> erec;
+    DBuf<uint4> ehist;
     DBuf<int32_t> alpha;
     int max_leaf = 0;
     std::vector<int64_t> ord;   // device entry -> reference table position
@@ -950,6 +1058,7 @@ struct gts_queries {
     DBuf<int64_t> soff;
     DBuf<uint32_t> peq;
     DBuf<int64_t> peq_off;
+    DBuf<uint4> qhist;
 };
 
 struct gts_result {
@@ -977,6 +1086,8 @@ IndexView make_view(const gts_index *ix, const gts_queries *q)
     v.sword = ix->sword.p;
     v.slen = ix->slen.p;
     v.row = ix->row.p;
+    v.erec = ix->erec.p;
+    v.ehist = ix->ehist.p;
     v.D = ix->D;
     v.Dp = ix->Dp;
     v.nc = ix->nc;
@@ -1005,6 +1116,7 @@ QueryView make_qview(const gts_index *ix, const gts_queries *q)
     v.str = q->str.p;
     v.peq = q->peq.p;
     v.peq_off = q->peq_off.p;
+    v.qhist = q->qhist.p;
     v.A = ix->A;
     return v;
 }
@@ -1165,6 +1277,7 @@ struct Search {
     // bound rows x largest leaf, so it cannot overflow.
     DBuf<Cand> cands;
     int64_t ncand = 0;
+    DBuf<unsigned> hist;   // kNN edit: per-query distance histogram (shrinking bound)
 
     void filter_edit(const Row *rows, int64_t m, int stats_on)
     {
@@ -1218,7 +1331,9 @@ struct Search {
             CK(cudaMemsetAsync(counter.p, 0, sizeof(unsigned long long), st));
             timed("k_leaf_edit", [&] {
                 k_leaf_edit<<<grid, 32 * kLeafWarps, 0, st>>>(iv, qv, rows, m, pruning, r32.p, hb, verified.p,
-                                                             stats_on, stats_on ? work.p : nullptr, counter.p);
+                                                             stats_on, stats_on ? work.p : nullptr, counter.p,
+                                                             // a re-run (stats_on == 0) must not count twice
+                                                             stats_on ? hist.p : nullptr, ks.p);
             });
             LAUNCH_CHECK();
             break;
@@ -1286,6 +1401,10 @@ struct Search {
     void run()
     {
         if (ix->levels == 0 || ix->n == 0 || nq == 0) return;
+        if (mode == 1 && ix->metric == GTS_EDIT) {
+            hist.alloc((size_t)nq * kHistBins, st);
+            CK(cudaMemsetAsync(hist.p, 0, sizeof(unsigned) * (size_t)nq * kHistBins, st));
+        }
         if (mode == 1 && pruning) {
             switch (ix->metric) {
             case GTS_EDIT: launch_probe<kMetricEdit>(); break;
@@ -1472,6 +1591,11 @@ gts_queries *upload_queries(gts_index *ix, const gts_query_batch *qb, cudaStream
                                                                  q->peq.p);
                 LAUNCH_CHECK();
             }
+            if (ix->ehist.p && nq) {
+                q->qhist.alloc((size_t)nq * 2, st);
+                k_query_hist<<<grid_for(nq, 128), 128, 0, st>>>(q->str.p, q->soff.p, (int)nq, q->qhist.p);
+                LAUNCH_CHECK();
+            }
         } else {
             q->D = (int)qb->dim;
             q->Dp = (q->D + 3) & ~3;
@@ -1502,9 +1626,16 @@ gts_queries *upload_queries(gts_index *ix, const gts_query_batch *qb, cudaStream
     }
 }
 
+static double now_ms()
+{
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 gts_result *run_search(gts_index *ix, const gts_queries *q, int mode, const double *radii, const int64_t *ks,
                        int64_t memory_units, int pruning, cudaStream_t st)
 {
+    static const bool trace = std::getenv("GTS_TRACE") != nullptr;
+    const double t0 = trace ? now_ms() : 0.0;
     check_queries(ix, q);
     CK(cudaSetDevice(ix->device));
     const int64_t cap = memory_units > 0 ? memory_units : (1ll << 20);
@@ -1542,7 +1673,9 @@ gts_result *run_search(gts_index *ix, const gts_queries *q, int mode, const doub
             h2d(s.r64.p, inf64.data(), (size_t)nq, st);
         }
     }
+    const double t1 = trace ? now_ms() : 0.0;
     s.run();
+    const double t2 = trace ? now_ms() : 0.0;
     {
         const unsigned long long want = s.hits + s.hits / 4;
         unsigned long long cur = ix->hit_hint[mode].load();
@@ -1554,6 +1687,11 @@ gts_result *run_search(gts_index *ix, const gts_queries *q, int mode, const doub
     } catch (...) {
         delete res;
         throw;
+    }
+    if (trace) {
+        const double t3 = now_ms();
+        fprintf(stderr, "[gts] %s nq=%lld setup=%.2fms run=%.2fms collect=%.2fms hits=%llu\n", mode ? "knn" : "range",
+                (long long)nq, t1 - t0, t2 - t1, t3 - t2, (unsigned long long)s.hits);
     }
     return res;
 }
@@ -1783,6 +1921,31 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
             h2d(ix->sword.p, wstart.data(), wstart.size(), st);
             ix->slen.alloc(lens.size(), st);
             h2d(ix->slen.p, lens.data(), lens.size(), st);
+            std::vector<uint4> rec((size_t)n);
+            for (int64_t e = 0; e < n; e++) {
+                float d = (float)t->dis[ord[(size_t)e]];
+                uint32_t db;
+                std::memcpy(&db, &d, 4);
+                rec[(size_t)e] = make_uint4(db, (uint32_t)lens[(size_t)e], wstart[(size_t)e], 0u);
+            }
+            ix->erec.alloc(rec.size(), st);
+            h2d(ix->erec.p, rec.data(), rec.size(), st);
+            if (ix->A > kHistMinAlphabet) {
+                // 32 byte-buckets of symbol counts per entry (saturating)
+                std::vector<uint8_t> hb((size_t)n * 32, 0);
+                for (int64_t e = 0; e < n; e++) {
+                    const int64_t r = drow[(size_t)e];
+                    uint8_t *h = hb.data() + e * 32;
+                    for (int64_t k = ds->offsets[r]; k < ds->offsets[r + 1]; k++) {
+                        const int sym = (int)(std::lower_bound(alpha.begin(), alpha.end(), ds->codes[k]) - alpha.begin());
+                        uint8_t &c = h[sym & 31];
+                        if (c < 255) c++;
+                    }
+                }
+                ix->ehist.alloc((size_t)n * 2, st);
+                CK(cudaMemcpyAsync(ix->ehist.p, hb.data(), hb.size(), cudaMemcpyHostToDevice, st));
+                CK(cudaStreamSynchronize(st));
+            }
         } else {
             ix->D = (int)ds->dim;
             ix->Dp = (ix->D + 3) & ~3;

@@ -45,6 +45,8 @@ struct IndexView {
     const uint32_t *sword;   // [n] first word of each entry's symbols
     const int32_t *slen;     // [n] symbols per entry
     const int32_t *row;      // [n] dataset row of each entry (row order = id order)
+    const uint4 *erec;       // [n] edit scan records {dis f32 bits, len, first text word, 0}
+    const uint4 *ehist;      // [2n] 32 byte-buckets of symbol counts (symbol % 32), or null
     int D, Dp, nc, levels;
     float rel, abs_eps;    // fp32 slack model (vectors); 0 for edit
 };
@@ -56,8 +58,20 @@ struct QueryView {
     const uint8_t *str;    // dense symbols
     const uint32_t *peq;   // Myers match masks, [A][W] per query
     const int64_t *peq_off;
+    const uint4 *qhist;    // [2nq] query symbol histograms (same buckets as ehist)
     int A;
 };
+
+// Symbol-histogram lower bound of the edit distance: every edit changes the
+// multiset difference by at most one, so ED >= (SAD(hist_q, hist_o) + |lq - lo|) / 2
+// (buckets merge symbols, saturating byte counts only shrink SAD: still a
+// lower bound).  Eight byte-SIMD absolute-difference sums.
+__device__ __forceinline__ int hist_lb(const uint4 &a0, const uint4 &a1, const uint4 &b0, const uint4 &b1, int dl)
+{
+    unsigned sad = __vsadu4(a0.x, b0.x) + __vsadu4(a0.y, b0.y) + __vsadu4(a0.z, b0.z) + __vsadu4(a0.w, b0.w) +
+                   __vsadu4(a1.x, b1.x) + __vsadu4(a1.y, b1.y) + __vsadu4(a1.z, b1.z) + __vsadu4(a1.w, b1.w);
+    return (int)((sad + (unsigned)abs(dl)) >> 1);
+}
 
 struct HitBuf {
     int32_t *q;
@@ -164,6 +178,50 @@ __device__ __forceinline__ int myers_fixed(const uint32_t *peq, int m, const uin
         score += __popc(P[b] & mk) - __popc(M[b] & mk);
     }
     return score;
+}
+
+// Two independent single-word DPs (pattern m <= 32) interleaved symbol by
+// symbol: twice the instruction-level parallelism per lane.  Texts a and b
+// come from one length-sorted leaf run, so their common prefix dominates.
+__device__ __forceinline__ void myers_w1_tail(const uint32_t *peq, const uint32_t *__restrict__ t, int j0, int n,
+                                              uint32_t &P, uint32_t &M)
+{
+    // finish text t from word j0 (symbols 4*j0 .. n-1)
+    uint32_t Pa[1] = {P}, Ma[1] = {M};
+    const int nfull = n >> 2;
+    for (int jw = j0; jw < nfull; jw++) myers_word<1>(peq, __ldg(t + jw), Pa, Ma);
+    const int rem = n & 3;
+    if (rem) {
+        const uint32_t w = __ldg(t + nfull);
+        myers_char<1>(peq, w & 0xffu, Pa, Ma);
+        if (rem > 1) myers_char<1>(peq, (w >> 8) & 0xffu, Pa, Ma);
+        if (rem > 2) myers_char<1>(peq, (w >> 16) & 0xffu, Pa, Ma);
+    }
+    P = Pa[0];
+    M = Ma[0];
+}
+
+__device__ __forceinline__ void myers2_w1(const uint32_t *peq, int m, const uint32_t *__restrict__ ta, int na,
+                                          const uint32_t *__restrict__ tb, int nb, int &da, int &db)
+{
+    uint32_t Pa = ~0u, Ma = 0u, Pb = ~0u, Mb = 0u;
+    const int nf = min(na, nb) >> 2;
+    uint32_t wa = __ldg(ta), wb = __ldg(tb);
+    for (int jw = 0; jw < nf; jw++) {
+        const uint32_t xa = __ldg(ta + jw + 1), xb = __ldg(tb + jw + 1);
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            myers_step1(peq[(wa >> (8 * k)) & 0xffu], Pa, Ma);
+            myers_step1(peq[(wb >> (8 * k)) & 0xffu], Pb, Mb);
+        }
+        wa = xa;
+        wb = xb;
+    }
+    myers_w1_tail(peq, ta, nf, na, Pa, Ma);
+    myers_w1_tail(peq, tb, nf, nb, Pb, Mb);
+    const uint32_t mk = (m & 31) ? ((1u << (m & 31)) - 1u) : ~0u;
+    da = (m == 0) ? na : (na == 0 ? m : na + __popc(Pa & mk) - __popc(Ma & mk));
+    db = (m == 0) ? nb : (nb == 0 ? m : nb + __popc(Pb & mk) - __popc(Mb & mk));
 }
 
 __device__ __noinline__ int myers_generic(const uint32_t *peq, int W, int m, const uint32_t *__restrict__ t4, int n)
