@@ -304,139 +304,6 @@ __global__ void __launch_bounds__(256) k_verify(IndexView ix, QueryView qv, cons
     }
 }
 
-struct Cand {
-    int32_t q, e;
-};
-
-// Leaf filter for edit distance (search.py:518-524), one warp per leaf row:
-// live entries passing the lemma-1 pivot test are "verified" (the
-// reference's counter); those whose length difference also fits the
-// radius (|len q - len o| is a lower bound of the edit distance) are
-// candidates for k_verify_edit.  Two passes without contended atomics:
-// WRITE=false counts candidates per row, an exclusive scan gives each row
-// its slice, WRITE=true fills it in leaf order (leaves are length-sorted,
-// so neighbouring candidates have similar DP lengths).
-template <bool WRITE>
-__global__ void __launch_bounds__(256) k_filter_edit(IndexView ix, QueryView qv, const Row *__restrict__ rows,
-                                                     int64_t m, int pruning, const float *__restrict__ r32,
-                                                     int32_t *row_count, const long long *row_off, Cand *out,
-                                                     unsigned long long *verified_stat, int stats_on,
-                                                     unsigned long long *work)
-{
-    const int lane = lane_id();
-    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < m; w += warps) {
-        const Row lr = rows[w];
-        const int q = lr.q;
-        const NodeRec leaf = ix.node[lr.node];
-        const int pos = ix.npos[lr.node];
-        const float r = r32[q];
-        const int mq = qlen(qv, q);
-        unsigned ver = 0, ncand = 0;
-        long long base = WRITE ? row_off[w] : 0;
-        for (int b = 0; b < leaf.size; b += kWarp) {
-            const int k = b + lane;
-            const int e = pos + k;
-            bool pass = false;
-            if (k < leaf.size && is_alive(ix.alive, e))
-                pass = !pruning || fabsf(__ldg(ix.dis + e) - lr.dqp) <= r;
-            if (!WRITE) ver += __popc(__ballot_sync(kFull, pass));
-            const bool cand = pass && (float)abs(mq - __ldg(ix.slen + e)) <= r;
-            const unsigned cb = __ballot_sync(kFull, cand);
-            if (WRITE && cand) out[base + ncand + __popc(cb & ((1u << lane) - 1u))] = Cand{q, e};
-            ncand += __popc(cb);
-        }
-        if (lane == 0) {
-            if (!WRITE) {
-                row_count[w] = (int32_t)ncand;
-                if (stats_on && ver) atomicAdd(verified_stat + q, (unsigned long long)ver);
-                if (work) {
-                    atomicAdd(work + kWorkPairs, (unsigned long long)ver);
-                    atomicAdd(work + kWorkEntries, (unsigned long long)leaf.size);
-                    atomicAdd(work + kWorkRows, 1ull);
-                }
-            }
-        }
-    }
-}
-
-constexpr int kSlots = 32;
-constexpr int kSlotWords = 256;
-
-// Exact edit distance of every candidate, one thread per (query, object)
-// pair (bit-parallel Myers/Hyyro), emitting hits d <= r.  The match masks of
-// the (few) distinct queries of a block are staged in shared memory.
-__global__ void __launch_bounds__(256) k_verify_edit(IndexView ix, QueryView qv, const Cand *__restrict__ cand,
-                                                     int64_t ncand, const float *__restrict__ r32, HitBuf out,
-                                                     unsigned long long *work)
-{
-    __shared__ uint32_t peq_s[kSlots * kSlotWords];
-    __shared__ int slot_q[kSlots];
-    __shared__ int warp_tot[8];
-    const int lane = lane_id(), warp = threadIdx.x >> 5;
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < ncand; base += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = base + threadIdx.x;
-        const bool valid = i < ncand;
-        Cand c{-1, -1};
-        if (valid) c = cand[i];
-        const int prevq = (valid && threadIdx.x > 0) ? cand[i - 1].q : -2;
-        const unsigned start = (valid && c.q != prevq) ? 1u : 0u;
-        // block-wide inclusive scan of segment starts -> slot index
-        unsigned inc = start;
-        for (int o = 1; o < 32; o <<= 1) {
-            unsigned v = __shfl_up_sync(kFull, inc, o);
-            if (lane >= o) inc += v;
-        }
-        if (lane == 31) warp_tot[warp] = inc;
-        __syncthreads();
-        unsigned off = 0, total = 0;
-        for (int w2 = 0; w2 < (int)(blockDim.x >> 5); w2++) {
-            if (w2 < warp) off += warp_tot[w2];
-            total += warp_tot[w2];
-        }
-        const int slot = (int)(inc + off) - 1;
-        if (start && slot < kSlots) slot_q[slot] = c.q;
-        __syncthreads();
-        const int nslot = min((int)total, kSlots);
-        for (int t = threadIdx.x; t < nslot * kSlotWords; t += blockDim.x) {
-            const int sidx = t / kSlotWords, wi = t - sidx * kSlotWords;
-            const int sq = slot_q[sidx];
-            const int words = qv.A * ((qlen(qv, sq) + 31) >> 5);
-            if (wi < words) peq_s[t] = __ldg(qv.peq + qv.peq_off[sq] + wi);
-        }
-        __syncthreads();
-        bool hit = false;
-        int d = 0;
-        unsigned long long steps = 0;
-        if (valid) {
-            const int mq = qlen(qv, c.q);
-            const int words = qv.A * ((mq + 31) >> 5);
-            const int n = __ldg(ix.slen + c.e);
-            const uint32_t *txt = ix.str + __ldg(ix.sword + c.e);
-            // two call sites so the staged one compiles to shared-memory loads
-            if (slot < kSlots && words <= kSlotWords) d = edit_peq(peq_s + slot * kSlotWords, mq, txt, n);
-            else d = edit_peq(qv.peq + qv.peq_off[c.q], mq, txt, n);
-            hit = (float)d <= r32[c.q];
-            steps = (unsigned long long)((mq + 31) >> 5) * (unsigned long long)n;
-        }
-        const unsigned hb = __ballot_sync(kFull, hit);
-        if (hb) {
-            unsigned long long hbase = 0;
-            if (lane == 0) hbase = atomicAdd(out.counter, (unsigned long long)__popc(hb));
-            hbase = __shfl_sync(kFull, hbase, 0);
-            if (hit) {
-                const unsigned long long sl = hbase + __popc(hb & ((1u << lane) - 1u));
-                if (sl < out.cap) { out.q[sl] = c.q; out.e[sl] = c.e; out.d[sl] = (double)d; }
-            }
-        }
-        if (work) {
-            for (int o = 16; o > 0; o >>= 1) steps += __shfl_down_sync(kFull, steps, o);
-            if (lane == 0 && steps) atomicAdd(work + kWorkSteps, steps);
-        }
-        __syncthreads();
-    }
-}
-
 constexpr int kLeafWarps = 8;          // warps per block of k_leaf_edit
 constexpr int kRowChunk = 16;          // rows a warp claims per cursor bump
 
@@ -464,7 +331,7 @@ __global__ void __launch_bounds__(256, 4) k_leaf_edit(IndexView ix, QueryView qv
                                                       unsigned *hist, const int32_t *__restrict__ ks)
 {
     __shared__ uint32_t peq_s[kLeafWarps][kWarpPeqWords];
-    __shared__ int32_t queue[kLeafWarps][3][96];   // entry, first text word, length
+    __shared__ int32_t queue[kLeafWarps][3][64];   // entry, first text word, length
     const int lane = lane_id(), wib = threadIdx.x >> 5;
     uint32_t *peq_w = peq_s[wib];
     int32_t *qu = queue[wib][0];
@@ -529,38 +396,20 @@ __global__ void __launch_bounds__(256, 4) k_leaf_edit(IndexView ix, QueryView qv
             }
         }
     };
-    // run DPs for queue slots [0, cnt) (cnt <= 64): lane takes slots lane
-    // and lane + 32; with a single-word pattern both run interleaved
+    // run DPs for queue slots [0, cnt) (cnt <= 32), one per lane
     auto run_batch = [&](int cnt) {
-        const bool va = lane < cnt, vb = lane + 32 < cnt;
-        int ea = -1, eb = -1, da = 0, db = 0;
+        const bool va = lane < cnt;
+        int ea = -1, da = 0;
         if (va) {
             ea = qu[lane];
             const int na = ql[lane];
             const uint32_t *tA = ix.str + (uint32_t)qw[lane];
-            if (vb) {
-                eb = qu[lane + 32];
-                const int nb = ql[lane + 32];
-                const uint32_t *tB = ix.str + (uint32_t)qw[lane + 32];
-                if (staged && mq <= 32) {
-                    myers2_w1(peq_w, mq, tA, na, tB, nb, da, db);
-                } else if (staged) {
-                    da = edit_peq(peq_w, mq, tA, na);
-                    db = edit_peq(peq_w, mq, tB, nb);
-                } else {
-                    da = edit_peq_global(peq_g, mq, tA, na);
-                    db = edit_peq_global(peq_g, mq, tB, nb);
-                }
-                steps += (unsigned long long)((mq + 31) >> 5) * (unsigned long long)nb;
-            } else {
-                da = staged ? edit_peq(peq_w, mq, tA, na) : edit_peq_global(peq_g, mq, tA, na);
-            }
+            da = staged ? edit_peq(peq_w, mq, tA, na) : edit_peq_global(peq_g, mq, tA, na);
             steps += (unsigned long long)((mq + 31) >> 5) * (unsigned long long)na;
         }
-        const bool ha = va && (float)da <= r, hb2 = vb && (float)db <= r;
+        const bool ha = va && (float)da <= r;
         emit(ha, ea, da);
-        emit(hb2, eb, db);
-        shrink(ha, da, hb2, db);
+        shrink(ha, da, false, 0);
         __syncwarp();
     };
 
@@ -640,14 +489,10 @@ __global__ void __launch_bounds__(256, 4) k_leaf_edit(IndexView ix, QueryView qv
             }
             qn += __popc(cb);
             __syncwarp();
-            if (qn >= 2 * kWarp) {
-                run_batch(2 * kWarp);
-                qn -= 2 * kWarp;
-                if (lane < qn) {
-                    qu[lane] = qu[2 * kWarp + lane];
-                    qw[lane] = qw[2 * kWarp + lane];
-                    ql[lane] = ql[2 * kWarp + lane];
-                }
+            if (qn >= kWarp) {
+                run_batch(kWarp);
+                qn -= kWarp;
+                if (lane < qn) { qu[lane] = qu[kWarp + lane]; qw[lane] = qw[kWarp + lane]; ql[lane] = ql[kWarp + lane]; }
                 __syncwarp();
             }
         }
@@ -1272,54 +1117,7 @@ struct Search {
         hits = after;
     }
 
-    // edit distance: k_filter_edit compacts candidates, k_verify_edit runs
-    // one Myers DP per candidate.  The candidate list is sized by the exact
-    // bound rows x largest leaf, so it cannot overflow.
-    DBuf<Cand> cands;
-    int64_t ncand = 0;
     DBuf<unsigned> hist;   // kNN edit: per-query distance histogram (shrinking bound)
-
-    void filter_edit(const Row *rows, int64_t m, int stats_on)
-    {
-        DBuf<int32_t> cnt((size_t)m, st);
-        DBuf<long long> off((size_t)m + 1, st);
-        unsigned grid = grid_for(m * 32, 256, 148u * 64u);
-        timed("k_filter_edit", [&] {
-            k_filter_edit<false><<<grid, 256, 0, st>>>(iv, qv, rows, m, pruning, r32.p, cnt.p, nullptr, nullptr,
-                                                       verified.p, stats_on, stats_on ? work.p : nullptr);
-        });
-        LAUNCH_CHECK();
-        size_t tb = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.p, off.p, (int)m, st);
-        DBuf<uint8_t> tmp(tb, st);
-        CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, cnt.p, off.p, (int)m, st));
-        g_launches += 2;
-        // total = off[m-1] + cnt[m-1]
-        long long last_off = 0;
-        int32_t last_cnt = 0;
-        CK(cudaMemcpyAsync(&last_off, off.p + m - 1, sizeof(long long), cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(&last_cnt, cnt.p + m - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        ncand = last_off + last_cnt;
-        if (ncand == 0) return;
-        if ((int64_t)cands.n < ncand) cands.alloc((size_t)ncand, st);
-        timed("k_filter_edit", [&] {
-            k_filter_edit<true><<<grid, 256, 0, st>>>(iv, qv, rows, m, pruning, r32.p, nullptr, off.p, cands.p,
-                                                      nullptr, 0, nullptr);
-        });
-        LAUNCH_CHECK();
-    }
-
-    void verify_edit(int stats_on)
-    {
-        if (ncand == 0) return;
-        HitBuf hb{hq.p, he.p, hd.p, (unsigned long long)hq.n, counter.p + 1};
-        unsigned grid = grid_for(ncand, 256, 148u * 16u);
-        timed("k_verify_edit", [&] {
-            k_verify_edit<<<grid, 256, 0, st>>>(iv, qv, cands.p, ncand, r32.p, hb, stats_on ? work.p : nullptr);
-        });
-        LAUNCH_CHECK();
-    }
 
     void dispatch_verify(const Row *rows, int64_t m, int stats_on)
     {

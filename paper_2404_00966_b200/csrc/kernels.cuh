@@ -180,50 +180,6 @@ __device__ __forceinline__ int myers_fixed(const uint32_t *peq, int m, const uin
     return score;
 }
 
-// Two independent single-word DPs (pattern m <= 32) interleaved symbol by
-// symbol: twice the instruction-level parallelism per lane.  Texts a and b
-// come from one length-sorted leaf run, so their common prefix dominates.
-__device__ __forceinline__ void myers_w1_tail(const uint32_t *peq, const uint32_t *__restrict__ t, int j0, int n,
-                                              uint32_t &P, uint32_t &M)
-{
-    // finish text t from word j0 (symbols 4*j0 .. n-1)
-    uint32_t Pa[1] = {P}, Ma[1] = {M};
-    const int nfull = n >> 2;
-    for (int jw = j0; jw < nfull; jw++) myers_word<1>(peq, __ldg(t + jw), Pa, Ma);
-    const int rem = n & 3;
-    if (rem) {
-        const uint32_t w = __ldg(t + nfull);
-        myers_char<1>(peq, w & 0xffu, Pa, Ma);
-        if (rem > 1) myers_char<1>(peq, (w >> 8) & 0xffu, Pa, Ma);
-        if (rem > 2) myers_char<1>(peq, (w >> 16) & 0xffu, Pa, Ma);
-    }
-    P = Pa[0];
-    M = Ma[0];
-}
-
-__device__ __forceinline__ void myers2_w1(const uint32_t *peq, int m, const uint32_t *__restrict__ ta, int na,
-                                          const uint32_t *__restrict__ tb, int nb, int &da, int &db)
-{
-    uint32_t Pa = ~0u, Ma = 0u, Pb = ~0u, Mb = 0u;
-    const int nf = min(na, nb) >> 2;
-    uint32_t wa = __ldg(ta), wb = __ldg(tb);
-    for (int jw = 0; jw < nf; jw++) {
-        const uint32_t xa = __ldg(ta + jw + 1), xb = __ldg(tb + jw + 1);
-#pragma unroll
-        for (int k = 0; k < 4; k++) {
-            myers_step1(peq[(wa >> (8 * k)) & 0xffu], Pa, Ma);
-            myers_step1(peq[(wb >> (8 * k)) & 0xffu], Pb, Mb);
-        }
-        wa = xa;
-        wb = xb;
-    }
-    myers_w1_tail(peq, ta, nf, na, Pa, Ma);
-    myers_w1_tail(peq, tb, nf, nb, Pb, Mb);
-    const uint32_t mk = (m & 31) ? ((1u << (m & 31)) - 1u) : ~0u;
-    da = (m == 0) ? na : (na == 0 ? m : na + __popc(Pa & mk) - __popc(Ma & mk));
-    db = (m == 0) ? nb : (nb == 0 ? m : nb + __popc(Pb & mk) - __popc(Mb & mk));
-}
-
 __device__ __noinline__ int myers_generic(const uint32_t *peq, int W, int m, const uint32_t *__restrict__ t4, int n)
 {
     uint32_t P[kMaxWords], M[kMaxWords];
