@@ -47,6 +47,12 @@ WORKLOADS = {
                 radius=8.0, k=10, config_index=3),
     # configs[0]: T-Loc-like 2-D L2, CPU-reference-runnable
     "tloc": dict(metric="l2", n=100_000, nq=1_000, dim=2, radius=0.0582588, k=10, config_index=0),
+    # configs[2]: 128-d L2 n=1M, kNN k=10, 100k-query batch (clustered)
+    "vec128": dict(metric="l2", n=1_000_000, nq=100_000, dim=128, clusters=1000, spread=0.05, noise=0.01,
+                   radius=0.5, k=10, config_index=2),
+    # configs[4] single shard: 32-d L1, 12.5M per GPU at 8 GPUs, kNN k=100
+    "l1shard": dict(metric="l1", n=12_500_000, nq=100_000, dim=32, clusters=10_000, spread=0.05, noise=0.01,
+                    radius=0.5, k=100, config_index=4),
 }
 
 
@@ -97,6 +103,22 @@ def make_workload(name, rank, args):
         codes, off = gen_strings(w["n"], seed, w["min_len"], w["max_len"], w["alphabet"])
         qcodes, qoff = string_queries(codes, off, w["nq"], 13, w["alphabet"] if True else None)
         w.update(codes=codes, off=off, qcodes=qcodes, qoff=qoff)
+    elif "clusters" in w:
+        # clustered vectors: centers U[0,1)^D, members N(center, spread); queries are
+        # members + N(0, noise); fp32-representable
+        rng = np.random.default_rng(seed)
+        D, n = w["dim"], w["n"]
+        centers = rng.uniform(0.0, 1.0, size=(w["clusters"], D)).astype(np.float32)
+        mat = np.empty((n, D), dtype=np.float32)
+        step = 1 << 20
+        for a in range(0, n, step):
+            b = min(n, a + step)
+            assign = rng.integers(0, w["clusters"], size=b - a)
+            mat[a:b] = centers[assign] + rng.normal(0.0, w["spread"], size=(b - a, D)).astype(np.float32)
+        qr = np.random.default_rng(13)
+        qi = qr.integers(0, n, size=w["nq"])
+        q = mat[qi] + qr.normal(0.0, w["noise"], size=(w["nq"], D)).astype(np.float32)
+        w.update(mat=mat.astype(np.float64), q=q.astype(np.float32).astype(np.float64))
     else:
         rng = np.random.default_rng(seed)
         mat = rng.uniform(0.0, 1.0, size=(w["n"], w["dim"])).astype(np.float32).astype(np.float64)
@@ -213,6 +235,7 @@ class Engine:
             self.qb = _lib.GtsQueryBatch(code, nq, 0, None, p(w["qcodes"], _lib._i32p), p(w["qoff"], _lib._i64p))
         else:
             self.qb = _lib.GtsQueryBatch(code, nq, w["dim"], p(w["q"], _lib._f64p), None, None)
+        self.code = code
 
     def upload(self, stream):
         q = C.c_void_p()
@@ -346,7 +369,7 @@ def run_ours(args, rank, world, local_rank):
         "config": {
             "workload": f"{args.workload} (BASELINE.json configs[{w['config_index']}])",
             "n_per_gpu": w["n"], "nq": nq, "radius": w["radius"], "k": w["k"], "node_capacity": 20,
-            "levels": eng.levels, "memory_units": 1 << 20,
+            "levels": eng.levels, "memory_units": 1 << 24,
             "l2_policy": "index payload+tables exceed nothing: words (~25 MB) stay L2-resident by design; "
                          "no flush between steps (device-resident index is the operating point)",
             "parallelism": f"dp{world} (one shard per GPU)",
@@ -380,7 +403,7 @@ def run_e2e(eng, w, args, sp, merger, world, max_total):
         h2d_in = pc.numel() * 4 + po.numel() * 8
     else:
         pv = torch.from_numpy(w["q"]).pin_memory()
-        qb = _lib.GtsQueryBatch(2, nq, w["dim"], C.cast(pv.data_ptr(), _lib._f64p), None, None)
+        qb = _lib.GtsQueryBatch(eng.code, nq, w["dim"], C.cast(pv.data_ptr(), _lib._f64p), None, None)
         h2d_in = pv.numel() * 8
     prad = torch.from_numpy(eng.radii).pin_memory()
     pks = torch.from_numpy(eng.ks).pin_memory()
@@ -474,7 +497,7 @@ def oracle_setup(w):
     if w["metric"] == "edit":
         data = O.Payloads(O.EDIT, codes=w["codes"], off=w["off"], ids=w["ids"])
     else:
-        data = O.Payloads(O.L2, vec=w["mat"], ids=w["ids"])
+        data = O.Payloads({"l1": O.L1, "l2": O.L2}[w["metric"]], vec=w["mat"], ids=w["ids"])
     t0 = time.perf_counter()
     tree = O.build(data, 20, 0, threads=os.cpu_count() or 1)
     return O, data, tree, time.perf_counter() - t0
@@ -487,7 +510,7 @@ def oracle_queries(O, w, idx):
         np.cumsum([len(s) for s in qs], out=off[1:])
         codes = np.concatenate(qs) if qs else np.zeros(0, np.int32)
         return O.Payloads(O.EDIT, codes=codes, off=off)
-    return O.Payloads(O.L2, vec=w["q"][idx])
+    return O.Payloads({"l1": O.L1, "l2": O.L2}[w["metric"]], vec=w["q"][idx])
 
 
 def time_oracle(O, data, tree, w, n_range, n_knn, threads, seed=0):
@@ -506,7 +529,7 @@ def time_oracle(O, data, tree, w, n_range, n_knn, threads, seed=0):
 def cpu_baseline(w, args):
     O, data, tree, build_s = oracle_setup(w)
     threads = os.cpu_count() or 1
-    n_range, n_knn = (256, 64) if w["metric"] == "edit" else (1000, 1000)
+    n_range, n_knn = (256, 64) if w["metric"] == "edit" else ((1000, 1000) if w["n"] <= 100_000 else (32, 32))
     t = time_oracle(O, data, tree, w, n_range, n_knn, threads)
     per_q = (t["range"][1] / t["range"][0] + t["knn"][1] / t["knn"][0]) / 2
     return {
@@ -525,7 +548,7 @@ def run_reference(args, rank, world):
     w = make_workload(args.workload, 0, args)
     O, data, tree, build_s = oracle_setup(w)
     threads = os.cpu_count() or 1
-    n_r, n_k = (32, 32) if w["metric"] == "edit" else (500, 500)
+    n_r, n_k = (32, 32) if w["metric"] == "edit" else ((500, 500) if w["n"] <= 100_000 else (16, 16))
     for i in range(args.warmup):
         time_oracle(O, data, tree, w, 4, 4, threads, seed=100 + i)
     tot_q, tot_t = 0, 0.0

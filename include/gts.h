@@ -106,7 +106,8 @@ int gts_queries_free(gts_queries *q);
 typedef struct gts_result gts_result;     /* device CSR + stats */
 
 /* BatchSearcher.range_batch (search.py:238-248): radii[nq] >= 0.
- * memory_units: row budget (search.py:229, runtime.py:18); 0 = default.
+ * memory_units: row budget (search.py:229, runtime.py:18); 0 = the device
+ * default of 1<<24 rows (the reference's CPU default is 1<<20).
  * Answers per query are every live object with d <= r, sorted by
  * (distance, id) (search.py:298-314). */
 int gts_range_batch(gts_index *ix, const gts_queries *q, const double *radii,

@@ -541,6 +541,146 @@ __global__ void k_seg_counts(const unsigned long long *key, int64_t n, int qshif
     counts[q] = lb((unsigned long long)(q + 1) << qshift) - lb((unsigned long long)q << qshift);
 }
 
+// ---------------------------------------------------------------------------
+// Leaf-grouped verification for vectors.  The chunk's leaf rows are counting-
+// sorted by leaf; a work item is (leaf, up to kItemQueries queries).  A block
+// stages the leaf's vectors in shared memory once and every query visiting
+// the leaf reads them from there: one HBM/L2 read of a leaf per item instead
+// of one per (query, entry) pair.  Same filter / screen / float64 recheck as
+// k_verify (search.py:507-570).
+// ---------------------------------------------------------------------------
+struct Item {
+    int32_t leaf, start, count, pad;
+};
+constexpr int kItemQueries = 128;
+
+__global__ void k_leaf_hist(const Row *rows, int64_t m, int leaf_first, int *cnt)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) atomicAdd(cnt + (rows[i].node - leaf_first), 1);
+}
+
+__global__ void k_leaf_scatter(const Row *rows, int64_t m, int leaf_first, int *cursor, Row *out)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) {
+        const Row r = rows[i];
+        out[atomicAdd(cursor + (r.node - leaf_first), 1)] = r;
+    }
+}
+
+__global__ void k_item_counts(const int *cnt, int nleaf, int *nitem)
+{
+    int l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l < nleaf) nitem[l] = (cnt[l] + kItemQueries - 1) / kItemQueries;
+}
+
+__global__ void k_make_items(const int *cnt, const int *off, const int *item_off, int nleaf, int leaf_first, Item *items)
+{
+    int l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= nleaf) return;
+    const int c = cnt[l];
+    for (int j = 0, s = 0; s < c; j++, s += kItemQueries)
+        items[item_off[l] + j] = Item{leaf_first + l, off[l] + s, min(kItemQueries, c - s), 0};
+}
+
+template <int MET>
+__device__ __forceinline__ float vdist32_smem(const float *a, const float *b, int Dp)
+{
+    float acc = 0.f;
+    for (int i = 0; i < Dp; i += 4) {
+        const float4 x = *reinterpret_cast<const float4 *>(a + i);
+        const float4 y = *reinterpret_cast<const float4 *>(b + i);
+        const float d0 = x.x - y.x, d1 = x.y - y.y, d2 = x.z - y.z, d3 = x.w - y.w;
+        if (MET == kMetricL1) acc += (fabsf(d0) + fabsf(d1)) + (fabsf(d2) + fabsf(d3));
+        else acc += (d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3);
+    }
+    return MET == kMetricL1 ? acc : sqrtf(acc);
+}
+
+template <int MET>
+__global__ void __launch_bounds__(256) k_leafgroup_vec(IndexView ix, QueryView qv, const Row *__restrict__ srows,
+                                                       const Item *__restrict__ items, int nitems, int pruning,
+                                                       const float *__restrict__ r32, const double *__restrict__ r64,
+                                                       HitBuf out, unsigned long long *verified_stat, int stats_on,
+                                                       unsigned long long *work)
+{
+    extern __shared__ float4 smem4[];
+    float *smem = reinterpret_cast<float *>(smem4);
+    const int lane = lane_id(), warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int stride = ix.Dp + 4;                      // padded: conflict-free LDS.128 per quarter warp
+    float *ent = smem;
+    float *qslot = smem + (size_t)ix.max_leaf * stride + (size_t)warp * ix.Dp;
+    const int d4 = ix.Dp >> 2;
+    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+        const Item item = items[it];
+        const NodeRec leaf = ix.node[item.leaf];
+        const int pos = ix.npos[item.leaf];
+        for (int t = threadIdx.x; t < leaf.size * d4; t += blockDim.x) {
+            const int e = t / d4, c = t - e * d4;
+            *reinterpret_cast<float4 *>(ent + e * stride + 4 * c) =
+                __ldg(reinterpret_cast<const float4 *>(ix.vec32 + (size_t)(pos + e) * ix.Dp) + c);
+        }
+        __syncthreads();
+        unsigned long long pairs = 0;
+        for (int qi = warp; qi < item.count; qi += nwarps) {
+            const Row lr = srows[item.start + qi];
+            const int q = lr.q;
+            const float r = r32[q];
+            const double rr = r64[q];
+            for (int c = lane; c < d4; c += kWarp)
+                *reinterpret_cast<float4 *>(qslot + 4 * c) =
+                    __ldg(reinterpret_cast<const float4 *>(qv.vec32 + (size_t)q * ix.Dp) + c);
+            __syncwarp();
+            unsigned ver = 0;
+            for (int b = 0; b < leaf.size; b += kWarp) {
+                const int k = b + lane;
+                const int e = pos + k;
+                bool pass = false;
+                if (k < leaf.size && is_alive(ix.alive, e)) {
+                    if (!pruning) pass = true;
+                    else {
+                        const float de = __ldg(ix.dis + e);
+                        pass = fabsf(de - lr.dqp) <= r + slack(ix, de, lr.dqp, r);
+                    }
+                }
+                ver += __popc(__ballot_sync(kFull, pass));
+                bool hit = false;
+                double d64 = 0.0;
+                if (pass) {
+                    const float d = vdist32_smem<MET>(ent + k * stride, qslot, ix.Dp);
+                    if (d - slack(ix, d, 0.f) <= r) {
+                        d64 = vdist64<MET>(ix, qv, q, e);
+                        hit = d64 <= rr;
+                    }
+                }
+                const unsigned hb = __ballot_sync(kFull, hit);
+                if (hb) {
+                    unsigned long long base = 0;
+                    if (lane == 0) base = atomicAdd(out.counter, (unsigned long long)__popc(hb));
+                    base = __shfl_sync(kFull, base, 0);
+                    if (hit) {
+                        const unsigned long long slot = base + __popc(hb & ((1u << lane) - 1u));
+                        if (slot < out.cap) { out.q[slot] = q; out.e[slot] = e; out.d[slot] = d64; }
+                    }
+                }
+            }
+            if (lane == 0 && stats_on && ver) atomicAdd(verified_stat + q, (unsigned long long)ver);
+            pairs += ver;
+            __syncwarp();
+        }
+        if (work && lane == 0) {
+            atomicAdd(work + kWorkPairs, pairs);
+            atomicAdd(work + kWorkRows, 0ull);
+        }
+        if (work && threadIdx.x == 0) {
+            atomicAdd(work + kWorkEntries, (unsigned long long)leaf.size * item.count);
+            atomicAdd(work + kWorkRows, (unsigned long long)item.count);
+        }
+        __syncthreads();
+    }
+}
+
 // Rows (q, leaf) for every live leaf when pruning is disabled (search.py:338-355).
 __global__ void k_all_leaves(const int32_t *leaves, int nleaves, int q0, int nqc, Row *out)
 {
@@ -882,6 +1022,7 @@ struct gts_index {
     DBuf<uint4> ehist;
     DBuf<int32_t> alpha;
     int max_leaf = 0;
+    int leaf_first = 0, leaf_count = 0;
     std::vector<int64_t> ord;   // device entry -> reference table position
     std::atomic<unsigned long long> hit_hint[2] = {{0}, {0}};   // hits of the last range / kNN call
     DBuf<int32_t> live_leaves;
@@ -937,6 +1078,9 @@ IndexView make_view(const gts_index *ix, const gts_queries *q)
     v.Dp = ix->Dp;
     v.nc = ix->nc;
     v.levels = ix->levels;
+    v.leaf_first = ix->leaf_first;
+    v.leaf_count = ix->leaf_count;
+    v.max_leaf = ix->max_leaf;
     if (ix->metric == GTS_EDIT) {
         v.rel = 0.f;
         v.abs_eps = 0.f;
@@ -1079,9 +1223,64 @@ struct Search {
         return h_counter[i];
     }
 
+    // smem bytes of k_leafgroup_vec for this index (0 = does not fit)
+    size_t grouped_smem() const
+    {
+        const size_t b = ((size_t)ix->max_leaf * (ix->Dp + 4) + 8 * (size_t)ix->Dp) * sizeof(float);
+        return b <= 200 * 1024 ? b : 0;
+    }
+
+    template <int MET>
+    void launch_grouped(const Row *rows, int64_t m, int stats_on)
+    {
+        const int nleaf = ix->leaf_count;
+        DBuf<int> cnt((size_t)nleaf + 1, st), off((size_t)nleaf + 1, st), cur((size_t)nleaf + 1, st);
+        DBuf<int> nit((size_t)nleaf + 1, st), ioff((size_t)nleaf + 1, st);
+        DBuf<Row> srows((size_t)m, st);
+        CK(cudaMemsetAsync(cnt.p, 0, sizeof(int) * (nleaf + 1), st));
+        k_leaf_hist<<<grid_for(m, 256), 256, 0, st>>>(rows, m, ix->leaf_first, cnt.p);
+        LAUNCH_CHECK();
+        size_t tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.p, off.p, nleaf + 1, st);
+        DBuf<uint8_t> tmp(tb, st);
+        CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, cnt.p, off.p, nleaf + 1, st));
+        CK(cudaMemcpyAsync(cur.p, off.p, sizeof(int) * (nleaf + 1), cudaMemcpyDeviceToDevice, st));
+        k_leaf_scatter<<<grid_for(m, 256), 256, 0, st>>>(rows, m, ix->leaf_first, cur.p, srows.p);
+        LAUNCH_CHECK();
+        k_item_counts<<<grid_for(nleaf, 256), 256, 0, st>>>(cnt.p, nleaf, nit.p);
+        LAUNCH_CHECK();
+        CK(cudaMemsetAsync(nit.p + nleaf, 0, sizeof(int), st));
+        CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, nit.p, ioff.p, nleaf + 1, st));
+        g_launches += 4;
+        int nitems = 0;
+        CK(cudaMemcpyAsync(&nitems, ioff.p + nleaf, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (nitems == 0) return;
+        DBuf<Item> items((size_t)nitems, st);
+        k_make_items<<<grid_for(nleaf, 256), 256, 0, st>>>(cnt.p, off.p, ioff.p, nleaf, ix->leaf_first, items.p);
+        LAUNCH_CHECK();
+        HitBuf hb{hq.p, he.p, hd.p, (unsigned long long)hq.n, counter.p + 1};
+        const size_t sm = grouped_smem();
+        static bool attr_set[3] = {false, false, false};
+        if (!attr_set[MET]) {
+            CK(cudaFuncSetAttribute(k_leafgroup_vec<MET>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            attr_set[MET] = true;
+        }
+        unsigned grid = (unsigned)std::min<int>(nitems, 148 * 8);
+        timed("k_leafgroup_vec", [&] {
+            k_leafgroup_vec<MET><<<grid, 256, sm, st>>>(iv, qv, srows.p, items.p, nitems, pruning, r32.p, r64.p, hb,
+                                                       verified.p, stats_on, stats_on ? work.p : nullptr);
+        });
+        LAUNCH_CHECK();
+    }
+
     template <int MET>
     void launch_verify(const Row *rows, int64_t m, int stats_on)
     {
+        if (grouped_smem() && ix->Dp >= 8 && std::getenv("GTS_NO_GROUPED") == nullptr) {
+            launch_grouped<MET>(rows, m, stats_on);
+            return;
+        }
         HitBuf hb{hq.p, he.p, hd.p, (unsigned long long)hq.n, counter.p + 1};
         unsigned grid = grid_for(m * 32, 256, 148u * 64u);
         timed("k_verify", [&] {
@@ -1436,7 +1635,9 @@ gts_result *run_search(gts_index *ix, const gts_queries *q, int mode, const doub
     const double t0 = trace ? now_ms() : 0.0;
     check_queries(ix, q);
     CK(cudaSetDevice(ix->device));
-    const int64_t cap = memory_units > 0 ? memory_units : (1ll << 20);
+    // 0 = device default: 16M frontier rows (256 MiB per child table) -- the
+    // reference's 1<<20 (runtime.py:18) was sized for a CPU; same formula
+    const int64_t cap = memory_units > 0 ? memory_units : (1ll << 24);
     if (ix->n > 0 && cap < ix->nc) fail(GTS_EBUDGET, "memory_units %lld below fan-out %d", (long long)cap, ix->nc);
     const int64_t nq = q->nq;
     Search s(ix, q, st, mode, cap, pruning);
@@ -1673,6 +1874,8 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
             ix->live_leaves.alloc(std::max<size_t>(lv.size(), 1), st);
             h2d(ix->live_leaves.p, lv.data(), lv.size(), st);
             for (int64_t i = first; i < first + count; i++) ix->max_leaf = std::max<int>(ix->max_leaf, (int)t->size[i]);
+            ix->leaf_first = (int)first;
+            ix->leaf_count = (int)count;
         }
         {
             std::vector<int32_t> row((size_t)n);

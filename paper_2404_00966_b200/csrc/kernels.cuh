@@ -48,6 +48,7 @@ struct IndexView {
     const uint4 *erec;       // [n] edit scan records {dis f32 bits, len, first text word, 0}
     const uint4 *ehist;      // [2n] 32 byte-buckets of symbol counts (symbol % 32), or null
     int D, Dp, nc, levels;
+    int leaf_first, leaf_count, max_leaf;
     float rel, abs_eps;    // fp32 slack model (vectors); 0 for edit
 };
 

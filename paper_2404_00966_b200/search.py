@@ -17,7 +17,9 @@ import numpy as np
 
 from . import _lib
 from .metrics import METRIC_CODES, STRING_METRICS
-from .runtime import DEFAULT_MEMORY_UNITS, BudgetError
+from .runtime import BudgetError
+
+DEVICE_MEMORY_UNITS = 1 << 24
 
 RANGE = "range"
 KNN = "knn"
@@ -123,14 +125,15 @@ class BatchSearcher:
 
     Args mirror the reference (search.py:214-234): tree, runtime (accepted,
     unused: the device does the parallel work), memory_units (row budget of
-    the one materialized frontier table; default 1<<20), pruning.
+    the one materialized frontier table; None = the device default of 1<<24
+    rows, the reference's CPU default being 1<<20), pruning.
     """
 
     def __init__(self, tree, runtime=None, memory_units=None, pruning=True, device=0):
         self.tree = tree
         self.ds = tree.dataset
         self.rt = runtime
-        self.capacity = int(memory_units or DEFAULT_MEMORY_UNITS)
+        self.capacity = int(memory_units or DEVICE_MEMORY_UNITS)
         self.pruning = pruning
         self.device = device
         if tree.n > 0 and self.capacity < tree.nc:
