@@ -29,11 +29,13 @@
 #include <vector>
 
 #include <cub/cub.cuh>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include "../../include/gts.h"
 #include "common.h"
 #include "kernels.cuh"
+#include "tcgen05.cuh"
 
 namespace gts {
 
@@ -84,6 +86,7 @@ struct ProfRec {
 static std::mutex g_prof_mu;
 static std::vector<std::pair<std::string, ProfRec>> g_prof;
 static unsigned long long g_work[4] = {0, 0, 0, 0};   // pairs, word-steps, entries, rows
+static unsigned long long *g_phase_dev = nullptr;       // GTS_PHASES: per-phase clocks of k_leafgroup_mma
 enum { kWorkPairs = 0, kWorkSteps = 1, kWorkEntries = 2, kWorkRows = 3 };
 
 static void prof_add(const char *name, double ms)
@@ -598,12 +601,18 @@ __device__ __forceinline__ float vdist32_smem(const float *a, const float *b, in
     return MET == kMetricL1 ? acc : sqrtf(acc);
 }
 
+constexpr int kFHistBins = 64;
+__device__ __forceinline__ void fhist_add(unsigned *hist, const float *r0, int q, double d);
+__device__ __forceinline__ void fhist_shrink(unsigned *hist, const float *r0, const int32_t *ks, float *r32,
+                                             double *r64, int q);
+
 template <int MET>
 __global__ void __launch_bounds__(256) k_leafgroup_vec(IndexView ix, QueryView qv, const Row *__restrict__ srows,
                                                        const Item *__restrict__ items, int nitems, int pruning,
-                                                       const float *__restrict__ r32, const double *__restrict__ r64,
+                                                       float *r32, double *r64,
                                                        HitBuf out, unsigned long long *verified_stat, int stats_on,
-                                                       unsigned long long *work)
+                                                       unsigned long long *work, unsigned *fhist, const float *r0,
+                                                       const int32_t *ks)
 {
     extern __shared__ float4 smem4[];
     float *smem = reinterpret_cast<float *>(smem4);
@@ -626,8 +635,9 @@ __global__ void __launch_bounds__(256) k_leafgroup_vec(IndexView ix, QueryView q
         for (int qi = warp; qi < item.count; qi += nwarps) {
             const Row lr = srows[item.start + qi];
             const int q = lr.q;
-            const float r = r32[q];
-            const double rr = r64[q];
+            const float r = __ldcg(r32 + q);
+            const double rr = __ldcg(r64 + q);
+            unsigned nh = 0;
             for (int c = lane; c < d4; c += kWarp)
                 *reinterpret_cast<float4 *>(qslot + 4 * c) =
                     __ldg(reinterpret_cast<const float4 *>(qv.vec32 + (size_t)q * ix.Dp) + c);
@@ -662,8 +672,14 @@ __global__ void __launch_bounds__(256) k_leafgroup_vec(IndexView ix, QueryView q
                     if (hit) {
                         const unsigned long long slot = base + __popc(hb & ((1u << lane) - 1u));
                         if (slot < out.cap) { out.q[slot] = q; out.e[slot] = e; out.d[slot] = d64; }
+                        if (fhist) fhist_add(fhist, r0, q, d64);
                     }
+                    nh += __popc(hb);
                 }
+            }
+            if (fhist && nh) {
+                __threadfence();
+                if (lane == 0) fhist_shrink(fhist, r0, ks, r32, r64, q);
             }
             if (lane == 0 && stats_on && ver) atomicAdd(verified_stat + q, (unsigned long long)ver);
             pairs += ver;
@@ -679,6 +695,264 @@ __global__ void __launch_bounds__(256) k_leafgroup_vec(IndexView ix, QueryView q
         }
         __syncthreads();
     }
+}
+
+// ---------------------------------------------------------------------------
+// Tensor-core verification for dense L2 (north_star: "norm-expansion MMA with
+// an exact recheck").  One work item = (leaf, up to 128 queries): a
+// kind::f16 (bf16 in, fp32 accumulate) tcgen05 MMA of M=128 queries x
+// N=leaf entries x K=D into TMEM.  Both operands are centred on the leaf's
+// pivot c, so
+//     d^2(q,o) = dqp^2 + dis^2 - 2 (q-c).(o-c)
+// reuses the pivot distances the tree already holds and keeps operand norms
+// small.  bf16 rounding (2^-9 per operand) bounds the dot error by
+// 2^-8 ||q-c|| ||o-c||, i.e. d^2 by 2^-7 dqp dis; the screen uses twice that.
+// Every entry passing lemma 1 whose approximate d^2 is within the band of r^2
+// is recomputed exactly in float64 (numpy order), so answers are exact.
+// ~64 KB of shared memory per CTA: three CTAs per SM overlap each other's
+// staging, MMA and epilogue.
+// ---------------------------------------------------------------------------
+// kNN shrinking bound for float metrics: per-query 64-bin histogram of the
+// exact distances found so far over [0, r0] (r0 = the probe radius).  The
+// upper edge of the bin where the count reaches k bounds the k-th distance
+// from above (k distinct real objects lie at or below it), so the radius can
+// only shrink to values that still admit every true answer and its ties.
+constexpr int kFHist = 64;
+
+__device__ __forceinline__ void fhist_add(unsigned *hist, const float *r0, int q, double d)
+{
+    const double R0 = (double)r0[q];
+    if (!(d <= R0) || !(R0 > 0.0) || isinf(R0)) return;
+    int b = (int)(d / R0 * kFHist);
+    b = min(max(b, 0), kFHist - 1);
+    atomicAdd(hist + (size_t)q * kFHist + b, 1u);
+}
+
+__device__ __forceinline__ void fhist_shrink(unsigned *hist, const float *r0, const int32_t *ks, float *r32,
+                                             double *r64, int q)
+{
+    const double R0 = (double)r0[q];
+    if (!(R0 > 0.0) || isinf(R0)) return;
+    const uint4 *h4 = reinterpret_cast<const uint4 *>(hist + (size_t)q * kFHist);
+    const unsigned k = (unsigned)ks[q];
+    unsigned run = 0;
+    int t = -1;
+    for (int i = 0; i < kFHist / 4 && t < 0; i++) {
+        const uint4 v = __ldcg(h4 + i);
+        const unsigned c[4] = {v.x, v.y, v.z, v.w};
+        for (int j = 0; j < 4; j++) {
+            run += c[j];
+            if (run >= k) { t = 4 * i + j; break; }
+        }
+    }
+    if (t < 0) return;
+    const double R = (double)(t + 1) / kFHist * R0 * (1.0 + 1.0 / (1 << 20));
+    if (R < r64[q]) {
+        atomicMin(reinterpret_cast<unsigned long long *>(r64 + q), (unsigned long long)__double_as_longlong(R));
+        float Rf = (float)R;
+        if ((double)Rf < R) Rf = nextafterf(Rf, INFINITY);
+        atomicMin(reinterpret_cast<int *>(r32 + q), __float_as_int(Rf));
+    }
+}
+
+constexpr int kMmaThreads = 256;  // 8 warps: warps w and w+4 share TMEM lane quadrant w%4
+// TMEM columns per CTA: power of two >= the largest leaf (N <= 256); the
+// host launches at most 512 / cols CTAs per SM so allocation never waits.
+
+__global__ void __launch_bounds__(kMmaThreads, 3) k_leafgroup_mma(IndexView ix, QueryView qv, const Row *__restrict__ srows,
+                                                                   const Item *__restrict__ items, int nitems,
+                                                                   float *r32, double *r64, HitBuf out,
+                                                                   unsigned long long *verified_stat, int stats_on,
+                                                                   unsigned long long *work, uint32_t tmem_cols,
+                                                                   unsigned long long *phase_clk, unsigned *fhist,
+                                                                   const float *r0, const int32_t *ks)
+{
+    long long t_stage = 0, t_wait = 0, t_epi = 0;
+    extern __shared__ __align__(1024) uint8_t smraw[];
+    __shared__ uint64_t mbar;
+    __shared__ uint32_t tmem_slot;
+    __shared__ float s_dis[256];
+    __shared__ uint8_t s_al[256];
+    __shared__ int s_q[128];
+    // 1024-byte alignment for the 128-byte swizzle, kept as an index into the
+    // shared array so the compiler emits STS (not generic stores)
+    const uint32_t pad = (1024u - (tc::smem_u32(smraw) & 1023u)) & 1023u;
+    uint8_t *sm = smraw + pad;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int nkb = ix.Dk >> 6;           // 64 bf16 (128 bytes) per K-block row
+    uint8_t *A = sm;
+    uint8_t *B = sm + (size_t)nkb * 128 * 128;
+    if (warp == 0) tc::tmem_alloc(&tmem_slot, tmem_cols);
+    if (tid == 0) {
+        tc::mbar_init(&mbar, 1);
+        tc::fence_mbar_init();
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tmem = tmem_slot;
+    uint32_t phase = 0;
+    const int c16 = ix.Dk >> 3;           // 16-byte chunks (8 bf16) per row
+    const int dp4 = ix.Dp >> 2;
+    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+        const Item item = items[it];
+        const NodeRec leaf = ix.node[item.leaf];
+        const int pos = ix.npos[item.leaf];
+        const int N = max(16, (leaf.size + 15) & ~15);
+        const float4 *pv = reinterpret_cast<const float4 *>(ix.vec32 + (size_t)leaf.piv * ix.Dp);
+        const long long c_a = clock64();
+        if (tid < 128) s_q[tid] = tid < item.count ? srows[item.start + tid].q : -1;
+        for (int j = tid; j < leaf.size; j += blockDim.x) {
+            s_dis[j] = __ldg(ix.dis + pos + j);
+            s_al[j] = is_alive(ix.alive, pos + j) ? 1 : 0;
+        }
+        __syncthreads();
+        // A: query rows centred on the leaf pivot, rounded to bf16 (zero pad)
+        constexpr int kBatch = 4;
+        for (int t0 = tid; t0 < 128 * c16; t0 += kBatch * kMmaThreads) {
+            uint4 pk[kBatch];
+#pragma unroll
+            for (int u = 0; u < kBatch; u++) {
+                const int t = t0 + u * kMmaThreads;
+                const int row = t / c16, c = t - row * c16;
+                pk[u] = make_uint4(0u, 0u, 0u, 0u);
+                const int q = (t < 128 * c16) ? s_q[row] : -1;
+                if (q >= 0 && 2 * c < dp4) {
+                    const float4 *qp = reinterpret_cast<const float4 *>(qv.vec32 + (size_t)q * ix.Dp);
+                    const float4 x0 = __ldg(qp + 2 * c), y0 = __ldg(pv + 2 * c);
+                    float4 x1 = make_float4(0.f, 0.f, 0.f, 0.f), y1 = x1;
+                    if (2 * c + 1 < dp4) { x1 = __ldg(qp + 2 * c + 1); y1 = __ldg(pv + 2 * c + 1); }
+                    __nv_bfloat162 b0 = __floats2bfloat162_rn(x0.x - y0.x, x0.y - y0.y);
+                    __nv_bfloat162 b1 = __floats2bfloat162_rn(x0.z - y0.z, x0.w - y0.w);
+                    __nv_bfloat162 b2 = __floats2bfloat162_rn(x1.x - y1.x, x1.y - y1.y);
+                    __nv_bfloat162 b3 = __floats2bfloat162_rn(x1.z - y1.z, x1.w - y1.w);
+                    pk[u] = make_uint4(*reinterpret_cast<uint32_t *>(&b0), *reinterpret_cast<uint32_t *>(&b1),
+                                       *reinterpret_cast<uint32_t *>(&b2), *reinterpret_cast<uint32_t *>(&b3));
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kBatch; u++) {
+                const int t = t0 + u * kMmaThreads;
+                if (t < 128 * c16) {
+                    const int row = t / c16, c = t - row * c16;
+                    *reinterpret_cast<uint4 *>(A + (c >> 3) * 16384 + tc::sw128_offset(row, c & 7)) = pk[u];
+                }
+            }
+        }
+        // B: the leaf's centred bf16 entries (contiguous rows)
+        for (int t0 = tid; t0 < N * c16; t0 += kBatch * kMmaThreads) {
+            uint4 pk[kBatch];
+#pragma unroll
+            for (int u = 0; u < kBatch; u++) {
+                const int t = t0 + u * kMmaThreads;
+                const int row = t / c16, c = t - row * c16;
+                pk[u] = make_uint4(0u, 0u, 0u, 0u);
+                if (t < N * c16 && row < leaf.size) pk[u] = __ldg(ix.vcent + (size_t)(pos + row) * c16 + c);
+            }
+#pragma unroll
+            for (int u = 0; u < kBatch; u++) {
+                const int t = t0 + u * kMmaThreads;
+                if (t < N * c16) {
+                    const int row = t / c16, c = t - row * c16;
+                    *reinterpret_cast<uint4 *>(B + (size_t)(c >> 3) * N * 128 + tc::sw128_offset(row, c & 7)) = pk[u];
+                }
+            }
+        }
+        tc::fence_async_smem();
+        __syncthreads();
+        const long long c_b = clock64();
+        if (tid == 0) {
+            tc::fence_after_sync();
+            const uint32_t idesc = tc::idesc_bf16(128, N);
+            const uint32_t a0 = tc::smem_u32(A), b0 = tc::smem_u32(B);
+            for (int kb = 0; kb < nkb; kb++) {
+#pragma unroll
+                for (int ks = 0; ks < 4; ks++) {   // K = 16 bf16 = 32 bytes per MMA
+                    const uint64_t ad = tc::desc_k_sw128(a0 + kb * 16384 + ks * 32);
+                    const uint64_t bd = tc::desc_k_sw128(b0 + kb * N * 128 + ks * 32);
+                    tc::mma_bf16(tmem, ad, bd, idesc, (kb | ks) ? 1u : 0u);
+                }
+            }
+            tc::mma_commit(&mbar);
+        }
+        tc::mbar_wait(&mbar, phase);
+        phase ^= 1u;
+        tc::fence_after_sync();
+        const long long c_c = clock64();
+        // epilogue: query row = TMEM lane 32*(warp%4)+lane; warps w and w+4
+        // split the N columns in halves
+        const int qrow = 32 * (warp & 3) + (tid & 31);
+        const int half = warp >> 2;
+        const int cbeg = half ? ((N >> 5) << 4) : 0;            // multiple of 16
+        const int cend = half ? N : ((N >> 5) << 4);
+        const bool valid = qrow < item.count;
+        int q = 0;
+        float dqp = 0.f, r = 0.f;
+        double rr = 0.0;
+        if (valid) {
+            const Row lr = srows[item.start + qrow];
+            q = lr.q;
+            dqp = lr.dqp;
+            r = __ldcg(r32 + q);
+            rr = __ldcg(r64 + q);
+        }
+        const bool inf_r = isinf(r);
+        const float R2 = r * r * (1.f + 1e-6f);
+        unsigned nhits = 0;
+        const float kd = ldexpf(dqp, -6);
+        const float kq = 8.f * ix.rel * dqp * dqp + 4.f * ix.abs_eps * (dqp + ix.abs_eps);
+        unsigned ver = 0;
+        const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+        for (int c0 = cbeg; c0 < cend; c0 += 16) {
+            float acc[16];
+            tc::tmem_ld16(lane_base + (uint32_t)c0, acc);   // warp-collective: every thread runs it
+            if (!valid) continue;
+#pragma unroll
+            for (int jj = 0; jj < 16; jj++) {
+                const int j = c0 + jj;
+                if (j >= leaf.size || !s_al[j]) continue;
+                const float dis = s_dis[j];
+                if (!(fabsf(dis - dqp) <= r + slack(ix, dis, dqp, r))) continue;   // lemma 1
+                ver++;
+                bool cand = inf_r;
+                if (!cand) {
+                    const float d2a = dqp * dqp + dis * dis - 2.f * acc[jj];
+                    const float err = kd * dis + kq + 8.f * ix.rel * dis * dis + 4.f * ix.abs_eps * dis;
+                    cand = d2a <= R2 + err;
+                }
+                if (cand) {
+                    const double d64 = vdist64<kMetricL2>(ix, qv, q, pos + j);
+                    if (d64 <= rr) {
+                        const unsigned long long sl = atomicAdd(out.counter, 1ull);
+                        if (sl < out.cap) { out.q[sl] = q; out.e[sl] = pos + j; out.d[sl] = d64; }
+                        if (fhist) fhist_add(fhist, r0, q, d64);
+                        nhits++;
+                    }
+                }
+            }
+        }
+        if (fhist && valid && nhits) fhist_shrink(fhist, r0, ks, r32, r64, q);
+        if (valid && stats_on && ver) atomicAdd(verified_stat + q, (unsigned long long)ver);
+        if (work && valid) atomicAdd(work + kWorkPairs, (unsigned long long)ver);
+        if (work && tid == 0) {
+            atomicAdd(work + kWorkEntries, (unsigned long long)leaf.size * item.count);
+            atomicAdd(work + kWorkRows, (unsigned long long)item.count);
+            atomicAdd(work + kWorkSteps, (unsigned long long)128 * N * ix.Dk);   // MMA MACs issued
+        }
+        tc::fence_before_sync();
+        __syncthreads();
+        const long long c_d = clock64();
+        t_stage += c_b - c_a;
+        t_wait += c_c - c_b;
+        t_epi += c_d - c_c;
+    }
+    if (phase_clk && tid == 0) {
+        atomicAdd(phase_clk + 0, (unsigned long long)t_stage);
+        atomicAdd(phase_clk + 1, (unsigned long long)t_wait);
+        atomicAdd(phase_clk + 2, (unsigned long long)t_epi);
+    }
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc(tmem, tmem_cols);
 }
 
 // Rows (q, leaf) for every live leaf when pruning is disabled (search.py:338-355).
@@ -1020,6 +1294,8 @@ struct gts_index {
     DBuf<int32_t> row;
     DBuf<uint4> erec;
     DBuf<uint4> ehist;
+    DBuf<uint4> vcent;   // bf16 x 8 per uint4
+    int Dk = 0;
     DBuf<int32_t> alpha;
     int max_leaf = 0;
     int leaf_first = 0, leaf_count = 0;
@@ -1074,6 +1350,8 @@ IndexView make_view(const gts_index *ix, const gts_queries *q)
     v.row = ix->row.p;
     v.erec = ix->erec.p;
     v.ehist = ix->ehist.p;
+    v.vcent = ix->vcent.p;
+    v.Dk = ix->Dk;
     v.D = ix->D;
     v.Dp = ix->Dp;
     v.nc = ix->nc;
@@ -1261,6 +1539,28 @@ struct Search {
         LAUNCH_CHECK();
         HitBuf hb{hq.p, he.p, hd.p, (unsigned long long)hq.n, counter.p + 1};
         const size_t sm = grouped_smem();
+        if (MET == kMetricL2 && ix->vcent.p && pruning) {
+            const int nmax = std::max(16, (ix->max_leaf + 15) & ~15);
+            const size_t smb = (size_t)(ix->Dk / 64) * (128 * 128 + (size_t)nmax * 128) + 1024;
+            static bool mma_attr = false;
+            if (!mma_attr) {
+                CK(cudaFuncSetAttribute(k_leafgroup_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+                mma_attr = true;
+            }
+            int sms = 148;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
+            uint32_t cols = 32;
+            while ((int)cols < nmax) cols <<= 1;
+            const int per_sm = std::max(1, std::min(3, (int)(512 / cols)));
+            unsigned gridm = (unsigned)std::min<int>(nitems, sms * per_sm);
+            timed("k_leafgroup_mma", [&] {
+                k_leafgroup_mma<<<gridm, kMmaThreads, smb, st>>>(iv, qv, srows.p, items.p, nitems, r32.p, r64.p, hb,
+                                                         verified.p, stats_on, stats_on ? work.p : nullptr, cols,
+                                                         g_phase_dev, stats_on ? fhist.p : nullptr, r0.p, ks.p);
+            });
+            LAUNCH_CHECK();
+            return;
+        }
         static bool attr_set[3] = {false, false, false};
         if (!attr_set[MET]) {
             CK(cudaFuncSetAttribute(k_leafgroup_vec<MET>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -1269,7 +1569,8 @@ struct Search {
         unsigned grid = (unsigned)std::min<int>(nitems, 148 * 8);
         timed("k_leafgroup_vec", [&] {
             k_leafgroup_vec<MET><<<grid, 256, sm, st>>>(iv, qv, srows.p, items.p, nitems, pruning, r32.p, r64.p, hb,
-                                                       verified.p, stats_on, stats_on ? work.p : nullptr);
+                                                       verified.p, stats_on, stats_on ? work.p : nullptr,
+                                                       stats_on ? fhist.p : nullptr, r0.p, ks.p);
         });
         LAUNCH_CHECK();
     }
@@ -1317,6 +1618,8 @@ struct Search {
     }
 
     DBuf<unsigned> hist;   // kNN edit: per-query distance histogram (shrinking bound)
+    DBuf<unsigned> fhist;  // kNN vectors: per-query 64-bin histogram over [0, r0]
+    DBuf<float> r0;        // kNN vectors: the probe radius (histogram scale)
 
     void dispatch_verify(const Row *rows, int64_t m, int stats_on)
     {
@@ -1407,6 +1710,12 @@ struct Search {
             case GTS_EDIT: launch_probe<kMetricEdit>(); break;
             case GTS_L1: launch_probe<kMetricL1>(); break;
             default: launch_probe<kMetricL2>(); break;
+            }
+            if (ix->metric != GTS_EDIT) {
+                fhist.alloc((size_t)nq * kFHist, st);
+                CK(cudaMemsetAsync(fhist.p, 0, sizeof(unsigned) * (size_t)nq * kFHist, st));
+                r0.alloc((size_t)nq, st);
+                CK(cudaMemcpyAsync(r0.p, r32.p, sizeof(float) * nq, cudaMemcpyDeviceToDevice, st));
             }
         }
         if (!pruning) {
@@ -1691,6 +2000,14 @@ gts_result *run_search(gts_index *ix, const gts_queries *q, int mode, const doub
         const double t3 = now_ms();
         fprintf(stderr, "[gts] %s nq=%lld setup=%.2fms run=%.2fms collect=%.2fms hits=%llu\n", mode ? "knn" : "range",
                 (long long)nq, t1 - t0, t2 - t1, t3 - t2, (unsigned long long)s.hits);
+        if (g_phase_dev) {
+            unsigned long long ph[3];
+            cudaMemcpy(ph, g_phase_dev, sizeof(ph), cudaMemcpyDeviceToHost);
+            cudaMemset(g_phase_dev, 0, 3 * sizeof(unsigned long long));
+            const double tot = (double)(ph[0] + ph[1] + ph[2]) + 1e-9;
+            fprintf(stderr, "[gts]   mma phases (CTA clocks): stage %.3f  mma-wait %.3f  epilogue %.3f\n",
+                    ph[0] / tot, ph[1] / tot, ph[2] / tot);
+        }
     }
     return res;
 }
@@ -1802,6 +2119,10 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
         fail(GTS_EMETRIC, "metric %d not supported on the device path (edit, l1, l2)", ds->metric);
     if (ds->n > (1ll << 31) - 64) fail(GTS_EINVAL, "index larger than 2^31 entries; shard it");
     CK(cudaSetDevice(device));
+    if (std::getenv("GTS_PHASES") && !g_phase_dev) {
+        CK(cudaMalloc((void **)&g_phase_dev, 4 * sizeof(unsigned long long)));
+        CK(cudaMemset(g_phase_dev, 0, 4 * sizeof(unsigned long long)));
+    }
     {
         cudaMemPool_t pool;
         CK(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -1964,6 +2285,27 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
             }
             ix->data_exact = exact;
             ix->data_maxabs = mx;
+            // tensor-core L2 path: entries centred on their leaf's pivot, bf16, K padded to 64
+            if (ds->metric == GTS_L2 && ix->D >= 32 && ix->D <= 128 && ix->max_leaf <= 256 &&
+                std::getenv("GTS_NO_MMA") == nullptr) {
+                ix->Dk = (ix->D + 63) & ~63;
+                std::vector<__nv_bfloat16> vc((size_t)n * ix->Dk, __float2bfloat16(0.f));
+                __int128 c = 1;
+                for (int l = 1; l < ix->levels; l++) c *= ix->nc;
+                const int64_t lfirst = (int64_t)((c - 1) / (ix->nc - 1) + 1), lcount = (int64_t)c;
+                for (int64_t i = lfirst; i < lfirst + lcount; i++) {
+                    const int64_t p0 = t->pos[i], sz = t->size[i];
+                    if (sz <= 0) continue;
+                    const int pvp = nodes[(size_t)i].piv;
+                    for (int64_t e = p0; e < p0 + sz; e++)
+                        for (int d = 0; d < ix->D; d++)
+                            vc[(size_t)e * ix->Dk + d] = __float2bfloat16(
+                                v32[(size_t)(e * ix->Dp + d)] - v32[(size_t)((int64_t)pvp * ix->Dp + d)]);
+                }
+                ix->vcent.alloc(vc.size() / 8, st);
+                CK(cudaMemcpyAsync(ix->vcent.p, vc.data(), vc.size() * sizeof(__nv_bfloat16), cudaMemcpyHostToDevice, st));
+                CK(cudaStreamSynchronize(st));
+            }
             ix->vec32.alloc(v32.size(), st);
             h2d(ix->vec32.p, v32.data(), v32.size(), st);
             if (!exact) {

@@ -47,6 +47,8 @@ struct IndexView {
     const int32_t *row;      // [n] dataset row of each entry (row order = id order)
     const uint4 *erec;       // [n] edit scan records {dis f32 bits, len, first text word, 0}
     const uint4 *ehist;      // [2n] 32 byte-buckets of symbol counts (symbol % 32), or null
+    const uint4 *vcent;      // [n][Dk/8] bf16 vectors centred on their leaf pivot (tensor-core L2 path), or null
+    int Dk;                  // D rounded up to 64 (one 128-byte bf16 row per K-block)
     int D, Dp, nc, levels;
     int leaf_first, leaf_count, max_leaf;
     float rel, abs_eps;    // fp32 slack model (vectors); 0 for edit

@@ -268,3 +268,25 @@ def test_streaming_index_matches_live_set():
         c, i, d = csr(got)
         assert np.array_equal(i, want.ids) and np.array_equal(d, want.dis)
     assert si.rebuild_count >= 1
+
+
+# -- tensor-core (tcgen05 tf32) L2 verification path ------------------------
+
+@pytest.mark.parametrize("dim,clustered", [(64, True), (100, False), (128, True), (128, False)])
+def test_l2_tensor_core_path_exact(dim, clustered):
+    """L2 with D >= 32 verifies leaf blocks with a tf32 tcgen05 MMA plus an
+    exact float64 recheck; answers must equal brute force bit-exactly."""
+    rng = np.random.default_rng(dim + 7 * clustered)
+    n = 30_000
+    if clustered:
+        mat = f32(P.generate_clustered(n, dim, 60, seed=dim, spread=0.05))
+        q = mat[rng.integers(0, n, 200)] + f32(rng.normal(0, 0.01, (200, dim)))
+    else:
+        mat = f32(P.generate_uniform(n, dim, seed=dim))
+        q = f32(rng.uniform(0, 1, (200, dim)))
+    q = f32(q)
+    ds = P.Dataset.from_vectors(mat, P.L2)
+    tree = P.build(ds, P.TreeConfig(20, 1))
+    radii = rng.uniform(0.2, 0.9, 200) * (1.0 if clustered else np.sqrt(dim / 6.0))
+    check_against_oracle(ds, tree, list(q), O.Payloads(O.L2, vec=mat), O.Payloads(O.L2, vec=q), radii,
+                         rng.integers(1, 30, 200))
