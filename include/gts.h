@@ -39,6 +39,11 @@ extern "C" {
 #define GTS_EMETRIC 3
 #define GTS_ECUDA 4
 #define GTS_EOOM 5
+#define GTS_EREBUILD 6   /* cache insert needs a rebuild (symbol outside the index alphabet) */
+
+/* gts_batch_host flags */
+#define GTS_FLAG_PRUNING 1   /* BatchSearcher pruning=True (search.py:225) */
+#define GTS_FLAG_CACHE 2     /* also scan the pending-insert cache (StreamingIndex queries) */
 
 /* metric codes = the reference snapshot codes (io.py:30-35) */
 #define GTS_EDIT 0
@@ -121,6 +126,17 @@ int gts_range_batch_host(gts_index *ix, const gts_query_batch *qb, const double 
                          int64_t memory_units, int pruning, void *stream, gts_result **out);
 int gts_knn_batch_host(gts_index *ix, const gts_query_batch *qb, const int64_t *ks,
                        int64_t memory_units, int pruning, void *stream, gts_result **out);
+
+/* Generic host entry point: mode 0 = range (radii), 1 = kNN (ks); flags as
+ * above.  With GTS_FLAG_CACHE the answers are exact over tree entries that
+ * are not tombstoned plus the pending-insert cache, i.e. StreamingIndex
+ * query_range / query_knn (updates.py:167-196). */
+int gts_batch_host(gts_index *ix, const gts_query_batch *qb, int mode, const double *radii,
+                   const int64_t *ks, int64_t memory_units, int flags, void *stream, gts_result **out);
+/* Replace the device copy of the pending-insert cache (StreamingIndex.pending,
+ * updates.py:109-122) with `items` (ids + payloads).  Returns GTS_EREBUILD when
+ * a string holds a symbol the index alphabet lacks. */
+int gts_index_cache_set(gts_index *ix, const gts_dataset *items, void *stream);
 
 /* Result access: sizes, then a copy into caller buffers (host or device,
  * decided by the pointer).  offsets[nq+1], ids[total], dis[total],

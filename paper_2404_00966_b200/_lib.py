@@ -15,7 +15,8 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libgts.so")
 
-GTS_OK, GTS_EINVAL, GTS_EBUDGET, GTS_EMETRIC, GTS_ECUDA, GTS_EOOM = range(6)
+GTS_OK, GTS_EINVAL, GTS_EBUDGET, GTS_EMETRIC, GTS_ECUDA, GTS_EOOM, GTS_EREBUILD = range(7)
+FLAG_PRUNING, FLAG_CACHE = 1, 2
 
 _i64p = C.POINTER(C.c_int64)
 _f64p = C.POINTER(C.c_double)
@@ -77,6 +78,9 @@ def lib():
             "gts_knn_batch": (C.c_int, [v, v, _i64p, C.c_int64, C.c_int, v, C.POINTER(v)]),
             "gts_range_batch_host": (C.c_int, [v, C.POINTER(GtsQueryBatch), _f64p, C.c_int64, C.c_int, v, C.POINTER(v)]),
             "gts_knn_batch_host": (C.c_int, [v, C.POINTER(GtsQueryBatch), _i64p, C.c_int64, C.c_int, v, C.POINTER(v)]),
+            "gts_batch_host": (C.c_int, [v, C.POINTER(GtsQueryBatch), C.c_int, _f64p, _i64p, C.c_int64, C.c_int,
+                                         v, C.POINTER(v)]),
+            "gts_index_cache_set": (C.c_int, [v, C.POINTER(GtsDataset), v]),
             "gts_result_info": (C.c_int, [v, _i64p, _i64p, _i64p, _i64p]),
             "gts_result_copy": (C.c_int, [v, _i64p, _i64p, _f64p, _i64p, _i64p, v]),
             "gts_result_device": (C.c_int, [v, C.POINTER(v), C.POINTER(v), C.POINTER(v)]),
@@ -103,7 +107,8 @@ EXPORTED = (
     "gts_index_set_tombstones", "gts_queries_upload", "gts_queries_free", "gts_range_batch",
     "gts_knn_batch", "gts_range_batch_host", "gts_knn_batch_host", "gts_result_info", "gts_result_copy",
     "gts_result_device", "gts_result_free", "gts_pair_distances", "gts_launch_count", "gts_last_error",
-    "gts_version", "gts_profile_enable", "gts_profile_read", "gts_bench_int_peak",
+    "gts_version", "gts_profile_enable", "gts_profile_read", "gts_bench_int_peak", "gts_batch_host",
+    "gts_index_cache_set",
 )
 
 

@@ -955,6 +955,46 @@ __global__ void __launch_bounds__(kMmaThreads, 3) k_leafgroup_mma(IndexView ix, 
     if (warp == 0) tc::tmem_dealloc(tmem, tmem_cols);
 }
 
+// ---------------------------------------------------------------------------
+// Pending-insert cache (StreamingIndex, updates.py:109-215): a small set of
+// objects not yet in the tree, scanned exactly for every query of the batch
+// (one extra leaf with no pivot filter).  Hits carry entry id -(slot+1).
+// ---------------------------------------------------------------------------
+struct CacheView {
+    int n;
+    const int64_t *ids;
+    const float *vec32;       // [n][Dp]
+    const double *vec64;      // [n][D]
+    const uint32_t *words;    // packed dense symbols
+    const uint32_t *sword;
+    const int32_t *slen;
+};
+
+template <int MET>
+__global__ void k_cache_scan(IndexView ix, QueryView qv, CacheView cv, int nq, const float *__restrict__ r32,
+                             const double *__restrict__ r64, HitBuf out)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (int64_t)nq * cv.n) return;
+    const int q = (int)(i / cv.n), c = (int)(i - (int64_t)q * cv.n);
+    double d;
+    if (MET == kMetricEdit) {
+        d = (double)edit_peq(qv.peq + qv.peq_off[q], qlen(qv, q), cv.words + cv.sword[c], cv.slen[c]);
+    } else {
+        const double s = pw_sum64<MET>(nullptr, cv.vec64 + (size_t)c * ix.D, qv.vec64 + (size_t)q * ix.D, 0, ix.D);
+        d = MET == kMetricL1 ? s : __dsqrt_rn(s);
+    }
+    if (d <= r64[q]) {
+        const unsigned long long sl = atomicAdd(out.counter, 1ull);
+        if (sl < out.cap) { out.q[sl] = q; out.e[sl] = -(c + 1); out.d[sl] = d; }
+    }
+}
+
+__device__ __forceinline__ int64_t entry_id(const int64_t *ids, const int64_t *cache_ids, int32_t e)
+{
+    return e >= 0 ? ids[e] : cache_ids[-e - 1];
+}
+
 // Rows (q, leaf) for every live leaf when pruning is disabled (search.py:338-355).
 __global__ void k_all_leaves(const int32_t *leaves, int nleaves, int q0, int nqc, Row *out)
 {
@@ -1162,11 +1202,13 @@ __global__ void k_vec_prep(const double *v64, int64_t nq, int D, int Dp, float *
 
 // collect -------------------------------------------------------------------
 
-__global__ void k_gather_id(const int32_t *e, int64_t n, const int64_t *ids, unsigned long long *key, int32_t *perm)
+__global__ void k_gather_id(const int32_t *e, int64_t n, const int64_t *ids, const int64_t *cache_ids,
+                            unsigned long long *key, int32_t *perm)
 {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    key[i] = (unsigned long long)ids[e[i]];
+    const int32_t ei = e[i];
+    key[i] = (unsigned long long)(ei >= 0 ? ids[ei] : cache_ids[-ei - 1]);
     perm[i] = (int32_t)i;
 }
 
@@ -1203,7 +1245,7 @@ __global__ void k_clamp_counts(const long long *counts, const int32_t *ks, int n
 // to out_off[q] + r when r < out count (kNN truncation keeps the k first).
 __global__ void k_emit(const int32_t *perm, const int32_t *hq, const int32_t *he, const double *hd,
                        const long long *in_off, const long long *out_off, const long long *out_cnt,
-                       const int64_t *ids, int64_t n, int64_t *out_ids, double *out_dis)
+                       const int64_t *ids, const int64_t *cache_ids, int64_t n, int64_t *out_ids, double *out_dis)
 {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -1211,7 +1253,8 @@ __global__ void k_emit(const int32_t *perm, const int32_t *hq, const int32_t *he
     const int q = hq[h];
     const long long r = i - in_off[q];
     if (r < out_cnt[q]) {
-        out_ids[out_off[q] + r] = ids[he[h]];
+        const int32_t e = he[h];
+        out_ids[out_off[q] + r] = e >= 0 ? ids[e] : cache_ids[-e - 1];
         out_dis[out_off[q] + r] = hd[h];
     }
 }
@@ -1301,6 +1344,13 @@ struct gts_index {
     int leaf_first = 0, leaf_count = 0;
     std::vector<int64_t> ord;   // device entry -> reference table position
     std::atomic<unsigned long long> hit_hint[2] = {{0}, {0}};   // hits of the last range / kNN call
+    // pending-insert cache (device copy of the caller's pending set)
+    int cache_n = 0;
+    DBuf<int64_t> cache_ids;
+    DBuf<float> cache_vec32;
+    DBuf<double> cache_vec64;
+    DBuf<uint32_t> cache_words, cache_sword;
+    DBuf<int32_t> cache_slen;
     DBuf<int32_t> live_leaves;
     int n_live_leaves = 0;
     std::vector<int32_t> h_alpha;
@@ -1432,6 +1482,8 @@ struct Search {
     DBuf<double> hd;
     unsigned long long hits = 0;
     int max_qlen = 0;
+    bool use_cache = false;
+    bool cache_hits = false;
     int64_t peak = 0;
     int64_t limits[64] = {0};
     bool prof = false;
@@ -1743,6 +1795,46 @@ struct Search {
         process(1, root.p, nq);
     }
 
+    template <int MET>
+    void launch_cache_scan()
+    {
+        CacheView cv{ix->cache_n, ix->cache_ids.p, ix->cache_vec32.p, ix->cache_vec64.p, ix->cache_words.p,
+                     ix->cache_sword.p, ix->cache_slen.p};
+        HitBuf hb{hq.p, he.p, hd.p, (unsigned long long)hq.n, counter.p + 1};
+        k_cache_scan<MET><<<grid_for((int64_t)nq * cv.n, 256), 256, 0, st>>>(iv, qv, cv, (int)nq, r32.p, r64.p, hb);
+        LAUNCH_CHECK();
+    }
+
+    // the pending-insert cache after the tree (the radius is final for kNN)
+    void scan_cache()
+    {
+        if (!use_cache || ix->cache_n == 0 || nq == 0) return;
+        const unsigned long long before = hits;
+        for (int attempt = 0; attempt < 2; attempt++) {
+            h_counter[1] = before;
+            CK(cudaMemcpyAsync(counter.p + 1, h_counter + 1, sizeof(unsigned long long), cudaMemcpyHostToDevice, st));
+            switch (ix->metric) {
+            case GTS_EDIT: launch_cache_scan<kMetricEdit>(); break;
+            case GTS_L1: launch_cache_scan<kMetricL1>(); break;
+            default: launch_cache_scan<kMetricL2>(); break;
+            }
+            const unsigned long long after = read_counter(1);
+            if (after <= hq.n) { cache_hits = after > before; hits = after; return; }
+            const size_t ncap = (size_t)after * 2;
+            DBuf<int32_t> nq_(ncap, st), ne_(ncap, st);
+            DBuf<double> nd_(ncap, st);
+            if (before) {
+                CK(cudaMemcpyAsync(nq_.p, hq.p, before * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+                CK(cudaMemcpyAsync(ne_.p, he.p, before * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+                CK(cudaMemcpyAsync(nd_.p, hd.p, before * sizeof(double), cudaMemcpyDeviceToDevice, st));
+            }
+            hq = std::move(nq_);
+            he = std::move(ne_);
+            hd = std::move(nd_);
+        }
+        fail(GTS_ECUDA, "cache scan: hit buffer growth failed");
+    }
+
     // sort hits by (q, d, id) and build the CSR result (search.py:298-314)
     void collect(gts_result *res)
     {
@@ -1781,7 +1873,7 @@ struct Search {
         while ((1ll << dbits) <= (long long)std::max(ix->max_len, max_qlen)) dbits++;
         int rbits = 1;
         while ((1ll << rbits) < ix->n) rbits++;
-        const bool packed = ix->metric == GTS_EDIT && qbits + dbits + rbits <= 64;
+        const bool packed = ix->metric == GTS_EDIT && qbits + dbits + rbits <= 64 && !cache_hits;
         if (n > 0 && packed) {
             DBuf<unsigned long long> ka((size_t)n, st), kb((size_t)n, st);
             perm_a.alloc((size_t)n, st);
@@ -1803,7 +1895,7 @@ struct Search {
             perm_a.alloc((size_t)n, st);
             perm_b.alloc((size_t)n, st);
             const unsigned g = grid_for(n, 256);
-            k_gather_id<<<g, 256, 0, st>>>(he.p, n, ix->ids.p, ka.p, perm_a.p);
+            k_gather_id<<<g, 256, 0, st>>>(he.p, n, ix->ids.p, ix->cache_ids.p, ka.p, perm_a.p);
             LAUNCH_CHECK();
             size_t tmp_bytes = 0, t2 = 0;
             cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, ka.p, kb.p, perm_a.p, perm_b.p, (int)n, 0, 64, st);
@@ -1845,7 +1937,7 @@ struct Search {
         CK(cudaMemcpyAsync(res->offsets.p, out_off.p, sizeof(long long) * (nq + 1), cudaMemcpyDeviceToDevice, st));
         if (n > 0) {
             k_emit<<<grid_for(n, 256), 256, 0, st>>>(perm_b.p, hq.p, he.p, hd.p, in_off.p, out_off.p, outcnt.p,
-                                                     ix->ids.p, n, res->ids.p, res->dis.p);
+                                                     ix->ids.p, ix->cache_ids.p, n, res->ids.p, res->dis.p);
             LAUNCH_CHECK();
         }
     }
@@ -1938,7 +2030,7 @@ static double now_ms()
 }
 
 gts_result *run_search(gts_index *ix, const gts_queries *q, int mode, const double *radii, const int64_t *ks,
-                       int64_t memory_units, int pruning, cudaStream_t st)
+                       int64_t memory_units, int pruning, cudaStream_t st, bool use_cache = false)
 {
     static const bool trace = std::getenv("GTS_TRACE") != nullptr;
     const double t0 = trace ? now_ms() : 0.0;
@@ -1974,15 +2066,16 @@ gts_result *run_search(gts_index *ix, const gts_queries *q, int mode, const doub
         }
         s.ks.alloc((size_t)std::max<int64_t>(nq, 1), st);
         h2d(s.ks.p, hk.data(), (size_t)nq, st);
-        if (!pruning) {
-            std::vector<float> inf32((size_t)nq, INFINITY);
-            std::vector<double> inf64((size_t)nq, INFINITY);
-            h2d(s.r32.p, inf32.data(), (size_t)nq, st);
-            h2d(s.r64.p, inf64.data(), (size_t)nq, st);
-        }
+        // +inf until the probe (if any) estimates a radius
+        std::vector<float> inf32((size_t)nq, INFINITY);
+        std::vector<double> inf64((size_t)nq, INFINITY);
+        h2d(s.r32.p, inf32.data(), (size_t)nq, st);
+        h2d(s.r64.p, inf64.data(), (size_t)nq, st);
     }
     const double t1 = trace ? now_ms() : 0.0;
+    s.use_cache = use_cache;
     s.run();
+    s.scan_cache();
     const double t2 = trace ? now_ms() : 0.0;
     {
         const unsigned long long want = s.hits + s.hits / 4;
@@ -2421,6 +2514,66 @@ extern "C" int gts_knn_batch_host(gts_index *ix, const gts_query_batch *qb, cons
         throw;
     }
     delete q;
+    return GTS_OK;
+    ABI_END
+}
+
+extern "C" int gts_batch_host(gts_index *ix, const gts_query_batch *qb, int mode, const double *radii,
+                              const int64_t *ks, int64_t memory_units, int flags, void *stream, gts_result **out)
+{
+    ABI_BEGIN
+    if (!ix || !out) fail(GTS_EINVAL, "null argument");
+    if (mode != 0 && mode != 1) fail(GTS_EINVAL, "mode must be 0 (range) or 1 (knn)");
+    gts_queries *q = upload_queries(ix, qb, (cudaStream_t)stream);
+    try {
+        *out = run_search(ix, q, mode, radii, ks, memory_units, (flags & GTS_FLAG_PRUNING) ? 1 : 0,
+                          (cudaStream_t)stream, (flags & GTS_FLAG_CACHE) != 0);
+    } catch (...) {
+        delete q;
+        throw;
+    }
+    delete q;
+    return GTS_OK;
+    ABI_END
+}
+
+extern "C" int gts_index_cache_set(gts_index *ix, const gts_dataset *items, void *stream)
+{
+    ABI_BEGIN
+    if (!ix || !items) fail(GTS_EINVAL, "null argument");
+    CK(cudaSetDevice(ix->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t n = items->n;
+    ix->cache_n = 0;
+    if (n == 0) return GTS_OK;
+    if (n > (1 << 30)) fail(GTS_EINVAL, "cache too large");
+    if (items->metric != ix->metric) fail(GTS_EMETRIC, "cache metric %d != index metric %d", items->metric, ix->metric);
+    ix->cache_ids.alloc((size_t)n, st);
+    h2d(ix->cache_ids.p, items->ids, (size_t)n, st);
+    if (ix->metric == GTS_EDIT) {
+        const auto &alpha = ix->h_alpha;
+        bool missing = false;
+        std::vector<uint32_t> words, wstart;
+        std::vector<int32_t> lens;
+        pack_words(n, items->offsets, [&](int64_t k) {
+            auto it = std::lower_bound(alpha.begin(), alpha.end(), items->codes[k]);
+            if (it == alpha.end() || *it != items->codes[k]) { missing = true; return 0u; }
+            return (uint32_t)(it - alpha.begin());
+        }, words, wstart, lens);
+        if (missing) return set_error(GTS_EREBUILD, "cache holds a symbol outside the index alphabet");
+        ix->cache_words.alloc(words.size(), st);
+        h2d(ix->cache_words.p, words.data(), words.size(), st);
+        ix->cache_sword.alloc(wstart.size(), st);
+        h2d(ix->cache_sword.p, wstart.data(), wstart.size(), st);
+        ix->cache_slen.alloc(lens.size(), st);
+        h2d(ix->cache_slen.p, lens.data(), lens.size(), st);
+    } else {
+        if (items->dim != ix->D) fail(GTS_EMETRIC, "cache dimensionality %lld != %d", (long long)items->dim, ix->D);
+        ix->cache_vec64.alloc((size_t)(n * ix->D), st);
+        h2d(ix->cache_vec64.p, items->vectors, (size_t)(n * ix->D), st);
+    }
+    CK(cudaStreamSynchronize(st));
+    ix->cache_n = (int)n;
     return GTS_OK;
     ABI_END
 }

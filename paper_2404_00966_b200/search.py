@@ -129,7 +129,8 @@ class BatchSearcher:
     rows, the reference's CPU default being 1<<20), pruning.
     """
 
-    def __init__(self, tree, runtime=None, memory_units=None, pruning=True, device=0):
+    def __init__(self, tree, runtime=None, memory_units=None, pruning=True, device=0, _use_cache=False):
+        self._use_cache = _use_cache
         self.tree = tree
         self.ds = tree.dataset
         self.rt = runtime
@@ -204,11 +205,10 @@ class BatchSearcher:
         dev = tree.device_index(self.device)
         L = _lib.lib()
         h = C.c_void_p()
-        if mode == RANGE:
-            rc = L.gts_range_batch_host(dev.h, C.byref(qb), _lib.ptr(radii, _lib._f64p), self.capacity,
-                                        int(bool(self.pruning)), None, C.byref(h))
-        else:
-            rc = L.gts_knn_batch_host(dev.h, C.byref(qb), _lib.ptr(ks, _lib._i64p), self.capacity,
-                                      int(bool(self.pruning)), None, C.byref(h))
+        flags = (_lib.FLAG_PRUNING if self.pruning else 0) | (_lib.FLAG_CACHE if self._use_cache else 0)
+        rc = L.gts_batch_host(dev.h, C.byref(qb), 0 if mode == RANGE else 1,
+                              _lib.ptr(radii, _lib._f64p) if radii is not None else None,
+                              _lib.ptr(ks, _lib._i64p) if ks is not None else None,
+                              self.capacity, flags, None, C.byref(h))
         _lib.check(rc)
         return _fetch(h, nq)

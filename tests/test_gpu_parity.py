@@ -290,3 +290,55 @@ def test_l2_tensor_core_path_exact(dim, clustered):
     radii = rng.uniform(0.2, 0.9, 200) * (1.0 if clustered else np.sqrt(dim / 6.0))
     check_against_oracle(ds, tree, list(q), O.Payloads(O.L2, vec=mat), O.Payloads(O.L2, vec=q), radii,
                          rng.integers(1, 30, 200))
+
+
+def test_streaming_index_vectors_and_new_symbols():
+    """Device pending-insert cache: L2 vectors, and strings whose inserts bring
+    symbols the index alphabet lacks (the pair-distance fallback)."""
+    rng = np.random.default_rng(12)
+    mat = f32(P.generate_uniform(2000, 8, seed=3))
+    si = P.StreamingIndex(P.Dataset.from_vectors(mat, P.L2), P.TreeConfig(6, 0), cache_capacity=200)
+    live = {i: mat[i] for i in range(2000)}
+    nid = 5000
+    for step in range(4):
+        for oid in rng.choice(sorted(live), 25, replace=False):
+            si.delete(int(oid))
+            del live[int(oid)]
+        for _ in range(40):
+            v = f32(rng.uniform(0, 1, 8))
+            si.insert(nid, v)
+            live[nid] = v
+            nid += 1
+        # re-insert a deleted id with a new payload (the tombstone hides the stale entry)
+        q = f32(rng.uniform(0, 1, (12, 8)))
+        ids = np.array(sorted(live), dtype=np.int64)
+        od = O.Payloads(O.L2, vec=np.array([live[i] for i in ids]), ids=ids)
+        oq = O.Payloads(O.L2, vec=q)
+        got, _ = si.query_range(list(q), 0.3)
+        want = O.brute(od, oq, O.RANGE, radii=np.full(12, 0.3))
+        c, i, d = csr(got)
+        assert np.array_equal(i, want.ids) and np.array_equal(d, want.dis)
+        got, _ = si.query_knn(list(q), 9)
+        want = O.brute(od, oq, O.KNN, ks=np.full(12, 9))
+        c, i, d = csr(got)
+        assert np.array_equal(i, want.ids) and np.array_equal(d, want.dis)
+    # strings: a pending insert with a symbol outside the alphabet
+    strs = P.generate_sequences(500, seed=4, min_len=5, max_len=15, alphabet="ACGT")
+    si = P.StreamingIndex(P.Dataset.from_strings(strs, P.EDIT), P.TreeConfig(5, 0), cache_capacity=50)
+    si.insert(900, "ACGTZZ")
+    si.insert(901, "ACGTAC")
+    si.delete(3)
+    live = {i: s for i, s in enumerate(strs) if i != 3}
+    live.update({900: "ACGTZZ", 901: "ACGTAC"})
+    ids = np.array(sorted(live), dtype=np.int64)
+    q = ["ACGTZZ", "ACG", "TTTTT", "Z"]
+    od = O.Payloads.from_strings([live[i] for i in ids], ids=ids)
+    oq = O.Payloads.from_strings(q)
+    got, _ = si.query_knn(q, 5)
+    want = O.brute(od, oq, O.KNN, ks=np.full(4, 5))
+    c, i, d = csr(got)
+    assert np.array_equal(i, want.ids) and np.array_equal(d, want.dis)
+    got, _ = si.query_range(q, 3.0)
+    want = O.brute(od, oq, O.RANGE, radii=np.full(4, 3.0))
+    c, i, d = csr(got)
+    assert np.array_equal(i, want.ids) and np.array_equal(d, want.dis)
