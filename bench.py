@@ -45,6 +45,9 @@ WORKLOADS = {
     # configs[3] (static part): DNA len 108
     "dna": dict(metric="edit", n=1_000_000, nq=10_000, min_len=108, max_len=108, alphabet="ACGT",
                 radius=8.0, k=10, config_index=3),
+    # configs[3] streaming: per step 1,000 deletes + 1,000 re-inserts, then the batch
+    "dna_stream": dict(metric="edit", n=1_000_000, nq=10_000, min_len=108, max_len=108, alphabet="ACGT",
+                       radius=8.0, k=10, config_index=3, updates=1000, cache_capacity=4096),
     # configs[0]: T-Loc-like 2-D L2, CPU-reference-runnable
     "tloc": dict(metric="l2", n=100_000, nq=1_000, dim=2, radius=0.0582588, k=10, config_index=0),
     # configs[2]: 128-d L2 n=1M, kNN k=10, 100k-query batch (clustered)
@@ -265,6 +268,69 @@ class Engine:
     def free(self, hs):
         for h in hs:
             self.L.gts_result_free(h)
+
+
+def run_stream(args, rank, world, local_rank):
+    """configs[3]: StreamingIndex (the user-facing API) on 1M DNA strings; a
+    step = 1,000 deletes + 1,000 re-inserts of the same ids with mutated
+    payloads, then one 10k-query range (r=8) + kNN (k=10) batch over the live
+    set (tree minus tombstones plus the device pending cache; a cache overflow
+    rebuilds inside the step, as updates.py:121 does)."""
+    import torch
+    import paper_2404_00966_b200 as P
+    from paper_2404_00966_b200 import _lib
+    torch.cuda.set_device(local_rank)
+    w = make_workload("dna_stream", rank, args)
+    codes, off = w["codes"], w["off"]
+    alpha = w["alphabet"]
+    strs = ["".join(map(chr, codes[off[i]:off[i + 1]])) for i in range(off.size - 1)]
+    q = ["".join(map(chr, w["qcodes"][w["qoff"][i]:w["qoff"][i + 1]])) for i in range(w["nq"])]
+    t0 = time.perf_counter()
+    si = P.StreamingIndex(P.Dataset.from_strings(strs, P.EDIT, ids=w["ids"]), P.TreeConfig(20, 0),
+                          cache_capacity=w["cache_capacity"])
+    build_s = time.perf_counter() - t0
+    rng = np.random.default_rng(5)
+    live = set(int(i) for i in w["ids"])
+
+    def step():
+        dels = rng.choice(sorted(live)[:200_000], w["updates"], replace=False)
+        ins = []
+        for oid in dels:
+            s_ = list(strs[int(oid) - int(w["ids"][0])])
+            for _ in range(3):
+                s_[int(rng.integers(0, len(s_)))] = alpha[int(rng.integers(0, len(alpha)))]
+            ins.append((int(oid), "".join(s_)))
+        si.batch_update(inserts=ins, deletes=[int(x) for x in dels])
+        a, _ = si.query_range(q, w["radius"])
+        b, _ = si.query_knn(q, w["k"])
+        return sum(x[0].size for x in a) + sum(x[0].size for x in b)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches0 = _lib.launch_count()
+    rb0 = si.rebuild_count
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize()
+    ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    if rank != 0:
+        return None
+    nq = w["nq"]
+    return {
+        "metric": "range+kNN queries/sec (streaming)", "value": round(2 * nq / (ms / 1e3), 3), "unit": "queries/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8 symbols / int32 bit-parallel DP",
+        "data": "synthetic",
+        "config": {"workload": "dna_stream (BASELINE.json configs[3])", "n_per_gpu": w["n"], "nq": nq,
+                   "radius": w["radius"], "k": w["k"], "updates_per_step": f"{w['updates']} deletes + {w['updates']} re-inserts",
+                   "cache_capacity": w["cache_capacity"],
+                   "timing": "wall clock around whole steps through the Python StreamingIndex API (updates, "
+                             "H2D of the batch, search of tree + device cache, D2H of answers, rebuilds)"},
+        "rebuilds_in_timed_steps": si.rebuild_count - rb0, "initial_build_s": round(build_s, 2),
+        "gpu_launches": int(_lib.launch_count() - launches0),
+    }
 
 
 def run_ours(args, rank, world, local_rank):
@@ -596,7 +662,7 @@ def main():
             torch.cuda.set_device(local_rank)
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             dist.init_process_group("nccl")
-        out = run_ours(args, rank, world, local_rank)
+        out = (run_stream if args.workload == "dna_stream" else run_ours)(args, rank, world, local_rank)
         if world > 1:
             import torch.distributed as dist
             dist.destroy_process_group()
