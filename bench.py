@@ -26,9 +26,7 @@ import ctypes as C
 import json
 import os
 import statistics
-import subprocess
 import sys
-import tempfile
 import time
 
 import numpy as np
@@ -136,53 +134,78 @@ def make_workload(name, rank, args):
 # ---------------------------------------------------------------------------
 
 class ClockSampler:
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clocks + throttle reasons sampled DURING the timed region.
+
+    In-process NVML (pynvml) polled from a thread: NVML is initialised when the
+    sampler is created (before warm-up), so no nvidia-smi start-up (driver init,
+    seconds-long lock hold) ever lands inside a timed step."""
+
+    REASONS = (("hw_slowdown", 0x8), ("sw_thermal_slowdown", 0x20), ("hw_thermal_slowdown", 0x40),
+               ("sw_power_cap", 0x4), ("hw_power_brake_slowdown", 0x80))
 
     def __init__(self, gpu_index, interval_ms=200):
-        self.gpu = gpu_index
-        self.interval_ms = interval_ms
-        self.proc = None
-        self.path = tempfile.mktemp(suffix=".csv")
+        import threading
+        self.interval = interval_ms / 1e3
+        self.samples = []
+        self.on = threading.Event()
+        self.quit = threading.Event()
+        self.err = None
+        self.call_ms = []
+        self.mode = os.environ.get("GTS_CLOCK_MODE", "full")   # full | clock | none (diagnostics)
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[gpu_index]) if vis and vis.split(",")[0].isdigit() else gpu_index
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.smax = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            pynvml.nvmlDeviceGetClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # noqa: BLE001
+            self.nv = None
+            self.err = f"nvml unavailable: {e}"
+        self.th = threading.Thread(target=self._run, daemon=True)
+        self.th.start()
+
+    def _sample(self):
+        t0 = time.perf_counter()
+        sm = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+        t1 = time.perf_counter()
+        rs = 0 if self.mode == "clock" else self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        t2 = time.perf_counter()
+        self.call_ms.append((round((t1 - t0) * 1e3, 2), round((t2 - t1) * 1e3, 2)))
+        return sm, rs
+
+    def _run(self):
+        while not self.quit.is_set():
+            if self.on.is_set() and self.nv is not None and self.mode != "none":
+                try:
+                    self.samples.append(self._sample())
+                except Exception as e:  # noqa: BLE001
+                    self.err = str(e)
+            self.quit.wait(self.interval)
 
     def start(self):
-        try:
-            self.fh = open(self.path, "w")
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", str(self.interval_ms)], stdout=self.fh, stderr=subprocess.DEVNULL)
-        except Exception:
-            self.proc = None
+        self.samples = []
+        self.on.set()
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        self.fh.close()
-        sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.path):
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 9:
-                continue
+        self.on.clear()
+        # one sample right at the end so even a short timed region has one
+        if self.nv is not None and self.mode != "none":
             try:
-                sm.append(float(parts[1]))
-                smax.append(float(parts[2]))
-            except ValueError:
-                continue
-            for nm, val in zip(names, parts[5:9]):
-                if val.lower().startswith("active"):
-                    reasons.add(nm)
-        os.unlink(self.path)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
-                "samples": len(sm)}
+                self.samples.append(self._sample())
+            except Exception:  # noqa: BLE001
+                pass
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [self.err or "no samples"], "samples": 0}
+        reasons = sorted({nm for _, r in self.samples for nm, bit in self.REASONS if r & bit})
+        return {"sm_mhz": statistics.median(s for s, _ in self.samples), "sm_max_mhz": self.smax,
+                "reasons": reasons, "samples": len(self.samples), "source": "nvml (in-process)",
+                "nvml_call_ms_max": max((a + b for a, b in self.call_ms), default=None)}
+
+    def close(self):
+        self.quit.set()
 
 
 # ---------------------------------------------------------------------------
@@ -305,16 +328,20 @@ def run_stream(args, rank, world, local_rank):
         b, _ = si.query_knn(q, w["k"])
         return sum(x[0].size for x in a) + sum(x[0].size for x in b)
 
+    clocks = ClockSampler(local_rank, args.clock_ms)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     launches0 = _lib.launch_count()
     rb0 = si.rebuild_count
+    clocks.start()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         step()
     torch.cuda.synchronize()
     ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    clk = clocks.stop()
+    clocks.close()
     if rank != 0:
         return None
     nq = w["nq"]
@@ -328,7 +355,7 @@ def run_stream(args, rank, world, local_rank):
                    "cache_capacity": w["cache_capacity"],
                    "timing": "wall clock around whole steps through the Python StreamingIndex API (updates, "
                              "H2D of the batch, search of tree + device cache, D2H of answers, rebuilds)"},
-        "rebuilds_in_timed_steps": si.rebuild_count - rb0, "initial_build_s": round(build_s, 2),
+        "clocks": clk, "rebuilds_in_timed_steps": si.rebuild_count - rb0, "initial_build_s": round(build_s, 2),
         "gpu_launches": int(_lib.launch_count() - launches0),
     }
 
@@ -362,6 +389,7 @@ def run_ours(args, rank, world, local_rank):
                 merger.merge_handles(eng, hs, eng.ks, sp)
         eng.free(hs)
 
+    clocks = ClockSampler(local_rank, args.clock_ms)
     # warm-up
     for _ in range(args.warmup):
         one_step()
@@ -380,9 +408,7 @@ def run_ours(args, rank, world, local_rank):
     eng.free(hs)
 
     # timed region (value): inputs resident in HBM
-    clocks = ClockSampler(local_rank, args.clock_ms)
     clocks.start()
-    time.sleep(0.3)
     barrier()
     torch.cuda.synchronize()
     launches0 = _lib.launch_count()
@@ -402,6 +428,7 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     launches = _lib.launch_count() - launches0
     clk = clocks.stop()
+    clocks.close()
     ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:
         t = torch.tensor([ms], device="cuda")
@@ -414,7 +441,10 @@ def run_ours(args, rank, world, local_rank):
     if rank != 0:
         return None
     qps = 2 * nq * world / (ms / 1e3)
-    kver = prof["kernels"].get("k_leaf_edit" if eng.edit else "k_verify", {"ms": 0.0, "count": 0})
+    # the dominant leaf-verification kernel of this workload (whichever ran)
+    cands = ("k_leafgroup_edit", "k_leaf_edit") if eng.edit else ("k_leafgroup_mma", "k_leafgroup_vec", "k_verify")
+    kname = max(cands, key=lambda k: prof["kernels"].get(k, {"ms": 0.0})["ms"])
+    kver = dict(prof["kernels"].get(kname, {"ms": 0.0, "count": 0}), name=kname)
     work = prof["work"]
     step_ms_prof = sum(v["ms"] for v in prof["kernels"].values())
     out = {
@@ -516,38 +546,50 @@ def run_e2e(eng, w, args, sp, merger, world, max_total):
 
 
 def roofline(eng, prof, kver, step_ms_prof):
+    """Roofline of the dominant kernel.  achieved = ALGORITHMIC work of the
+    step / that kernel's device time (CUDA events around each
+    launch, profiling pass); peak = MEASURED_PEAKS.json, else the measured
+    integer peak (edit) or the B200_PROFILING.md fallback."""
     from paper_2404_00966_b200 import _lib
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     peaks = json.load(open(peaks_path)) if os.path.exists(peaks_path) else {}
     work = prof["work"]
     t = kver["ms"] / 1e3 if kver["ms"] else None
     share = kver["ms"] / step_ms_prof if step_ms_prof else None
+    common = {"kernel": kver["name"], "kernel_ms_per_step": round(kver["ms"], 4),
+              "kernel_launches_per_step": kver["count"], "kernel_share_of_step": round(share, 4) if share else None,
+              "pairs_per_step": work["pairs"], "entries_scanned_per_step": work["entries"]}
     if eng.edit:
         ops = C.c_double()
         _lib.check(_lib.lib().gts_bench_int_peak(C.byref(ops), None))
         peak = ops.value / 1e12
         achieved = work["word_steps"] * OPS_PER_WORD_STEP / t / 1e12 if t else None
-        return {
-            "bound": "int", "kernel": "k_leaf_edit (fused leaf scan + bit-parallel Myers/Hyyro DP, 32-bit words)",
-            "achieved": round(achieved, 3) if achieved else None, "peak": round(peak, 3), "unit": "Tops/s",
-            "frac": round(achieved / peak, 4) if achieved else None,
-            "traffic": None,
+        return dict(common, **{
+            "bound": "int", "achieved": round(achieved, 3) if achieved else None, "peak": round(peak, 3),
+            "unit": "Tops/s", "frac": round(achieved / peak, 4) if achieved else None, "traffic": None,
             "work_unit": f"word-step = one text symbol x one 32-bit pattern word = {OPS_PER_WORD_STEP} int ops "
-                         "(the minimal Hyyro recurrence; executed SASS is ~14/step incl. symbol extract + LDS)",
-            "word_steps_per_step": work["word_steps"], "pairs_per_step": work["pairs"],
-            "kernel_ms_per_step": round(kver["ms"], 4), "kernel_launches_per_step": kver["count"],
-            "kernel_share_of_step": round(share, 4) if share else None,
-            "peak_source": "gts_bench_int_peak: LOP3+IMAD chains on all SMs, measured in this run "
-                           "(MEASURED_PEAKS.json has no integer peak)",
-        }
-    hbm = peaks.get("hbm_gbs", 6650.0)
+                         "(the minimal Hyyro recurrence: 7 LOP3 + 1 add + 2 shifts)",
+            "word_steps_per_step": work["word_steps"],
+            "peak_source": "gts_bench_int_peak: best of LOP3-only / IMAD-only / mixed 16-chain loops on all SMs, "
+                           "measured in this run (MEASURED_PEAKS.json has no integer peak)"})
     D = eng.w.get("dim", 2)
+    if kver["name"] == "k_leafgroup_mma":
+        tf = peaks.get("bf16_tflops_sustained") or peaks.get("bf16_tflops") or 1590.0
+        flops = work["pairs"] * 2 * D
+        achieved = flops / t / 1e12 if t else None
+        return dict(common, **{
+            "bound": "tensor", "achieved": round(achieved, 3) if achieved else None, "peak": tf,
+            "unit": "TFLOP/s", "frac": round(achieved / tf, 5) if achieved else None, "traffic": None,
+            "work_unit": f"2*D = {2 * D} bf16 tensor flops per lemma-1-passing (query, entry) pair",
+            "peak_source": "MEASURED_PEAKS.json bf16" if peaks else "fallback 1590 TFLOP/s (B200_PROFILING.md)"})
+    hbm = peaks.get("hbm_gbs", 6650.0)
     bytes_alg = work["entries"] * 8 + work["pairs"] * 4 * D
     achieved = bytes_alg / t / 1e9 if t else None
-    return {"bound": "hbm", "kernel": "k_verify<l2>", "achieved": round(achieved, 2) if achieved else None,
-            "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4) if achieved else None, "traffic": None,
-            "kernel_ms_per_step": round(kver["ms"], 4), "kernel_share_of_step": round(share, 4) if share else None,
-            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"}
+    return dict(common, **{
+        "bound": "hbm", "achieved": round(achieved, 2) if achieved else None, "peak": hbm, "unit": "GB/s",
+        "frac": round(achieved / hbm, 4) if achieved else None, "traffic": None,
+        "work_unit": "8 B per (query, entry) scanned + 4*D B per lemma-1-passing pair",
+        "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s (B200_PROFILING.md)"})
 
 
 # Algorithmic integer ops per word-step: the 10-op Hyyro recurrence (DESIGN.md).

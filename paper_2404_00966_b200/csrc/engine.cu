@@ -572,19 +572,270 @@ __global__ void k_leaf_scatter(const Row *rows, int64_t m, int leaf_first, int *
     }
 }
 
-__global__ void k_item_counts(const int *cnt, int nleaf, int *nitem)
+__global__ void k_item_counts(const int *cnt, int nleaf, int per, int *nitem)
 {
     int l = blockIdx.x * blockDim.x + threadIdx.x;
-    if (l < nleaf) nitem[l] = (cnt[l] + kItemQueries - 1) / kItemQueries;
+    if (l < nleaf) nitem[l] = (cnt[l] + per - 1) / per;
 }
 
-__global__ void k_make_items(const int *cnt, const int *off, const int *item_off, int nleaf, int leaf_first, Item *items)
+__global__ void k_make_items(const int *cnt, const int *off, const int *item_off, int nleaf, int leaf_first, int per,
+                             Item *items)
 {
     int l = blockIdx.x * blockDim.x + threadIdx.x;
     if (l >= nleaf) return;
     const int c = cnt[l];
-    for (int j = 0, s = 0; s < c; j++, s += kItemQueries)
-        items[item_off[l] + j] = Item{leaf_first + l, off[l] + s, min(kItemQueries, c - s), 0};
+    for (int j = 0, s = 0; s < c; j++, s += per)
+        items[item_off[l] + j] = Item{leaf_first + l, off[l] + s, min(per, c - s), 0};
+}
+
+// ---------------------------------------------------------------------------
+// Leaf-grouped edit verification (the words / DNA hot kernel).  Rows are
+// grouped by leaf into items of <= kItemQueries rows (k_leaf_hist /
+// k_leaf_scatter above).  A block stages one leaf -- pivot distances,
+// lengths, alive bits, symbol histograms and the packed text -- in shared
+// memory ONCE, and every query row of the item scans it from there: a leaf
+// costs one L2 read per item instead of one per (query, entry) pair (kNN
+// over 1M words visits ~all 8,000 leaves from every query).  Each warp takes
+// kLgSlots rows at a time, stages their match masks, and feeds the
+// candidates of all of them into one warp queue, so 32-lane DP batches stay
+// full even when a row has only a few candidates.  Filters and counters are
+// those of k_leaf_edit (search.py:507-570): the lemma-1 pivot test is the
+// reference's "verified", then the |len q - len o| and symbol-histogram
+// lower bounds, then the exact bit-parallel DP with the text read from
+// shared memory.
+// ---------------------------------------------------------------------------
+constexpr int kLgSlots = 4;        // rows (queries) a warp has in flight
+constexpr int kLgWarps = 8;
+constexpr int kLgItemRows = 512;   // rows per item: leaf staging amortised over 512 rows
+
+struct LgEditLayout {              // shared-memory carve-up in bytes (host-computed)
+    int cap_e, cap_w;              // staged entries / text words per leaf
+    int wmax, slot_words;          // pattern words (<= 4); words per staged slot (wmax * A, padded)
+    int use_hist;
+    int off_meta, off_h0, off_h1, off_text, off_peq, off_queue, off_slot, total;
+    uint32_t two;                  // the constant 2, opaque to ptxas (see myers_smem)
+};
+
+// Shared-memory layouts are chosen for conflict-free LDS:
+//   text    entry k at word k * tstride (tstride odd), so the byte loads of
+//           32 lanes on 32 different entries spread over the banks;
+//   hist    two uint4 arrays (16-byte stride) instead of one 32-byte record;
+//   masks   per slot block-major [W][A], slots padded to an odd multiple
+//           of 8 words apart.
+__global__ void __launch_bounds__(32 * kLgWarps, 4)
+k_leafgroup_edit(IndexView ix, QueryView qv, const Row *__restrict__ srows, const Item *__restrict__ items, int nitems,
+                 unsigned long long *item_cursor, LgEditLayout L, int pruning, float *r32, HitBuf out,
+                 unsigned long long *verified_stat, int stats_on, unsigned long long *work, unsigned *hist,
+                 const int32_t *__restrict__ ks)
+{
+    extern __shared__ uint4 lg_smem4[];
+    char *sm = reinterpret_cast<char *>(lg_smem4);
+    float *dis_s = reinterpret_cast<float *>(sm);
+    uint32_t *meta_s = reinterpret_cast<uint32_t *>(sm + L.off_meta);   // len | alive << 31
+    uint4 *h0_s = reinterpret_cast<uint4 *>(sm + L.off_h0);
+    uint4 *h1_s = reinterpret_cast<uint4 *>(sm + L.off_h1);
+    uint32_t *text_s = reinterpret_cast<uint32_t *>(sm + L.off_text);
+    const int lane = lane_id(), warp = threadIdx.x >> 5;
+    uint32_t *peq_w = reinterpret_cast<uint32_t *>(sm + L.off_peq) + (size_t)warp * kLgSlots * L.slot_words;
+    int32_t *qk = reinterpret_cast<int32_t *>(sm + L.off_queue) + warp * 64;        // slot << 16 | entry
+    int32_t *slot_q = reinterpret_cast<int32_t *>(sm + L.off_slot) + warp * 4 * kLgSlots;
+    int32_t *slot_m = slot_q + kLgSlots;
+    int32_t *slot_w = slot_m + kLgSlots;
+    float *slot_r = reinterpret_cast<float *>(slot_w + kLgSlots);
+    __shared__ int item_s, group_s, tstride_s;
+    const int A = qv.A;
+    unsigned long long steps = 0, pairs = 0, entries = 0, nrows = 0;
+
+    for (;;) {
+        __syncthreads();   // the previous leaf is no longer read
+        if (threadIdx.x == 0) {
+            item_s = (int)atomicAdd(item_cursor, 1ull);
+            group_s = kLgWarps;
+        }
+        __syncthreads();
+        const int it = item_s;
+        if (it >= nitems) break;
+        const Item item = items[it];
+        const int size = ix.node[item.leaf].size;
+        const int pos = ix.npos[item.leaf];
+        if (size == 0) continue;
+        // entries are length-sorted inside a leaf: the last is the longest
+        const int tstride = ((__ldg(ix.slen + pos + size - 1) + 3) >> 2) | 1;
+        for (int k = threadIdx.x; k < size; k += blockDim.x) {
+            const int e = pos + k;
+            const uint4 rec = __ldg(ix.erec + e);
+            const uint32_t al = (__ldg(ix.alive + (e >> 5)) >> (e & 31)) & 1u;
+            dis_s[k] = __uint_as_float(rec.x);
+            meta_s[k] = rec.y | (al << 31);
+            if (L.use_hist) {
+                h0_s[k] = __ldg(ix.ehist + 2 * e);
+                h1_s[k] = __ldg(ix.ehist + 2 * e + 1);
+            }
+        }
+        for (int t = threadIdx.x; t < size * tstride; t += blockDim.x) {
+            const int k = t / tstride, w = t - k * tstride;
+            const int e = pos + k;
+            if (w < ((__ldg(ix.slen + e) + 3) >> 2)) text_s[t] = __ldg(ix.str + __ldg(ix.sword + e) + w);
+        }
+        __syncthreads();
+
+        const int ngroups = (item.count + kLgSlots - 1) / kLgSlots;
+        // row groups: warp w starts with group w, then claims the next free one
+        for (int g = warp; g < ngroups;) {
+            const int rbase = item.start + g * kLgSlots;
+            const int ns = min(kLgSlots, item.count - g * kLgSlots);
+            float dqp_l = 0.f;
+            if (lane < ns) {
+                const Row rw = srows[rbase + lane];
+                const int m = qlen(qv, rw.q);
+                dqp_l = rw.dqp;
+                slot_q[lane] = rw.q;
+                slot_m[lane] = m;
+                slot_w[lane] = max(1, (m + 31) >> 5);
+                slot_r[lane] = __ldcg(r32 + rw.q);
+            }
+            __syncwarp();
+            // stage masks: slot s block-major [W][A] (blocks past its own W zeroed)
+            for (int s = 0; s < ns; s++) {
+                const int qs = slot_q[s], ws = (slot_m[s] + 31) >> 5;
+                const uint32_t *src = qv.peq + qv.peq_off[qs];
+                uint32_t *dst = peq_w + s * L.slot_words;
+                for (int t = lane; t < L.wmax * A; t += kWarp) {
+                    const int b = t / A, c = t - b * A;
+                    dst[t] = b < ws ? __ldg(src + c * ws + b) : 0u;
+                }
+            }
+            __syncwarp();
+            nrows += (unsigned long long)ns;
+
+            // run queued DPs [0, cnt), one per lane; emit hits; shrink kNN radii
+            auto run_batch = [&](int cnt) {
+                const bool va = lane < cnt;
+                int d = 0, k = 0, sl = 0, wl = 1;
+                if (va) {
+                    const int v = qk[lane];
+                    sl = v >> 16;
+                    k = v & 0xffff;
+                    wl = slot_w[sl];
+                }
+                const int Wb = (int)__reduce_max_sync(kFull, (unsigned)wl);   // widest pattern in the batch
+                if (va) {
+                    const int n = (int)(meta_s[k] & 0xffffu);
+                    const uint8_t *t1 = reinterpret_cast<const uint8_t *>(text_s + k * tstride);
+                    const uint32_t *pq = peq_w + sl * L.slot_words;
+                    const int ms = slot_m[sl];
+                    switch (Wb) {
+                    case 1: d = myers_smem<1>(pq, ms, t1, n, L.two, A); break;
+                    case 2: d = myers_smem<2>(pq, ms, t1, n, L.two, A); break;
+                    case 3: d = myers_smem<3>(pq, ms, t1, n, L.two, A); break;
+                    default: d = myers_smem<4>(pq, ms, t1, n, L.two, A); break;
+                    }
+                    steps += (unsigned long long)wl * (unsigned long long)n;
+                }
+                const bool hit = va && (float)d <= slot_r[sl];
+                const unsigned hb = __ballot_sync(kFull, hit);
+                if (hb) {
+                    unsigned long long hbase = 0;
+                    if (lane == 0) hbase = atomicAdd(out.counter, (unsigned long long)__popc(hb));
+                    hbase = __shfl_sync(kFull, hbase, 0);
+                    if (hit) {
+                        const unsigned long long o = hbase + __popc(hb & ((1u << lane) - 1u));
+                        if (o < out.cap) { out.q[o] = slot_q[sl]; out.e[o] = pos + k; out.d[o] = (double)d; }
+                        if (hist && d < kHistBins) atomicAdd(hist + (size_t)slot_q[sl] * kHistBins + d, 1u);
+                    }
+                    if (hist) {
+                        __syncwarp();
+                        __threadfence_block();
+                        for (int s = 0; s < ns; s++) {
+                            if (!__any_sync(kFull, hit && sl == s)) continue;
+                            const int qs = slot_q[s];
+                            const unsigned *hq_ = hist + (size_t)qs * kHistBins;
+                            const unsigned kq = (unsigned)ks[qs];
+                            unsigned c[8], tot = 0;
+#pragma unroll
+                            for (int i = 0; i < 8; i++) { c[i] = __ldcg(hq_ + lane * 8 + i); tot += c[i]; }
+                            unsigned inc = tot;
+                            for (int o = 1; o < 32; o <<= 1) {
+                                const unsigned v = __shfl_up_sync(kFull, inc, o);
+                                if (lane >= o) inc += v;
+                            }
+                            const unsigned before = inc - tot;
+                            int t = kHistBins;
+                            if (before < kq && inc >= kq) {
+                                unsigned run = before;
+#pragma unroll
+                                for (int i = 0; i < 8; i++) {
+                                    run += c[i];
+                                    if (run >= kq) { t = lane * 8 + i; break; }
+                                }
+                            }
+                            t = (int)__reduce_min_sync(kFull, (unsigned)t);
+                            __syncwarp();
+                            if (t < kHistBins && (float)t < slot_r[s] && lane == 0) {
+                                slot_r[s] = (float)t;
+                                atomicMin(reinterpret_cast<int *>(r32 + qs), __float_as_int((float)t));
+                            }
+                            __syncwarp();
+                        }
+                    }
+                }
+                __syncwarp();
+            };
+
+            int qn = 0;
+            for (int s = 0; s < ns; s++) {
+                const int qs = slot_q[s];
+                const int ms = slot_m[s];
+                const float dq = __shfl_sync(kFull, dqp_l, s);
+                if (hist && lane == 0) slot_r[s] = fminf(slot_r[s], __ldcg(r32 + qs));   // other blocks shrink it
+                __syncwarp();
+                uint4 qh0 = make_uint4(0u, 0u, 0u, 0u), qh1 = qh0;
+                if (L.use_hist) { qh0 = qv.qhist[2 * qs]; qh1 = qv.qhist[2 * qs + 1]; }
+                unsigned ver = 0;
+                for (int b = 0; b < size; b += kWarp) {
+                    const float rs = slot_r[s];
+                    const int k = b + lane;
+                    bool pass = false;
+                    uint32_t mt = 0;
+                    if (k < size) {
+                        mt = meta_s[k];
+                        if (mt >> 31) pass = !pruning || fabsf(dis_s[k] - dq) <= rs;
+                    }
+                    ver += __popc(__ballot_sync(kFull, pass));
+                    const int len = (int)(mt & 0xffffu);
+                    bool cand = pass && (float)abs(ms - len) <= rs;
+                    if (cand && L.use_hist) cand = (float)hist_lb(qh0, qh1, h0_s[k], h1_s[k], ms - len) <= rs;
+                    const unsigned cb = __ballot_sync(kFull, cand);
+                    if (cand) qk[qn + __popc(cb & ((1u << lane) - 1u))] = (s << 16) | k;
+                    qn += __popc(cb);
+                    __syncwarp();
+                    if (qn >= kWarp) {
+                        run_batch(kWarp);
+                        qn -= kWarp;
+                        if (lane < qn) qk[lane] = qk[kWarp + lane];
+                        __syncwarp();
+                    }
+                }
+                if (lane == 0 && stats_on && ver) atomicAdd(verified_stat + qs, (unsigned long long)ver);
+                pairs += ver;
+                entries += (unsigned long long)size;
+            }
+            if (qn) run_batch(qn);
+            __syncwarp();
+            int nx = 0;
+            if (lane == 0) nx = atomicAdd(&group_s, 1);
+            g = __shfl_sync(kFull, nx, 0);
+        }
+    }
+    if (work) {
+        for (int o = 16; o > 0; o >>= 1) steps += __shfl_down_sync(kFull, steps, o);
+        if (lane == 0) {
+            atomicAdd(work + kWorkSteps, steps);
+            atomicAdd(work + kWorkPairs, pairs);
+            atomicAdd(work + kWorkEntries, entries);
+            atomicAdd(work + kWorkRows, nrows);
+        }
+    }
 }
 
 template <int MET>
@@ -1341,6 +1592,7 @@ struct gts_index {
     int Dk = 0;
     DBuf<int32_t> alpha;
     int max_leaf = 0;
+    int max_leaf_words = 0;   // largest leaf's packed text (words), edit only
     int leaf_first = 0, leaf_count = 0;
     std::vector<int64_t> ord;   // device entry -> reference table position
     std::atomic<unsigned long long> hit_hint[2] = {{0}, {0}};   // hits of the last range / kNN call
@@ -1560,13 +1812,19 @@ struct Search {
         return b <= 200 * 1024 ? b : 0;
     }
 
-    template <int MET>
-    void launch_grouped(const Row *rows, int64_t m, int stats_on)
+    // rows grouped by leaf into items of <= kItemQueries rows (counting sort)
+    struct Grouped {
+        DBuf<Row> srows;
+        DBuf<Item> items;
+        int nitems = 0;
+    };
+
+    void group_rows(const Row *rows, int64_t m, Grouped &G, int per = kItemQueries)
     {
         const int nleaf = ix->leaf_count;
         DBuf<int> cnt((size_t)nleaf + 1, st), off((size_t)nleaf + 1, st), cur((size_t)nleaf + 1, st);
         DBuf<int> nit((size_t)nleaf + 1, st), ioff((size_t)nleaf + 1, st);
-        DBuf<Row> srows((size_t)m, st);
+        G.srows.alloc((size_t)m, st);
         CK(cudaMemsetAsync(cnt.p, 0, sizeof(int) * (nleaf + 1), st));
         k_leaf_hist<<<grid_for(m, 256), 256, 0, st>>>(rows, m, ix->leaf_first, cnt.p);
         LAUNCH_CHECK();
@@ -1575,20 +1833,91 @@ struct Search {
         DBuf<uint8_t> tmp(tb, st);
         CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, cnt.p, off.p, nleaf + 1, st));
         CK(cudaMemcpyAsync(cur.p, off.p, sizeof(int) * (nleaf + 1), cudaMemcpyDeviceToDevice, st));
-        k_leaf_scatter<<<grid_for(m, 256), 256, 0, st>>>(rows, m, ix->leaf_first, cur.p, srows.p);
+        k_leaf_scatter<<<grid_for(m, 256), 256, 0, st>>>(rows, m, ix->leaf_first, cur.p, G.srows.p);
         LAUNCH_CHECK();
-        k_item_counts<<<grid_for(nleaf, 256), 256, 0, st>>>(cnt.p, nleaf, nit.p);
+        k_item_counts<<<grid_for(nleaf, 256), 256, 0, st>>>(cnt.p, nleaf, per, nit.p);
         LAUNCH_CHECK();
         CK(cudaMemsetAsync(nit.p + nleaf, 0, sizeof(int), st));
         CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, nit.p, ioff.p, nleaf + 1, st));
         g_launches += 4;
-        int nitems = 0;
-        CK(cudaMemcpyAsync(&nitems, ioff.p + nleaf, sizeof(int), cudaMemcpyDeviceToHost, st));
+        int *h_nitems = reinterpret_cast<int *>(h_counter + 2);
+        CK(cudaMemcpyAsync(h_nitems, ioff.p + nleaf, sizeof(int), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        if (nitems == 0) return;
-        DBuf<Item> items((size_t)nitems, st);
-        k_make_items<<<grid_for(nleaf, 256), 256, 0, st>>>(cnt.p, off.p, ioff.p, nleaf, ix->leaf_first, items.p);
+        G.nitems = *h_nitems;
+        if (G.nitems == 0) return;
+        G.items.alloc((size_t)G.nitems, st);
+        k_make_items<<<grid_for(nleaf, 256), 256, 0, st>>>(cnt.p, off.p, ioff.p, nleaf, ix->leaf_first, per, G.items.p);
         LAUNCH_CHECK();
+    }
+
+    // shared-memory layout of k_leafgroup_edit for this index and batch
+    // (total == 0: does not fit, use k_leaf_edit)
+    LgEditLayout edit_layout() const
+    {
+        LgEditLayout L{};
+        const int wmax = std::max(1, (qs->max_len + 31) >> 5);
+        if (wmax > 4 || ix->max_len > 65535) return L;
+        L.cap_e = std::max(ix->max_leaf, 1);
+        L.cap_w = L.cap_e * ((((ix->max_len + 3) >> 2)) | 1);
+        L.wmax = wmax;
+        L.slot_words = ((wmax * ix->A + 7) & ~7) | 8;   // odd multiple of 8: slots land on different banks
+        L.use_hist = ix->ehist.p != nullptr;
+        L.two = 2u;
+        auto al = [](size_t x) { return (int)((x + 15) & ~(size_t)15); };
+        size_t o = al((size_t)L.cap_e * 4);
+        L.off_meta = (int)o;
+        o += al((size_t)L.cap_e * 4);
+        L.off_h0 = (int)o;
+        if (L.use_hist) o += (size_t)L.cap_e * 16;
+        L.off_h1 = (int)o;
+        if (L.use_hist) o += (size_t)L.cap_e * 16;
+        L.off_text = (int)o;
+        o += al((size_t)L.cap_w * 4);
+        L.off_peq = (int)o;
+        o += al((size_t)kLgWarps * kLgSlots * L.slot_words * 4);
+        L.off_queue = (int)o;
+        o += (size_t)kLgWarps * 64 * 4;
+        L.off_slot = (int)o;
+        o += (size_t)kLgWarps * 4 * kLgSlots * 4;
+        if (o > 100 * 1024) return LgEditLayout{};
+        L.total = (int)o;
+        return L;
+    }
+
+    void launch_grouped_edit(const Row *rows, int64_t m, int stats_on, const LgEditLayout &L)
+    {
+        Grouped G;
+        group_rows(rows, m, G, kLgItemRows);
+        if (G.nitems == 0) return;
+        HitBuf hb{hq.p, he.p, hd.p, (unsigned long long)hq.n, counter.p + 1};
+        static int attr = 0;
+        if (attr < L.total) {
+            CK(cudaFuncSetAttribute(k_leafgroup_edit, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+            attr = 100 * 1024;
+        }
+        int sms = 148, per = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_leafgroup_edit, 32 * kLgWarps, L.total));
+        const unsigned grid = (unsigned)std::min<int64_t>(G.nitems, (int64_t)sms * std::max(per, 1));
+        CK(cudaMemsetAsync(counter.p, 0, sizeof(unsigned long long), st));
+        timed("k_leafgroup_edit", [&] {
+            k_leafgroup_edit<<<grid, 32 * kLgWarps, L.total, st>>>(iv, qv, G.srows.p, G.items.p, G.nitems, counter.p, L,
+                                                                  pruning, r32.p, hb, verified.p, stats_on,
+                                                                  stats_on ? work.p : nullptr,
+                                                                  stats_on ? hist.p : nullptr, ks.p);
+        });
+        LAUNCH_CHECK();
+    }
+
+    template <int MET>
+    void launch_grouped(const Row *rows, int64_t m, int stats_on)
+    {
+        Grouped G;
+        group_rows(rows, m, G);
+        const int nitems = G.nitems;
+        if (nitems == 0) return;
+        DBuf<Row> &srows = G.srows;
+        DBuf<Item> &items = G.items;
         HitBuf hb{hq.p, he.p, hd.p, (unsigned long long)hq.n, counter.p + 1};
         const size_t sm = grouped_smem();
         if (MET == kMetricL2 && ix->vcent.p && pruning) {
@@ -1677,6 +2006,11 @@ struct Search {
     {
         switch (ix->metric) {
         case GTS_EDIT: {
+            const LgEditLayout L = edit_layout();
+            if (L.total && std::getenv("GTS_NO_GROUPED") == nullptr) {
+                launch_grouped_edit(rows, m, stats_on, L);
+                break;
+            }
             HitBuf hb{hq.p, he.p, hd.p, (unsigned long long)hq.n, counter.p + 1};
             // one warp per ~contiguous run of rows; enough warps to fill the GPU
             unsigned grid = grid_for((m + kRowChunk - 1) / kRowChunk, kLeafWarps, 148u * 4u);
@@ -2152,22 +2486,38 @@ extern "C" int gts_profile_read(char *buf, int64_t cap, int reset)
     return GTS_OK;
 }
 
-// Integer peak microbenchmarks: 16 independent chains per thread (enough ILP
-// that issue, not latency, bounds them).  Variant 0: LOP3 only (alu pipe);
-// 1: IMAD only (fma pipe); 2: alternating LOP3 / IMAD (both pipes).  The
-// reported peak is the best variant (executed int instructions per second).
+// Integer peak microbenchmarks: 16 chains per thread (enough ILP that issue,
+// not latency, bounds them).  Variant 0: LOP3 only (alu pipe); 1: IMAD only
+// (fma pipe); 2: alternating LOP3 / IMAD (both pipes).  Each op reads a
+// neighbouring chain through inline PTX, so neither NVVM nor ptxas can fold
+// iterations together (a self-contained (a^b)|c or a*m+b chain has a closed
+// form and was collapsed).  The reported peak is the best variant, in
+// executed integer instructions (thread-ops) per second.
+__device__ __forceinline__ uint32_t lop3_xor3(uint32_t a, uint32_t b, uint32_t c)
+{
+    uint32_t d;
+    asm volatile("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+__device__ __forceinline__ uint32_t mad_lo(uint32_t a, uint32_t b, uint32_t c)
+{
+    uint32_t d;
+    asm volatile("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
 template <int VAR>
 __global__ void k_int_peak(uint32_t seed, uint32_t mul, int iters, uint32_t *sink)
 {
     uint32_t a[16];
 #pragma unroll
     for (int i = 0; i < 16; i++) a[i] = seed ^ (threadIdx.x * 2654435761u + i * 40503u);
-    const uint32_t b = seed * 7u + 3u, c = seed | 1u;
+    const uint32_t c = seed * 7u + mul;
     for (int it = 0; it < iters; it++) {
 #pragma unroll
         for (int i = 0; i < 16; i++) {
-            if (VAR == 0 || (VAR == 2 && (i & 1) == 0)) a[i] = (a[i] ^ b) | c;   // 1 LOP3
-            else a[i] = a[i] * mul + b;                                          // 1 IMAD
+            if (VAR == 0 || (VAR == 2 && (i & 1) == 0)) a[i] = lop3_xor3(a[i], a[(i + 1) & 15], c);   // 1 LOP3
+            else a[i] = mad_lo(a[i], a[(i + 1) & 15], c);                                                // 1 IMAD
         }
     }
     uint32_t r = 0;
@@ -2352,6 +2702,12 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
                 uint32_t db;
                 std::memcpy(&db, &d, 4);
                 rec[(size_t)e] = make_uint4(db, (uint32_t)lens[(size_t)e], wstart[(size_t)e], 0u);
+            }
+            for (int64_t i = ix->leaf_first; i < (int64_t)ix->leaf_first + ix->leaf_count; i++) {
+                if (t->size[i] <= 0) continue;
+                const int64_t a = t->pos[i], b = t->pos[i] + t->size[i] - 1;
+                const int64_t wend = (int64_t)wstart[(size_t)b] + ((lens[(size_t)b] + 15) / 16) * 4;
+                ix->max_leaf_words = std::max<int>(ix->max_leaf_words, (int)std::min<int64_t>(wend - wstart[(size_t)a], 1 << 30));
             }
             ix->erec.alloc(rec.size(), st);
             h2d(ix->erec.p, rec.data(), rec.size(), st);

@@ -100,6 +100,15 @@ __device__ __forceinline__ bool is_alive(const uint32_t *alive, int e)
 // carries no per-column score.  Same integer as the reference DP
 // (metrics.py:54-84).
 // ---------------------------------------------------------------------------
+// x * 2 + 1 as one IMAD (fma pipe): the ALU pipe (LOP3) is the binding pipe
+// of the DP, so the shift-or of the +1 boundary row must not land there.
+__device__ __forceinline__ uint32_t shl1_or1(uint32_t x)
+{
+    uint32_t d;
+    asm("mad.lo.u32 %0, %1, 2, 1;" : "=r"(d) : "r"(x));
+    return d;
+}
+
 __device__ __forceinline__ void myers_step1(uint32_t Eq, uint32_t &Pv, uint32_t &Mv)
 {
     // single block, top boundary row +1 per column.  Hyyro's form: with
@@ -109,7 +118,7 @@ __device__ __forceinline__ void myers_step1(uint32_t Eq, uint32_t &Pv, uint32_t 
     const uint32_t D0 = (((X & Pv) + Pv) ^ Pv) | X;
     const uint32_t HN = Pv & D0;
     const uint32_t HP = Mv | ~(Pv | D0);
-    const uint32_t Xs = (HP << 1) | 1u;
+    const uint32_t Xs = shl1_or1(HP);
     Mv = Xs & D0;
     Pv = (HN << 1) | ~(Xs | D0);
 }
@@ -154,16 +163,24 @@ __device__ __forceinline__ void myers_word(const uint32_t *peq, uint32_t w, uint
     myers_char<W>(peq, w >> 24, P, M);
 }
 
-template <int W>
+// text loads: global (read-only path) or shared (leaf staged by the block)
+template <bool SMEM>
+__device__ __forceinline__ uint32_t tload(const uint32_t *p)
+{
+    if (SMEM) return *p;
+    return __ldg(p);
+}
+
+template <int W, bool SMEM = false>
 __device__ __forceinline__ int myers_fixed(const uint32_t *peq, int m, const uint32_t *__restrict__ t4, int n)
 {
     uint32_t P[W], M[W];
 #pragma unroll
     for (int b = 0; b < W; b++) { P[b] = ~0u; M[b] = 0u; }
     const int nfull = n >> 2;
-    uint32_t w = __ldg(t4);
+    uint32_t w = tload<SMEM>(t4);
     for (int jw = 0; jw < nfull; jw++) {
-        const uint32_t nxt = __ldg(t4 + jw + 1);
+        const uint32_t nxt = tload<SMEM>(t4 + jw + 1);
         myers_word<W>(peq, w, P, M);
         w = nxt;
     }
@@ -173,11 +190,67 @@ __device__ __forceinline__ int myers_fixed(const uint32_t *peq, int m, const uin
         if (rem > 1) myers_char<W>(peq, (w >> 8) & 0xffu, P, M);
         if (rem > 2) myers_char<W>(peq, (w >> 16) & 0xffu, P, M);
     }
+    // blocks past the pattern's last word (a batch runs its widest lane's W)
+    // only see rows below row m; they never feed back into rows <= m
+    const int wl = (m + 31) >> 5;
     const uint32_t lastmask = (m & 31) ? ((1u << (m & 31)) - 1u) : ~0u;
     int score = n;
 #pragma unroll
     for (int b = 0; b < W; b++) {
-        const uint32_t mk = (b == W - 1) ? lastmask : ~0u;
+        const uint32_t mk = b < wl - 1 ? ~0u : (b == wl - 1 ? lastmask : 0u);
+        score += __popc(P[b] & mk) - __popc(M[b] & mk);
+    }
+    return score;
+}
+
+// Text in shared memory, one symbol per byte load (LDS.U8 with immediate
+// offsets): no ALU-pipe symbol extraction per step.  `two` is the runtime
+// constant 2 (a kernel argument ptxas cannot fold), so the +1-boundary shift
+// (HP * 2 + 1) and the mask address (peq + sym * 4 * W) are IMADs on the
+// fma pipe and the ALU pipe carries only the 7 LOP3 of the recurrence.
+// Blocks past the pattern's last word behave as in myers_fixed.
+template <int W>
+__device__ __forceinline__ void myers_char_s(const uint32_t *peq, uint32_t c, uint32_t two, int A, uint32_t (&P)[W],
+                                             uint32_t (&M)[W])
+{
+    // masks block-major [W][A]: block b of symbol c at peq[b * A + c]
+    const uint32_t *pe = reinterpret_cast<const uint32_t *>(reinterpret_cast<const char *>(peq) + c * (two * two));
+    if (W == 1) {
+        const uint32_t X = pe[0] | M[0];
+        const uint32_t D0 = (((X & P[0]) + P[0]) ^ P[0]) | X;
+        const uint32_t HN = P[0] & D0;
+        const uint32_t HP = M[0] | ~(P[0] | D0);
+        const uint32_t Xs = HP * two + 1u;
+        M[0] = Xs & D0;
+        P[0] = HN * two | ~(Xs | D0);
+    } else {
+        uint32_t hp = 1u, hm = 0u;
+#pragma unroll
+        for (int b = 0; b < W; b++) myers_stepb(pe[b * A], P[b], M[b], hp, hm);
+    }
+}
+
+template <int W>
+__device__ __forceinline__ int myers_smem(const uint32_t *peq, int m, const uint8_t *t, int n, uint32_t two, int A)
+{
+    uint32_t P[W], M[W];
+#pragma unroll
+    for (int b = 0; b < W; b++) { P[b] = ~0u; M[b] = 0u; }
+    int j = 0;
+    for (; j + 4 <= n; j += 4) {
+        const uint32_t c0 = t[j], c1 = t[j + 1], c2 = t[j + 2], c3 = t[j + 3];
+        myers_char_s<W>(peq, c0, two, A, P, M);
+        myers_char_s<W>(peq, c1, two, A, P, M);
+        myers_char_s<W>(peq, c2, two, A, P, M);
+        myers_char_s<W>(peq, c3, two, A, P, M);
+    }
+    for (; j < n; j++) myers_char_s<W>(peq, t[j], two, A, P, M);
+    const int wl = (m + 31) >> 5;
+    const uint32_t lastmask = (m & 31) ? ((1u << (m & 31)) - 1u) : ~0u;
+    int score = n;
+#pragma unroll
+    for (int b = 0; b < W; b++) {
+        const uint32_t mk = b < wl - 1 ? ~0u : (b == wl - 1 ? lastmask : 0u);
         score += __popc(P[b] & mk) - __popc(M[b] & mk);
     }
     return score;

@@ -18,6 +18,18 @@ from oracle import oracle as O
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(params=["grouped", "rowwise"], autouse=True)
+def leaf_path(request, monkeypatch):
+    """Every test runs on both leaf-verification paths: leaf-grouped
+    (k_leafgroup_edit / k_leafgroup_vec / k_leafgroup_mma, the default) and
+    row-wise (k_leaf_edit / k_verify, GTS_NO_GROUPED=1)."""
+    if request.param == "rowwise":
+        monkeypatch.setenv("GTS_NO_GROUPED", "1")
+    else:
+        monkeypatch.delenv("GTS_NO_GROUPED", raising=False)
+    return request.param
+
+
 def setup(name):
     g = load_golden(name)
     met = int(g["metric"])
@@ -221,6 +233,21 @@ def test_edge_cases_strings():
     check_against_oracle(ds, tree, q, O.Payloads.from_strings(strs), O.Payloads.from_strings(q),
                          np.concatenate([[0.0, 0.0, 3.0, 5.0, 1.0, 50.0], rng.integers(0, 40, nq - 6)]).astype(float),
                          np.concatenate([[1, 2, 400, 5, 3, 1], rng.integers(1, 30, nq - 6)]))
+
+
+def test_edge_cases_strings_mixed_widths():
+    # queries of 0..128 symbols (1-4 pattern words mixed inside one warp's
+    # row group), empty and duplicate objects, overfull leaves, tombstones
+    rng = np.random.default_rng(18)
+    alpha = "abcdefghij"
+    strs = ["", "", "a", "abc" * 40] + P.generate_sequences(3000, seed=19, min_len=0, max_len=140, alphabet=alpha)
+    ds = P.Dataset.from_strings(strs, P.EDIT)
+    tree = P.build(ds, P.TreeConfig(6, 7))
+    q = ["", "a", "abc" * 40 + "ab", "j" * 33, "ab" * 32] + \
+        P.generate_sequences(40, seed=20, min_len=0, max_len=128, alphabet=alpha + "z")
+    nq = len(q)
+    check_against_oracle(ds, tree, q, O.Payloads.from_strings(strs), O.Payloads.from_strings(q),
+                         rng.integers(0, 70, nq).astype(float), rng.integers(1, 40, nq))
 
 
 def test_edge_cases_vectors():

@@ -37,6 +37,10 @@ METRICS = [
     ("dram__bytes_write.sum", "DRAM bytes written"),
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput %"),
     ("lts__t_sector_hit_rate.pct", "L2 hit rate %"),
+    ("lts__t_bytes.sum", "L2 bytes (all requests)"),
+    ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 throughput % of peak"),
+    ("l1tex__throughput.avg.pct_of_peak_sustained_active", "L1tex throughput % of peak"),
+    ("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "LSU pipe % (dup check)"),
     ("l1tex__t_sector_hit_rate.pct", "L1 hit rate %"),
     ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe %"),
 ]
