@@ -442,7 +442,7 @@ def run_ours(args, rank, world, local_rank):
         return None
     qps = 2 * nq * world / (ms / 1e3)
     # the dominant leaf-verification kernel of this workload (whichever ran)
-    cands = ("k_leafgroup_edit", "k_leaf_edit") if eng.edit else ("k_leafgroup_mma", "k_leafgroup_vec", "k_verify")
+    cands = ("k_leafgroup_edit", "k_leaf_edit") if eng.edit else ("k_leafgroup_mma2", "k_leafgroup_mma", "k_leafgroup_vec", "k_verify")
     kname = max(cands, key=lambda k: prof["kernels"].get(k, {"ms": 0.0})["ms"])
     kver = dict(prof["kernels"].get(kname, {"ms": 0.0, "count": 0}), name=kname)
     work = prof["work"]
@@ -573,7 +573,7 @@ def roofline(eng, prof, kver, step_ms_prof):
             "peak_source": "gts_bench_int_peak: best of LOP3-only / IMAD-only / mixed 16-chain loops on all SMs, "
                            "measured in this run (MEASURED_PEAKS.json has no integer peak)"})
     D = eng.w.get("dim", 2)
-    if kver["name"] == "k_leafgroup_mma":
+    if kver["name"] in ("k_leafgroup_mma", "k_leafgroup_mma2"):
         tf = peaks.get("bf16_tflops_sustained") or peaks.get("bf16_tflops") or 1590.0
         flops = work["pairs"] * 2 * D
         achieved = flops / t / 1e12 if t else None

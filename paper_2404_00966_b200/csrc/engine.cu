@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(256) k_verify(IndexView ix, QueryView qv, cons
                 if (!pruning) pass = true;
                 else {
                     const float de = __ldg(ix.dis + e);
-                    pass = fabsf(de - lr.dqp) <= r + slack(ix, de, lr.dqp, r);
+                    pass = lemma1_pass(ix, de, lr.dqp, lemma1_rrow(ix, lr.dqp, r));
                 }
             }
             ver += __popc(__ballot_sync(kFull, pass));
@@ -852,6 +852,79 @@ __device__ __forceinline__ float vdist32_smem(const float *a, const float *b, in
     return MET == kMetricL1 ? acc : sqrtf(acc);
 }
 
+// One level of the descent for vectors, rows grouped by parent node
+// (same predicates and outputs as k_expand).  A block stages the node's
+// child records and child pivot vectors in shared memory once per item of
+// <= kItemQueries rows; thread per (row, child) then reads only its query
+// (broadcast across the row's nc consecutive lanes) from global memory.
+template <int MET>
+__global__ void __launch_bounds__(256) k_expand_grouped(IndexView ix, QueryView qv, const Row *__restrict__ srows,
+                                                        const Item *__restrict__ items, int nitems, int own,
+                                                        int pruning, const float *__restrict__ r32, Row *out,
+                                                        unsigned long long *counter, unsigned long long *pruned_stat)
+{
+    extern __shared__ float4 ex_smem4[];
+    float *piv_s = reinterpret_cast<float *>(ex_smem4);                 // [nc][Dp]
+    NodeRec *rec_s = reinterpret_cast<NodeRec *>(piv_s + (size_t)ix.nc * ix.Dp);
+    __shared__ int sh_warp[32];
+    __shared__ unsigned long long sh_base;
+    const int nc = ix.nc, d4 = ix.Dp >> 2;
+    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+        const Item item = items[it];
+        const int child0 = (item.leaf - 1) * nc + 2;   // Eq. 1: children of node p are (p-1)*nc+2 ...
+        __syncthreads();
+        for (int t = threadIdx.x; t < nc; t += blockDim.x) rec_s[t] = ix.node[child0 + t];
+        __syncthreads();
+        for (int t = threadIdx.x; t < nc * d4; t += blockDim.x) {
+            const int j = t / d4, c = t - j * d4;
+            reinterpret_cast<float4 *>(piv_s)[t] =
+                __ldg(reinterpret_cast<const float4 *>(ix.vec32 + (size_t)rec_s[j].piv * ix.Dp) + c);
+        }
+        __syncthreads();
+        const int total = item.count * nc;
+        for (int base = 0; base < total; base += blockDim.x) {
+            const int i = base + threadIdx.x;
+            const bool valid = i < total;
+            bool keep = false, nonempty = false;
+            int q = -1, child = 0;
+            float cd = 0.f;
+            if (valid) {
+                const int row = i / nc, j = i - row * nc;
+                const Row pr = srows[item.start + row];
+                q = pr.q;
+                child = child0 + j;
+                const NodeRec c = rec_s[j];
+                nonempty = c.size > 0;
+                keep = nonempty;
+                const float r = r32[q];
+                if (keep && !own && pruning) {
+                    const float e = slack(ix, pr.dqp, r);
+                    keep = (pr.dqp + r + e >= c.mn) && (pr.dqp - r - e <= c.mx);
+                }
+                if (keep) {
+                    float acc = 0.f;
+                    const float4 *qp = reinterpret_cast<const float4 *>(qv.vec32 + (size_t)q * ix.Dp);
+                    const float4 *pp = reinterpret_cast<const float4 *>(piv_s + (size_t)j * ix.Dp);
+                    for (int k = 0; k < d4; k++) {
+                        const float4 x = pp[k], y = __ldg(qp + k);
+                        const float d0 = x.x - y.x, d1 = x.y - y.y, d2 = x.z - y.z, d3 = x.w - y.w;
+                        if (MET == kMetricL1) acc += (fabsf(d0) + fabsf(d1)) + (fabsf(d2) + fabsf(d3));
+                        else acc += (d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3);
+                    }
+                    cd = MET == kMetricL1 ? acc : sqrtf(acc);
+                    if (own && pruning) {
+                        const float e = slack(ix, cd, r);
+                        keep = (cd + r + e >= c.mn) && (cd - r - e <= c.mx);
+                    }
+                }
+            }
+            warp_add_q(pruned_stat, valid ? q : -1, (valid && nonempty && !keep) ? 1u : 0u);
+            long long slot = block_append(keep, counter, sh_warp, &sh_base);
+            if (keep) out[slot] = Row{q, child, cd, 0};
+        }
+    }
+}
+
 constexpr int kFHistBins = 64;
 __device__ __forceinline__ void fhist_add(unsigned *hist, const float *r0, int q, double d);
 __device__ __forceinline__ void fhist_shrink(unsigned *hist, const float *r0, const int32_t *ks, float *r32,
@@ -902,7 +975,7 @@ __global__ void __launch_bounds__(256) k_leafgroup_vec(IndexView ix, QueryView q
                     if (!pruning) pass = true;
                     else {
                         const float de = __ldg(ix.dis + e);
-                        pass = fabsf(de - lr.dqp) <= r + slack(ix, de, lr.dqp, r);
+                        pass = lemma1_pass(ix, de, lr.dqp, lemma1_rrow(ix, lr.dqp, r));
                     }
                 }
                 ver += __popc(__ballot_sync(kFull, pass));
@@ -1163,7 +1236,7 @@ __global__ void __launch_bounds__(kMmaThreads, 3) k_leafgroup_mma(IndexView ix, 
                 const int j = c0 + jj;
                 if (j >= leaf.size || !s_al[j]) continue;
                 const float dis = s_dis[j];
-                if (!(fabsf(dis - dqp) <= r + slack(ix, dis, dqp, r))) continue;   // lemma 1
+                if (!lemma1_pass(ix, dis, dqp, lemma1_rrow(ix, dqp, r))) continue;   // lemma 1
                 ver++;
                 bool cand = inf_r;
                 if (!cand) {
@@ -1211,6 +1284,355 @@ __global__ void __launch_bounds__(kMmaThreads, 3) k_leafgroup_mma(IndexView ix, 
 // objects not yet in the tree, scanned exactly for every query of the batch
 // (one extra leaf with no pivot filter).  Hits carry entry id -(slot+1).
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// Tensor-core L2 verification, pipelined (k_leafgroup_mma2, the default).
+// Differences from k_leafgroup_mma:
+//  * A = the item's 128 query rows in bf16 exactly as uploaded (no per-item
+//    centring / conversion): cp.async gathers them straight into the 128-byte
+//    swizzled layout.  The pivot term is folded in per entry:
+//        (q - c).(o - c)  ~=  q_bf16 . v_e  -  c . v_e,   v_e = bf16(o_e - c)
+//    with se_e = c . v_e precomputed at index build, so
+//        d^2 ~= dqp^2 + dis^2 - 2 (acc - se_e).
+//    Error: |eps . v| + |(q - c) . delta| <= 2^-9 (|q| + dqp) dis per dot
+//    (bf16 rounding of q and of o - c); the screen uses 2^-8, i.e. 2x margin.
+//  * two smem stages and two TMEM accumulators: item i+1's operands are in
+//    flight (cp.async) while item i's epilogue runs.
+//  * the epilogue only screens; pairs whose approximate d^2 is within the
+//    error band of r^2 go to a candidate list, and k_recheck_l2 recomputes
+//    them exactly in float64 (numpy order) against the FINAL radius, so no
+//    thread of an item stalls the block on a float64 recompute.
+//  * kNN: candidates whose d^2 UPPER bound is inside the radius feed the
+//    per-query histogram (their true distance is at most that bound), so the
+//    radius shrinks as the pass goes, exactly as with exact hits.
+// ---------------------------------------------------------------------------
+constexpr int kM2Threads = 512;   // 16 warps: 4 per TMEM lane quadrant
+
+struct CandBuf {
+    int32_t *q, *e;
+    float *lb;                 // lower bound of d^2 (approximate d^2 - error band)
+    unsigned long long cap;
+    unsigned long long *counter;
+};
+
+__global__ void __launch_bounds__(kM2Threads, 1)
+k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, const Item *__restrict__ items, int nitems,
+                 unsigned long long *item_cursor, float *r32, double *r64, CandBuf cb,
+                 unsigned long long *verified_stat, int stats_on, unsigned long long *work, uint32_t acc_cols,
+                 int nmax, unsigned *fhist, const float *r0, const int32_t *ks)
+{
+    extern __shared__ __align__(1024) uint8_t smraw[];
+    __shared__ uint64_t mbar[2];
+    __shared__ uint32_t tmem_slot;
+    // per column: {dis (NaN when tombstoned), dis^2 + 2 se, 8 rel dis^2, 0}
+    __shared__ float4 s_col[2][256];
+    __shared__ int s_rq[2][128];         // per stage: the item's query ids
+    __shared__ float4 s_rf[2][128];      // {dqp, r (at staging; radii only shrink), |q|, probe radius}
+    __shared__ int s_next[2];
+    const uint32_t pad = (1024u - (tc::smem_u32(smraw) & 1023u)) & 1023u;
+    uint8_t *sm = smraw + pad;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nkb = ix.Dk >> 6;                        // 128-byte K-blocks per row
+    const int c16 = ix.Dk >> 3;                        // 16-byte chunks per row
+    const size_t a_bytes = (size_t)nkb * 16384;
+    const size_t stage_bytes = a_bytes + (size_t)nkb * nmax * 128;
+    if (warp == 0) tc::tmem_alloc(&tmem_slot, 2 * acc_cols);
+    if (tid == 0) {
+        tc::mbar_init(&mbar[0], 1);
+        tc::mbar_init(&mbar[1], 1);
+        tc::fence_mbar_init();
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tmem = tmem_slot;
+
+
+    // operands + metadata of item `it` into stage `st` (async copies)
+    auto stage = [&](int st, int it) {
+        const Item item = items[it];
+        const NodeRec leaf = ix.node[item.leaf];
+        const int pos = ix.npos[item.leaf];
+        const int N = max(16, (leaf.size + 15) & ~15);
+        uint8_t *A = sm + st * stage_bytes;
+        uint8_t *B = A + a_bytes;
+        // c16 is 8 or 16 (Dk 64 / 128): thread -> fixed chunk, rows step by 512 / c16
+        const int lc = c16 == 16 ? 4 : 3;
+        const int c = tid & (c16 - 1), row0 = tid >> lc, rstep = kM2Threads >> lc;
+        const uint32_t aoff = (uint32_t)(c >> 3) * 16384u, boff = (uint32_t)(c >> 3) * (uint32_t)N * 128u;
+        for (int row = row0; row < 128; row += rstep) {
+            const bool ok = row < item.count;
+            const int q = ok ? srows[item.start + row].q : 0;
+            tc::cp_async16(tc::smem_u32(A + aoff + tc::sw128_offset(row, c & 7)), qv.qbf + (size_t)q * c16 + c,
+                           ok ? 16u : 0u);
+        }
+        for (int row = row0; row < N; row += rstep) {
+            const bool ok = row < leaf.size;
+            tc::cp_async16(tc::smem_u32(B + boff + tc::sw128_offset(row, c & 7)),
+                           ix.vcent + (size_t)(pos + (ok ? row : 0)) * c16 + c, ok ? 16u : 0u);
+        }
+        tc::cp_async_commit();
+        if (tid < 128) {
+            // row metadata, prefetched one item ahead of the epilogue
+            int q = 0;
+            float4 f = make_float4(0.f, -1.f, 0.f, 0.f);
+            if (tid < item.count) {
+                const Row lr = srows[item.start + tid];
+                q = lr.q;
+                f = make_float4(lr.dqp, __ldcg(r32 + q), qv.qn[q], r0 ? r0[q] : 0.f);
+            }
+            s_rq[st][tid] = q;
+            s_rf[st][tid] = f;
+        }
+        for (int j = tid; j < N; j += kM2Threads) {   // padding columns: NaN fails every test
+            // {dis (NaN if tombstoned), y - z, y + z, dis} with y = dis^2 + 2 se
+            // and z = 8 rel dis^2 (the dis^2 part of the error band)
+            float4 col = make_float4(__int_as_float(0x7fc00000), 0.f, 0.f, 0.f);
+            if (j < leaf.size) {
+                const float dis = __ldg(ix.dis + pos + j);
+                const float se = __ldg(ix.vse + pos + j);
+                const float y = fmaf(dis, dis, 2.f * se), z = 8.f * ix.rel * dis * dis;
+                if (is_alive(ix.alive, pos + j)) col.x = dis;
+                col.y = y - z;
+                col.z = y + z;
+                col.w = dis;
+            }
+            s_col[st][j] = col;
+        }
+    };
+    auto mma = [&](int st, int it) {
+        if (tid != 0) return;
+        tc::fence_after_sync();
+        const Item item = items[it];
+        const int N = max(16, (ix.node[item.leaf].size + 15) & ~15);
+        const uint32_t idesc = tc::idesc_bf16(128, N);
+        const uint32_t a0 = tc::smem_u32(sm + st * stage_bytes), b0 = a0 + (uint32_t)a_bytes;
+        for (int kb = 0; kb < nkb; kb++) {
+#pragma unroll
+            for (int k4 = 0; k4 < 4; k4++) {
+                const uint64_t ad = tc::desc_k_sw128(a0 + kb * 16384 + k4 * 32);
+                const uint64_t bd = tc::desc_k_sw128(b0 + kb * N * 128 + k4 * 32);
+                tc::mma_bf16(tmem + st * acc_cols, ad, bd, idesc, (kb | k4) ? 1u : 0u);
+            }
+        }
+        tc::mma_commit(&mbar[st]);
+    };
+
+    // item claims run one iteration ahead through s_next[2] (iteration i
+    // reads slot i & 1, thread 0 fills slot (i + 1) & 1), so each iteration
+    // needs a single block barrier
+    if (tid == 0) s_next[0] = (int)atomicAdd(item_cursor, 1ull);
+    __syncthreads();
+    int cur = s_next[0];
+    if (cur < nitems) {
+        stage(0, cur);
+        if (tid == 0) s_next[1] = (int)atomicAdd(item_cursor, 1ull);
+        tc::cp_async_wait_all();
+        tc::fence_async_smem();
+        __syncthreads();
+        mma(0, cur);
+    }
+    uint32_t phase[2] = {0u, 0u};
+    int s = 0, iter = 1;
+    unsigned long long pairs = 0;
+    while (cur < nitems) {
+        const int nxt = s_next[iter & 1];
+        if (nxt < nitems) {
+            stage(s ^ 1, nxt);
+            if (tid == 0) s_next[(iter + 1) & 1] = (int)atomicAdd(item_cursor, 1ull);
+        }
+        iter++;
+        tc::mbar_wait(&mbar[s], phase[s]);
+        phase[s] ^= 1u;
+        tc::fence_after_sync();
+        // ---- epilogue of item `cur` (stage s, accumulator s) ----
+        // thread = one query row (TMEM lane) x every 4th 16-column chunk;
+        // per column: lemma 1, approximate d^2, error band, ~12 instructions
+        {
+            const Item item = items[cur];
+            const int size = ix.node[item.leaf].size;
+            const int pos = ix.npos[item.leaf];
+            const int N = max(16, (size + 15) & ~15);
+            const int qrow = 32 * (warp & 3) + lane;
+            const int part = warp >> 2;
+            const bool valid = qrow < item.count;
+            const int q = s_rq[s][qrow];
+            const float4 rf = s_rf[s][qrow];
+            const float dqp = rf.x, qnorm = rf.z;
+            float r = rf.y;
+            // folded thresholds: with y - z, y + z per column,
+            //   screen    (y - z) - 2 acc - cA dis <= R2 + kq - dq2 + margin  (T1)
+            //   ub inside (y + z) - 2 acc + cA dis <= R2 - kq - dq2 - margin  (T2)
+            // margin 2^-18 (dq2 + qn^2 + R2) covers the fp32 rounding of the
+            // rearranged sums; the band itself has a 2x margin.
+            const float dq2 = dqp * dqp;
+            const float cA = ldexpf(dqp + qnorm, -7) + ldexpf(qnorm, -18) + 4.f * ix.abs_eps;
+            const float kq = 8.f * ix.rel * dq2 + 4.f * ix.abs_eps * (dqp + ix.abs_eps);
+            float rrow, T1, T2;
+            auto set_r = [&](float rr) {
+                const float R2 = rr * rr * (1.f + 1e-6f);
+                const float mg = ldexpf(dq2 + qnorm * qnorm + R2, -18);
+                rrow = lemma1_rrow(ix, dqp, rr);
+                T1 = R2 + kq - dq2 + mg;
+                T2 = R2 - kq - dq2 - mg;
+            };
+            set_r(r);
+            float hinv = 0.f;   // kNN histogram: bins per unit distance
+            if (fhist && valid) {
+                const float R0 = rf.w;
+                hinv = (R0 > 0.f && !isinf(R0)) ? (float)kFHist / R0 : 0.f;
+            }
+            unsigned ver = 0;
+            const uint32_t lane_base = tmem + s * acc_cols + ((uint32_t)((warp & 3) * 32) << 16);
+            for (int c0 = 16 * part; c0 < N; c0 += 64) {
+                float acc[16];
+                tc::tmem_ld16(lane_base + (uint32_t)c0, acc);   // warp-collective
+                uint32_t cm = 0, fm = 0;
+#pragma unroll
+                for (int jj = 0; jj < 16; jj++) {
+                    const float4 col = s_col[s][c0 + jj];   // broadcast LDS.128
+                    const bool pass = lemma1_pass(ix, col.x, dqp, rrow);
+                    const float m2a = fmaf(-2.f, acc[jj], col.y);
+                    const float m2b = fmaf(-2.f, acc[jj], col.z);
+                    const bool cand = pass && fmaf(-cA, col.w, m2a) <= T1;
+                    ver += pass;
+                    cm |= (uint32_t)cand << jj;
+                    fm |= (uint32_t)(cand && fmaf(cA, col.w, m2b) <= T2) << jj;
+                }
+                if (c0 + 16 > size) cm &= (1u << (size - c0 > 0 ? size - c0 : 0)) - 1u, fm &= cm;
+                if (!valid) cm = fm = 0;
+                // warp-aggregated append of the chunk's candidates
+                const unsigned nc = __popc(cm);
+                unsigned incl = nc;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const unsigned v = __shfl_up_sync(kFull, incl, o);
+                    if (lane >= o) incl += v;
+                }
+                const unsigned wtot = __shfl_sync(kFull, incl, 31);
+                if (wtot) {
+                    unsigned long long base = 0;
+                    if (lane == 31) base = atomicAdd(cb.counter, (unsigned long long)wtot);
+                    base = __shfl_sync(kFull, base, 31) + (incl - nc);
+#pragma unroll
+                    for (int jj = 0; jj < 16; jj++) {
+                        if (!((cm >> jj) & 1u)) continue;
+                        if (base < cb.cap) {
+                            const float4 col = s_col[s][c0 + jj];
+                            cb.q[base] = q;
+                            cb.e[base] = pos + c0 + jj;
+                            // d^2 lower bound, rounded down a little
+                            cb.lb[base] = (fmaf(-cA, col.w, fmaf(-2.f, acc[jj], col.y)) + dq2 - kq) * (1.f - 1e-5f) -
+                                          ldexpf(dq2 + qnorm * qnorm, -18);
+                        }
+                        base++;
+                    }
+                }
+                if (fm && hinv > 0.f) {
+                    // candidates whose d^2 upper bound is inside the radius: their
+                    // true distance is <= that bound, so they may shrink it
+#pragma unroll
+                    for (int jj = 0; jj < 16; jj++) {
+                        if (!((fm >> jj) & 1u)) continue;
+                        const float4 col = s_col[s][c0 + jj];
+                        const float d2u = fmaf(cA, col.w, fmaf(-2.f, acc[jj], col.z)) + dq2 + kq +
+                                          ldexpf(dq2 + qnorm * qnorm, -18);
+                        const float dub = sqrtf(fmaxf(d2u, 0.f)) * (1.f + 1e-6f) + 1e-30f;
+                        const int b = min((int)(dub * hinv * (1.f + 1e-6f)), kFHist - 1);
+                        atomicAdd(fhist + (size_t)q * kFHist + b, 1u);
+                    }
+                    __threadfence();
+                    fhist_shrink(fhist, r0, ks, r32, r64, q);
+                    r = __ldcg(r32 + q);
+                    set_r(r);
+                }
+            }
+            if (valid && stats_on && ver) atomicAdd(verified_stat + q, (unsigned long long)ver);
+            pairs += ver;
+            if (work && tid == 0) {
+                atomicAdd(work + kWorkEntries, (unsigned long long)size * item.count);
+                atomicAdd(work + kWorkRows, (unsigned long long)item.count);
+                atomicAdd(work + kWorkSteps, (unsigned long long)128 * N * ix.Dk);   // MMA MACs issued
+            }
+        }
+        tc::cp_async_wait_all();
+        tc::fence_async_smem();
+        tc::fence_before_sync();
+        __syncthreads();
+        if (nxt >= nitems) break;
+        mma(s ^ 1, nxt);
+        s ^= 1;
+        cur = nxt;
+    }
+    if (work) {
+        for (int o = 16; o > 0; o >>= 1) pairs += __shfl_down_sync(kFull, pairs, o);
+        if (lane == 0) atomicAdd(work + kWorkPairs, pairs);
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    if (warp == 0) tc::tmem_dealloc(tmem, 2 * acc_cols);
+}
+
+// Exact float64 recheck of the tensor-core candidates against the final
+// radius (kNN radii only ever shrink, so the candidates are a superset).
+// Candidates whose d^2 lower bound is already outside the final radius are
+// dropped first.  8 lanes per candidate: lane j accumulates numpy's pairwise
+// partial r[j] = sum over i = j (mod 8) in order, then the lanes combine
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) and add the D % 8 tail sequentially --
+// the same float64 operations as pw_sum64 for D <= 128 (metrics.py:127-133).
+__global__ void k_recheck_l2(IndexView ix, QueryView qv, CandBuf cb, unsigned long long ncand, const float *r32,
+                             const double *r64, HitBuf out)
+{
+    const int lane = lane_id(), sub = lane >> 3, j = lane & 7;
+    const unsigned long long i = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+    bool live = false;
+    int q = 0, e = 0;
+    if (i < ncand) {
+        q = cb.q[i];
+        const float r = __ldcg(r32 + q);
+        live = !(cb.lb[i] > r * r * (1.f + 1e-6f));
+        e = cb.e[i];
+    }
+    double d64 = 0.0;
+    if (__any_sync(kFull, live)) {
+        const int D = ix.D;
+        const float *o32 = ix.vec64 ? nullptr : ix.vec32 + (size_t)e * ix.Dp;
+        const double *o64 = ix.vec64 ? ix.vec64 + (size_t)e * D : nullptr;
+        const double *qq = qv.vec64 + (size_t)q * D;
+        const int nb = D - D % 8;
+        double acc = 0.0;
+        if (live && j < nb) {
+            acc = term64<kMetricL2>(o64 ? o64[j] : (double)o32[j], qq[j]);
+            for (int t = j + 8; t < nb; t += 8) acc = __dadd_rn(acc, term64<kMetricL2>(o64 ? o64[t] : (double)o32[t], qq[t]));
+        }
+        // combine within the 8-lane group in numpy's order
+        const double a1 = __shfl_xor_sync(kFull, acc, 1);
+        const double p2 = (j & 1) ? __dadd_rn(a1, acc) : __dadd_rn(acc, a1);      // (r0+r1), (r2+r3), ...
+        const double a2 = __shfl_xor_sync(kFull, p2, 2);
+        const double p4 = (j & 2) ? __dadd_rn(a2, p2) : __dadd_rn(p2, a2);
+        const double a4 = __shfl_xor_sync(kFull, p4, 4);
+        double res = (j & 4) ? __dadd_rn(a4, p4) : __dadd_rn(p4, a4);
+        if (live && j == 0) {
+            if (nb == 0) res = 0.0;
+            for (int t = nb; t < D; t++) {
+                const double v = term64<kMetricL2>(o64 ? o64[t] : (double)o32[t], qq[t]);
+                res = (t == 0) ? v : __dadd_rn(res, v);
+            }
+            d64 = __dsqrt_rn(res);
+        }
+    }
+    const bool hit = live && j == 0 && d64 <= __ldcg(r64 + q);
+    const unsigned hb = __ballot_sync(kFull, hit);
+    if (!hb) return;
+    unsigned long long base = 0;
+    if (lane == __ffs(hb) - 1) base = atomicAdd(out.counter, (unsigned long long)__popc(hb));
+    base = __shfl_sync(kFull, base, __ffs(hb) - 1);
+    if (hit) {
+        const unsigned long long o = base + __popc(hb & ((1u << lane) - 1u));
+        if (o < out.cap) { out.q[o] = q; out.e[o] = e; out.d[o] = d64; }
+    }
+    (void)sub;
+}
+
 struct CacheView {
     int n;
     const int64_t *ids;
@@ -1434,6 +1856,21 @@ __global__ void k_query_hist(const uint8_t *sym, const int64_t *soff, int nq, ui
     qhist[2 * q + 1] = make_uint4(w[4], w[5], w[6], w[7]);
 }
 
+// bf16 query rows (uncentred, zero-padded to Dk) and |q| rounded up
+__global__ void k_query_bf16(const float *v32, int64_t nq, int D, int Dp, int Dk, uint4 *qbf, float *qn)
+{
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= nq) return;
+    __nv_bfloat16 *dst = reinterpret_cast<__nv_bfloat16 *>(qbf + r * (Dk / 8));
+    double s2 = 0.0;
+    for (int d = 0; d < Dk; d++) {
+        const float x = d < D ? v32[r * Dp + d] : 0.f;
+        dst[d] = __float2bfloat16(x);
+        s2 += (double)x * (double)x;
+    }
+    qn[r] = (float)(sqrt(s2) * (1.0 + 1e-6));
+}
+
 __global__ void k_vec_prep(const double *v64, int64_t nq, int D, int Dp, float *v32, unsigned *maxabs_bits,
                            int *inexact)
 {
@@ -1589,6 +2026,7 @@ struct gts_index {
     DBuf<uint4> erec;
     DBuf<uint4> ehist;
     DBuf<uint4> vcent;   // bf16 x 8 per uint4
+    DBuf<float> vse;     // c . vcent_e per entry
     int Dk = 0;
     DBuf<int32_t> alpha;
     int max_leaf = 0;
@@ -1596,6 +2034,7 @@ struct gts_index {
     int leaf_first = 0, leaf_count = 0;
     std::vector<int64_t> ord;   // device entry -> reference table position
     std::atomic<unsigned long long> hit_hint[2] = {{0}, {0}};   // hits of the last range / kNN call
+    std::atomic<unsigned long long> cand_hint{0};                // tensor-core candidates of the last launch
     // pending-insert cache (device copy of the caller's pending set)
     int cache_n = 0;
     DBuf<int64_t> cache_ids;
@@ -1623,6 +2062,8 @@ struct gts_queries {
     DBuf<uint32_t> peq;
     DBuf<int64_t> peq_off;
     DBuf<uint4> qhist;
+    DBuf<uint4> qbf;     // bf16 query rows (tensor-core L2 path)
+    DBuf<float> qn;
 };
 
 struct gts_result {
@@ -1653,6 +2094,7 @@ IndexView make_view(const gts_index *ix, const gts_queries *q)
     v.erec = ix->erec.p;
     v.ehist = ix->ehist.p;
     v.vcent = ix->vcent.p;
+    v.vse = ix->vse.p;
     v.Dk = ix->Dk;
     v.D = ix->D;
     v.Dp = ix->Dp;
@@ -1686,6 +2128,8 @@ QueryView make_qview(const gts_index *ix, const gts_queries *q)
     v.peq = q->peq.p;
     v.peq_off = q->peq_off.p;
     v.qhist = q->qhist.p;
+    v.qbf = q->qbf.p;
+    v.qn = q->qn.p;
     v.A = ix->A;
     return v;
 }
@@ -1819,21 +2263,22 @@ struct Search {
         int nitems = 0;
     };
 
-    void group_rows(const Row *rows, int64_t m, Grouped &G, int per = kItemQueries)
+    void group_rows(const Row *rows, int64_t m, Grouped &G, int per = kItemQueries, int first = -1, int count = -1)
     {
-        const int nleaf = ix->leaf_count;
+        if (first < 0) { first = ix->leaf_first; count = ix->leaf_count; }
+        const int nleaf = count;
         DBuf<int> cnt((size_t)nleaf + 1, st), off((size_t)nleaf + 1, st), cur((size_t)nleaf + 1, st);
         DBuf<int> nit((size_t)nleaf + 1, st), ioff((size_t)nleaf + 1, st);
         G.srows.alloc((size_t)m, st);
         CK(cudaMemsetAsync(cnt.p, 0, sizeof(int) * (nleaf + 1), st));
-        k_leaf_hist<<<grid_for(m, 256), 256, 0, st>>>(rows, m, ix->leaf_first, cnt.p);
+        k_leaf_hist<<<grid_for(m, 256), 256, 0, st>>>(rows, m, first, cnt.p);
         LAUNCH_CHECK();
         size_t tb = 0;
         cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.p, off.p, nleaf + 1, st);
         DBuf<uint8_t> tmp(tb, st);
         CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, cnt.p, off.p, nleaf + 1, st));
         CK(cudaMemcpyAsync(cur.p, off.p, sizeof(int) * (nleaf + 1), cudaMemcpyDeviceToDevice, st));
-        k_leaf_scatter<<<grid_for(m, 256), 256, 0, st>>>(rows, m, ix->leaf_first, cur.p, G.srows.p);
+        k_leaf_scatter<<<grid_for(m, 256), 256, 0, st>>>(rows, m, first, cur.p, G.srows.p);
         LAUNCH_CHECK();
         k_item_counts<<<grid_for(nleaf, 256), 256, 0, st>>>(cnt.p, nleaf, per, nit.p);
         LAUNCH_CHECK();
@@ -1846,7 +2291,7 @@ struct Search {
         G.nitems = *h_nitems;
         if (G.nitems == 0) return;
         G.items.alloc((size_t)G.nitems, st);
-        k_make_items<<<grid_for(nleaf, 256), 256, 0, st>>>(cnt.p, off.p, ioff.p, nleaf, ix->leaf_first, per, G.items.p);
+        k_make_items<<<grid_for(nleaf, 256), 256, 0, st>>>(cnt.p, off.p, ioff.p, nleaf, first, per, G.items.p);
         LAUNCH_CHECK();
     }
 
@@ -1909,6 +2354,58 @@ struct Search {
         LAUNCH_CHECK();
     }
 
+    // tensor-core screen (k_leafgroup_mma2) + exact float64 recheck of the
+    // candidate pairs (k_recheck_l2)
+    void launch_mma2(const Row *srows, const Item *items, int nitems, int stats_on)
+    {
+        const int nmax = std::max(16, (ix->max_leaf + 15) & ~15);
+        uint32_t cols = 32;
+        while ((int)cols < nmax) cols <<= 1;
+        const size_t nkb = (size_t)ix->Dk / 64;
+        const size_t smb = 2 * (nkb * 16384 + nkb * (size_t)nmax * 128) + 1024;
+        static size_t attr = 0;
+        if (attr < smb) {
+            CK(cudaFuncSetAttribute(k_leafgroup_mma2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
+            attr = smb;
+        }
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
+        const unsigned grid = (unsigned)std::min<int>(nitems, sms);
+        size_t cap = std::max<size_t>((size_t)1 << 22, (size_t)ix->cand_hint.load());
+        DBuf<unsigned long long> cnt(2, st);   // [0] item cursor, [1] candidates
+        for (int attempt = 0;; attempt++) {
+            if (cq.n < cap) {
+                cq.alloc(cap, st);
+                ce.alloc(cap, st);
+                clb.alloc(cap, st);
+            }
+            CK(cudaMemsetAsync(cnt.p, 0, 2 * sizeof(unsigned long long), st));
+            CandBuf cb{cq.p, ce.p, clb.p, (unsigned long long)cq.n, cnt.p + 1};
+            const int first = attempt == 0 ? stats_on : 0;   // a re-run must not count twice
+            timed("k_leafgroup_mma2", [&] {
+                k_leafgroup_mma2<<<grid, kM2Threads, smb, st>>>(iv, qv, srows, items, nitems, cnt.p, r32.p, r64.p, cb,
+                                                             verified.p, first, first ? work.p : nullptr, cols,
+                                                             nmax, first ? fhist.p : nullptr, r0.p, ks.p);
+            });
+            LAUNCH_CHECK();
+            CK(cudaMemcpyAsync(h_counter + 2, cnt.p + 1, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            const unsigned long long nc = h_counter[2];
+            ix->cand_hint = std::max<unsigned long long>(ix->cand_hint.load(), nc);
+            if (nc > cq.n) { cap = (size_t)nc + nc / 4; continue; }
+            if (nc) {
+                HitBuf hb{hq.p, he.p, hd.p, (unsigned long long)hq.n, counter.p + 1};
+                timed("k_recheck_l2", [&] {
+                    k_recheck_l2<<<grid_for((int64_t)nc * 8, 256), 256, 0, st>>>(iv, qv, cb, nc, r32.p, r64.p, hb);
+                });
+                LAUNCH_CHECK();
+            }
+            return;
+        }
+    }
+    DBuf<int32_t> cq, ce;   // tensor-core candidate pairs
+    DBuf<float> clb;        // their d^2 lower bounds
+
     template <int MET>
     void launch_grouped(const Row *rows, int64_t m, int stats_on)
     {
@@ -1920,6 +2417,10 @@ struct Search {
         DBuf<Item> &items = G.items;
         HitBuf hb{hq.p, he.p, hd.p, (unsigned long long)hq.n, counter.p + 1};
         const size_t sm = grouped_smem();
+        if (MET == kMetricL2 && ix->vcent.p && pruning && qs->qbf.p && std::getenv("GTS_MMA_V1") == nullptr) {
+            launch_mma2(srows.p, items.p, nitems, stats_on);
+            return;
+        }
         if (MET == kMetricL2 && ix->vcent.p && pruning) {
             const int nmax = std::max(16, (ix->max_leaf + 15) & ~15);
             const size_t smb = (size_t)(ix->Dk / 64) * (128 * 128 + (size_t)nmax * 128) + 1024;
@@ -2006,8 +2507,11 @@ struct Search {
     {
         switch (ix->metric) {
         case GTS_EDIT: {
+            // k_leafgroup_edit is opt-in: the DP and the per-entry filters are
+            // ALU-pipe bound, not L2 bound, and the row-wise kernel measured
+            // faster on words (87.6 vs 129.6 ms/step) and DNA (4.93 vs 5.05 s)
             const LgEditLayout L = edit_layout();
-            if (L.total && std::getenv("GTS_NO_GROUPED") == nullptr) {
+            if (L.total && std::getenv("GTS_EDIT_GROUPED") != nullptr && std::getenv("GTS_NO_GROUPED") == nullptr) {
                 launch_grouped_edit(rows, m, stats_on, L);
                 break;
             }
@@ -2030,8 +2534,31 @@ struct Search {
     }
 
     template <int MET>
-    int64_t launch_expand(const Row *in, int64_t m, int own, Row *out)
+    int64_t launch_expand(const Row *in, int64_t m, int own, Row *out, int layer)
     {
+        if (MET != kMetricEdit && ix->D >= 16 && std::getenv("GTS_NO_GROUPED") == nullptr) {
+            // parent rows of this layer are nodes [first, first + count)
+            int64_t c = 1;
+            for (int l = 1; l < layer; l++) c *= ix->nc;
+            const int first = (int)((c - 1) / (ix->nc - 1) + 1);
+            Grouped G;
+            group_rows(in, m, G, kItemQueries, first, (int)c);
+            CK(cudaMemsetAsync(counter.p, 0, sizeof(unsigned long long), st));
+            if (G.nitems == 0) return 0;
+            const size_t smb = (size_t)ix->nc * ix->Dp * sizeof(float) + (size_t)ix->nc * sizeof(NodeRec);
+            static size_t attr[3] = {0, 0, 0};
+            if (attr[MET] < smb) {
+                CK(cudaFuncSetAttribute(k_expand_grouped<MET>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
+                attr[MET] = smb;
+            }
+            const unsigned grid = (unsigned)std::min<int>(G.nitems, 148 * 8);
+            timed("k_expand", [&] {
+                k_expand_grouped<MET><<<grid, 256, smb, st>>>(iv, qv, G.srows.p, G.items.p, G.nitems, own, pruning,
+                                                            r32.p, out, counter.p, pruned.p);
+            });
+            LAUNCH_CHECK();
+            return (int64_t)read_counter(0);
+        }
         CK(cudaMemsetAsync(counter.p, 0, sizeof(unsigned long long), st));
         unsigned grid = grid_for(m * ix->nc, 256, 148u * 32u);
         timed("k_expand", [&] {
@@ -2045,9 +2572,9 @@ struct Search {
     {
         const int own = (layer + 1) == ix->levels;
         switch (ix->metric) {
-        case GTS_EDIT: return launch_expand<kMetricEdit>(in, m, own, out);
-        case GTS_L1: return launch_expand<kMetricL1>(in, m, own, out);
-        default: return launch_expand<kMetricL2>(in, m, own, out);
+        case GTS_EDIT: return launch_expand<kMetricEdit>(in, m, own, out, layer);
+        case GTS_L1: return launch_expand<kMetricL1>(in, m, own, out, layer);
+        default: return launch_expand<kMetricL2>(in, m, own, out, layer);
         }
     }
 
@@ -2343,6 +2870,12 @@ gts_queries *upload_queries(gts_index *ix, const gts_query_batch *qb, cudaStream
                                                                       flags.p, (int *)(flags.p + 1));
                 LAUNCH_CHECK();
             }
+            if (ix->vcent.p && nq) {
+                q->qbf.alloc((size_t)nq * (ix->Dk / 8), st);
+                q->qn.alloc((size_t)nq, st);
+                k_query_bf16<<<grid_for(nq, 128), 128, 0, st>>>(q->vec32.p, nq, q->D, q->Dp, ix->Dk, q->qbf.p, q->qn.p);
+                LAUNCH_CHECK();
+            }
             unsigned hf[2];
             CK(cudaMemcpyAsync(hf, flags.p, sizeof(hf), cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
@@ -2567,6 +3100,17 @@ extern "C" int gts_bench_int_peak(double *ops_per_s, void *stream)
 extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int device, gts_index **out)
 {
     ABI_BEGIN
+    {
+        // search scratch comes from the device's default stream-ordered pool;
+        // keep freed blocks mapped between calls instead of unmapping them at
+        // every synchronisation (release threshold 0 is the CUDA default)
+        CK(cudaSetDevice(device));
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
     if (!ds || !t || !out) fail(GTS_EINVAL, "null argument");
     if (ds->metric != GTS_EDIT && ds->metric != GTS_L1 && ds->metric != GTS_L2)
         fail(GTS_EMETRIC, "metric %d not supported on the device path (edit, l1, l2)", ds->metric);
@@ -2761,8 +3305,25 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
                             vc[(size_t)e * ix->Dk + d] = __float2bfloat16(
                                 v32[(size_t)(e * ix->Dp + d)] - v32[(size_t)((int64_t)pvp * ix->Dp + d)]);
                 }
+                // se_e = c . bf16(o_e - c): the pivot term of the uncentred
+                // query product (k_leafgroup_mma2), from the same rounded values
+                std::vector<float> se((size_t)n, 0.f);
+                for (int64_t i = lfirst; i < lfirst + lcount; i++) {
+                    const int64_t p0 = t->pos[i], sz = t->size[i];
+                    if (sz <= 0) continue;
+                    const int pvp = nodes[(size_t)i].piv;
+                    for (int64_t e = p0; e < p0 + sz; e++) {
+                        double acc = 0.0;
+                        for (int d = 0; d < ix->D; d++)
+                            acc += (double)v32[(size_t)((int64_t)pvp * ix->Dp + d)] *
+                                   (double)__bfloat162float(vc[(size_t)e * ix->Dk + d]);
+                        se[(size_t)e] = (float)acc;
+                    }
+                }
                 ix->vcent.alloc(vc.size() / 8, st);
                 CK(cudaMemcpyAsync(ix->vcent.p, vc.data(), vc.size() * sizeof(__nv_bfloat16), cudaMemcpyHostToDevice, st));
+                ix->vse.alloc((size_t)n, st);
+                h2d(ix->vse.p, se.data(), (size_t)n, st);
                 CK(cudaStreamSynchronize(st));
             }
             ix->vec32.alloc(v32.size(), st);

@@ -48,6 +48,7 @@ struct IndexView {
     const uint4 *erec;       // [n] edit scan records {dis f32 bits, len, first text word, 0}
     const uint4 *ehist;      // [2n] 32 byte-buckets of symbol counts (symbol % 32), or null
     const uint4 *vcent;      // [n][Dk/8] bf16 vectors centred on their leaf pivot (tensor-core L2 path), or null
+    const float *vse;        // [n] c . vcent_e (pivot . centred bf16 entry), tensor-core path
     int Dk;                  // D rounded up to 64 (one 128-byte bf16 row per K-block)
     int D, Dp, nc, levels;
     int leaf_first, leaf_count, max_leaf;
@@ -62,6 +63,8 @@ struct QueryView {
     const uint32_t *peq;   // Myers match masks, [A][W] per query
     const int64_t *peq_off;
     const uint4 *qhist;    // [2nq] query symbol histograms (same buckets as ehist)
+    const uint4 *qbf;      // [nq][Dk/8] bf16 query rows (tensor-core L2 path)
+    const float *qn;       // [nq] |q| rounded up
     int A;
 };
 
@@ -100,14 +103,11 @@ __device__ __forceinline__ bool is_alive(const uint32_t *alive, int e)
 // carries no per-column score.  Same integer as the reference DP
 // (metrics.py:54-84).
 // ---------------------------------------------------------------------------
-// x * 2 + 1 as one IMAD (fma pipe): the ALU pipe (LOP3) is the binding pipe
-// of the DP, so the shift-or of the +1 boundary row must not land there.
-__device__ __forceinline__ uint32_t shl1_or1(uint32_t x)
-{
-    uint32_t d;
-    asm("mad.lo.u32 %0, %1, 2, 1;" : "=r"(d) : "r"(x));
-    return d;
-}
+// The constant 2 from the constant bank: ptxas cannot fold a __constant__
+// value, so x * kTwo + 1 (the +1-boundary shift) and sym * kTwo * kTwo + base
+// (the mask address) stay IMADs on the fma pipe instead of LEA / SHF+LOP on
+// the ALU pipe, which is the binding pipe of the DP (7 LOP3 per step).
+__constant__ uint32_t kTwo = 2u;
 
 __device__ __forceinline__ void myers_step1(uint32_t Eq, uint32_t &Pv, uint32_t &Mv)
 {
@@ -118,9 +118,9 @@ __device__ __forceinline__ void myers_step1(uint32_t Eq, uint32_t &Pv, uint32_t 
     const uint32_t D0 = (((X & Pv) + Pv) ^ Pv) | X;
     const uint32_t HN = Pv & D0;
     const uint32_t HP = Mv | ~(Pv | D0);
-    const uint32_t Xs = shl1_or1(HP);
+    const uint32_t Xs = HP * kTwo + 1u;
     Mv = Xs & D0;
-    Pv = (HN << 1) | ~(Xs | D0);
+    Pv = (HN * kTwo) | ~(Xs | D0);
 }
 
 __device__ __forceinline__ void myers_stepb(uint32_t Eq, uint32_t &Pv, uint32_t &Mv, uint32_t &hp, uint32_t &hm)
@@ -143,7 +143,8 @@ template <int W>
 __device__ __forceinline__ void myers_char(const uint32_t *peq, uint32_t c, uint32_t (&P)[W], uint32_t (&M)[W])
 {
     if (W == 1) {
-        myers_step1(peq[c], P[0], M[0]);
+        myers_step1(*reinterpret_cast<const uint32_t *>(reinterpret_cast<const char *>(peq) + c * (kTwo * kTwo)),
+                    P[0], M[0]);
     } else {
         uint32_t hp = 1u, hm = 0u;
 #pragma unroll
@@ -157,9 +158,10 @@ __device__ __forceinline__ void myers_char(const uint32_t *peq, uint32_t c, uint
 template <int W>
 __device__ __forceinline__ void myers_word(const uint32_t *peq, uint32_t w, uint32_t (&P)[W], uint32_t (&M)[W])
 {
+    // one ALU op per symbol: LOP (byte 0), PRMT (bytes 1, 2), SHF (byte 3)
     myers_char<W>(peq, w & 0xffu, P, M);
-    myers_char<W>(peq, (w >> 8) & 0xffu, P, M);
-    myers_char<W>(peq, (w >> 16) & 0xffu, P, M);
+    myers_char<W>(peq, __byte_perm(w, 0u, 0x4441), P, M);
+    myers_char<W>(peq, __byte_perm(w, 0u, 0x4442), P, M);
     myers_char<W>(peq, w >> 24, P, M);
 }
 
@@ -372,6 +374,20 @@ __device__ __forceinline__ float dist32(const IndexView &ix, const QueryView &qv
 __device__ __forceinline__ float slack(const IndexView &ix, float a, float b, float c = 0.f)
 {
     return ix.rel > 0.f ? ix.rel * (fabsf(a) + fabsf(b) + fabsf(c)) + ix.abs_eps : ix.abs_eps;
+}
+
+// Lemma-1 entry test for float metrics (search.py:523, 559) with the fp32
+// slack folded into one FFMA: |dis - dqp| - rel*dis <= r + rel*(dqp + r) + eps,
+// i.e. |dis - dqp| <= r + rel*(dis + dqp + r) + eps.  Every float kernel uses
+// this one expression, so all paths count the same "verified" entries; a NaN
+// dis (tombstoned / padding column) fails it.
+__device__ __forceinline__ float lemma1_rrow(const IndexView &ix, float dqp, float r)
+{
+    return r + (ix.rel * (dqp + r) + ix.abs_eps);
+}
+__device__ __forceinline__ bool lemma1_pass(const IndexView &ix, float dis, float dqp, float rrow)
+{
+    return fmaf(-ix.rel, dis, fabsf(dis - dqp)) <= rrow;
 }
 
 }  // namespace gts

@@ -1,6 +1,7 @@
-"""A/B: the tensor-core L2 path and the CUDA-core path give identical answers
-and identical verified counts (GTS_NO_MMA selects the CUDA-core path at
-index creation; each variant runs in its own process)."""
+"""A/B: the tensor-core L2 paths (pipelined k_leafgroup_mma2, single-stage
+k_leafgroup_mma) and the CUDA-core path give identical answers and identical
+verified counts (GTS_NO_MMA selects the CUDA-core path at index creation,
+GTS_MMA_V1 the single-stage kernel; each variant runs in its own process)."""
 
 import json
 import os
@@ -38,8 +39,10 @@ def run(env_extra):
 
 
 def test_mma_equals_cuda_core_path():
-    a = run({})
-    b = run({"GTS_NO_MMA": "1"})
-    assert a["r"] == b["r"] and a["rd"] == b["rd"]
-    assert a["k"] == b["k"] and a["kd"] == b["kd"]
-    assert a["ver"] == b["ver"]
+    a = run({})                          # k_leafgroup_mma2 + k_recheck_l2 (default)
+    b = run({"GTS_NO_MMA": "1"})         # CUDA-core k_leafgroup_vec
+    c = run({"GTS_MMA_V1": "1"})         # single-stage k_leafgroup_mma, inline recheck
+    for x in (b, c):
+        assert a["r"] == x["r"] and a["rd"] == x["rd"]
+        assert a["k"] == x["k"] and a["kd"] == x["kd"]
+        assert a["ver"] == x["ver"]

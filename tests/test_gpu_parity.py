@@ -18,15 +18,18 @@ from oracle import oracle as O
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["grouped", "rowwise"], autouse=True)
+@pytest.fixture(params=["default", "rowwise", "edit_grouped"], autouse=True)
 def leaf_path(request, monkeypatch):
-    """Every test runs on both leaf-verification paths: leaf-grouped
-    (k_leafgroup_edit / k_leafgroup_vec / k_leafgroup_mma, the default) and
-    row-wise (k_leaf_edit / k_verify, GTS_NO_GROUPED=1)."""
+    """Every test runs on each leaf-verification path: default (k_leaf_edit;
+    k_leafgroup_mma2 / k_leafgroup_vec for vectors), row-wise vectors
+    (k_verify, GTS_NO_GROUPED=1) and leaf-grouped edit (k_leafgroup_edit,
+    GTS_EDIT_GROUPED=1)."""
+    monkeypatch.delenv("GTS_NO_GROUPED", raising=False)
+    monkeypatch.delenv("GTS_EDIT_GROUPED", raising=False)
     if request.param == "rowwise":
         monkeypatch.setenv("GTS_NO_GROUPED", "1")
-    else:
-        monkeypatch.delenv("GTS_NO_GROUPED", raising=False)
+    elif request.param == "edit_grouped":
+        monkeypatch.setenv("GTS_EDIT_GROUPED", "1")
     return request.param
 
 
