@@ -327,7 +327,7 @@ constexpr int kWarpPeqWords = 1024;     // per-warp staged match masks (A*W <= 1
 // memory.  Leaves are length-sorted, so a batch has similar DP lengths.
 constexpr int kHistBins = 256;   // kNN shrinking-bound histogram: exact distances 0..255
 
-__global__ void __launch_bounds__(256, 4) k_leaf_edit(IndexView ix, QueryView qv, const Row *__restrict__ rows,
+__global__ void __launch_bounds__(256, 3) k_leaf_edit(IndexView ix, QueryView qv, const Row *__restrict__ rows,
                                                       int64_t m, int pruning, float *r32,
                                                       HitBuf out, unsigned long long *verified_stat, int stats_on,
                                                       unsigned long long *work, unsigned long long *cursor,
@@ -478,10 +478,13 @@ __global__ void __launch_bounds__(256, 4) k_leaf_edit(IndexView ix, QueryView qv
                 pass = !pruning || fabsf(__uint_as_float(rec.x) - lr.dqp) <= r;
             ver += __popc(__ballot_sync(kFull, pass));
             const int len = (int)rec.y;
-            bool cand = pass && (float)abs(mq - len) <= r;
-            if (cand && ix.ehist) {
+            // integer radius: edit distances are integers, r32 holds floor(r)
+            const int ri = r < 1e9f ? (int)r : (1 << 30);
+            bool cand = pass && abs(mq - len) <= ri;
+            // the histogram bound never exceeds max(|q|, |o|): skip it when that fits
+            if (cand && ix.ehist && max(mq, len) > ri) {
                 const uint4 h0 = __ldg(ix.ehist + 2 * e), h1 = __ldg(ix.ehist + 2 * e + 1);
-                cand = (float)hist_lb(qh0, qh1, h0, h1, mq - len) <= r;
+                cand = hist_lb(qh0, qh1, h0, h1, mq - len) <= ri;
             }
             const unsigned cb = __ballot_sync(kFull, cand);
             if (cand) {
@@ -557,19 +560,32 @@ struct Item {
 };
 constexpr int kItemQueries = 128;
 
+// Counting sort of frontier rows by node.  Warp-aggregated: lanes holding the
+// same node elect one atomic (upper layers have only 1-20 distinct nodes, so
+// per-row atomics would serialise on a handful of counters).
 __global__ void k_leaf_hist(const Row *rows, int64_t m, int leaf_first, int *cnt)
 {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < m) atomicAdd(cnt + (rows[i].node - leaf_first), 1);
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int key = i < m ? rows[i].node - leaf_first : -1;
+    const unsigned peers = __match_any_sync(kFull, key);
+    if (key >= 0 && lane_id() == __ffs(peers) - 1) atomicAdd(cnt + key, __popc(peers));
 }
 
 __global__ void k_leaf_scatter(const Row *rows, int64_t m, int leaf_first, int *cursor, Row *out)
 {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    Row r{0, 0, 0.f, 0};
+    int key = -1;
     if (i < m) {
-        const Row r = rows[i];
-        out[atomicAdd(cursor + (r.node - leaf_first), 1)] = r;
+        r = rows[i];
+        key = r.node - leaf_first;
     }
+    const unsigned peers = __match_any_sync(kFull, key);
+    const int leader = __ffs(peers) - 1, lane = lane_id();
+    int base = 0;
+    if (key >= 0 && lane == leader) base = atomicAdd(cursor + key, __popc(peers));
+    base = __shfl_sync(kFull, base, leader);
+    if (key >= 0) out[base + __popc(peers & ((1u << lane) - 1u))] = r;
 }
 
 __global__ void k_item_counts(const int *cnt, int nleaf, int per, int *nitem)
@@ -864,8 +880,11 @@ __global__ void __launch_bounds__(256) k_expand_grouped(IndexView ix, QueryView 
                                                         unsigned long long *counter, unsigned long long *pruned_stat)
 {
     extern __shared__ float4 ex_smem4[];
-    float *piv_s = reinterpret_cast<float *>(ex_smem4);                 // [nc][Dp]
-    NodeRec *rec_s = reinterpret_cast<NodeRec *>(piv_s + (size_t)ix.nc * ix.Dp);
+    // [nc][Dp + 4]: the 16-byte row skew puts the nc children of one row on
+    // different banks (a 512-byte stride would make them a 20-way conflict)
+    const int ps = ix.Dp + 4;
+    float *piv_s = reinterpret_cast<float *>(ex_smem4);
+    NodeRec *rec_s = reinterpret_cast<NodeRec *>(piv_s + (size_t)ix.nc * ps);
     __shared__ int sh_warp[32];
     __shared__ unsigned long long sh_base;
     const int nc = ix.nc, d4 = ix.Dp >> 2;
@@ -877,7 +896,7 @@ __global__ void __launch_bounds__(256) k_expand_grouped(IndexView ix, QueryView 
         __syncthreads();
         for (int t = threadIdx.x; t < nc * d4; t += blockDim.x) {
             const int j = t / d4, c = t - j * d4;
-            reinterpret_cast<float4 *>(piv_s)[t] =
+            reinterpret_cast<float4 *>(piv_s + (size_t)j * ps)[c] =
                 __ldg(reinterpret_cast<const float4 *>(ix.vec32 + (size_t)rec_s[j].piv * ix.Dp) + c);
         }
         __syncthreads();
@@ -904,7 +923,7 @@ __global__ void __launch_bounds__(256) k_expand_grouped(IndexView ix, QueryView 
                 if (keep) {
                     float acc = 0.f;
                     const float4 *qp = reinterpret_cast<const float4 *>(qv.vec32 + (size_t)q * ix.Dp);
-                    const float4 *pp = reinterpret_cast<const float4 *>(piv_s + (size_t)j * ix.Dp);
+                    const float4 *pp = reinterpret_cast<const float4 *>(piv_s + (size_t)j * ps);
                     for (int k = 0; k < d4; k++) {
                         const float4 x = pp[k], y = __ldg(qp + k);
                         const float d0 = x.x - y.x, d1 = x.y - y.y, d2 = x.z - y.z, d3 = x.w - y.w;
@@ -1359,11 +1378,21 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
         const int lc = c16 == 16 ? 4 : 3;
         const int c = tid & (c16 - 1), row0 = tid >> lc, rstep = kM2Threads >> lc;
         const uint32_t aoff = (uint32_t)(c >> 3) * 16384u, boff = (uint32_t)(c >> 3) * (uint32_t)N * 128u;
-        for (int row = row0; row < 128; row += rstep) {
-            const bool ok = row < item.count;
-            const int q = ok ? srows[item.start + row].q : 0;
-            tc::cp_async16(tc::smem_u32(A + aoff + tc::sw128_offset(row, c & 7)), qv.qbf + (size_t)q * c16 + c,
-                           ok ? 16u : 0u);
+        // all query-id loads first (independent, in flight together), then the
+        // copies: a load -> cp.async chain per row would serialise L2 latencies
+        constexpr int kMaxRowsPerThread = 128 / (kM2Threads / 16);   // c16 = 16: 4 rows; c16 = 8: 2
+        int qrow[kMaxRowsPerThread];
+#pragma unroll
+        for (int u = 0; u < kMaxRowsPerThread; u++) {
+            const int row = row0 + u * rstep;
+            qrow[u] = (row < 128 && row < item.count) ? srows[item.start + row].q : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < kMaxRowsPerThread; u++) {
+            const int row = row0 + u * rstep;
+            if (row < 128)
+                tc::cp_async16(tc::smem_u32(A + aoff + tc::sw128_offset(row, c & 7)),
+                               qv.qbf + (size_t)max(qrow[u], 0) * c16 + c, qrow[u] >= 0 ? 16u : 0u);
         }
         for (int row = row0; row < N; row += rstep) {
             const bool ok = row < leaf.size;
@@ -2517,7 +2546,7 @@ struct Search {
             }
             HitBuf hb{hq.p, he.p, hd.p, (unsigned long long)hq.n, counter.p + 1};
             // one warp per ~contiguous run of rows; enough warps to fill the GPU
-            unsigned grid = grid_for((m + kRowChunk - 1) / kRowChunk, kLeafWarps, 148u * 4u);
+            unsigned grid = grid_for((m + kRowChunk - 1) / kRowChunk, kLeafWarps, 148u * 3u);   // 3 resident per SM
             CK(cudaMemsetAsync(counter.p, 0, sizeof(unsigned long long), st));
             timed("k_leaf_edit", [&] {
                 k_leaf_edit<<<grid, 32 * kLeafWarps, 0, st>>>(iv, qv, rows, m, pruning, r32.p, hb, verified.p,
@@ -2545,7 +2574,7 @@ struct Search {
             group_rows(in, m, G, kItemQueries, first, (int)c);
             CK(cudaMemsetAsync(counter.p, 0, sizeof(unsigned long long), st));
             if (G.nitems == 0) return 0;
-            const size_t smb = (size_t)ix->nc * ix->Dp * sizeof(float) + (size_t)ix->nc * sizeof(NodeRec);
+            const size_t smb = (size_t)ix->nc * (ix->Dp + 4) * sizeof(float) + (size_t)ix->nc * sizeof(NodeRec);
             static size_t attr[3] = {0, 0, 0};
             if (attr[MET] < smb) {
                 CK(cudaFuncSetAttribute(k_expand_grouped<MET>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
