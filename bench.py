@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import argparse
 import ctypes as C
+import gc
 import json
 import os
 import statistics
@@ -329,6 +330,8 @@ def run_stream(args, rank, world, local_rank):
         return sum(x[0].size for x in a) + sum(x[0].size for x in b)
 
     clocks = ClockSampler(local_rank, args.clock_ms)
+    gc.collect()
+    gc.disable()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -342,6 +345,7 @@ def run_stream(args, rank, world, local_rank):
     ms = (time.perf_counter() - t0) * 1e3 / args.steps
     clk = clocks.stop()
     clocks.close()
+    gc.enable()
     if rank != 0:
         return None
     nq = w["nq"]
@@ -390,6 +394,10 @@ def run_ours(args, rank, world, local_rank):
         eng.free(hs)
 
     clocks = ClockSampler(local_rank, args.clock_ms)
+    # no Python garbage-collector pauses inside timed steps (a gen-2 pass over
+    # the interpreter's objects idles the GPU for 100s of ms between calls)
+    gc.collect()
+    gc.disable()
     # warm-up
     for _ in range(args.warmup):
         one_step()
@@ -437,6 +445,7 @@ def run_ours(args, rank, world, local_rank):
 
     # e2e through the host C ABI with pinned buffers
     e2e_ms, h2d, d2h = run_e2e(eng, w, args, sp, merger, world, max(totals))
+    gc.enable()
 
     if rank != 0:
         return None

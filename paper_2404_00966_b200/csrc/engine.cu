@@ -327,7 +327,7 @@ constexpr int kWarpPeqWords = 1024;     // per-warp staged match masks (A*W <= 1
 // memory.  Leaves are length-sorted, so a batch has similar DP lengths.
 constexpr int kHistBins = 256;   // kNN shrinking-bound histogram: exact distances 0..255
 
-__global__ void __launch_bounds__(256, 3) k_leaf_edit(IndexView ix, QueryView qv, const Row *__restrict__ rows,
+__global__ void __launch_bounds__(256, 4) k_leaf_edit(IndexView ix, QueryView qv, const Row *__restrict__ rows,
                                                       int64_t m, int pruning, float *r32,
                                                       HitBuf out, unsigned long long *verified_stat, int stats_on,
                                                       unsigned long long *work, unsigned long long *cursor,
@@ -457,41 +457,35 @@ __global__ void __launch_bounds__(256, 3) k_leaf_edit(IndexView ix, QueryView qv
         leaf.size = __shfl_sync(kFull, pn.size, src);
         const int pos = __shfl_sync(kFull, ppos, src);
         unsigned ver = 0;
-        // the chunk's records and alive bits are loaded one chunk ahead
+        // the chunk's records are loaded one chunk ahead.  erec = {dis (NaN
+        // when tombstoned, k_erec_alive), len, first text word, float(len)}:
+        // the tombstone, lemma-1 and length tests are FP compares (fma pipe),
+        // leaving the ALU pipe to the DP
         uint4 nrec = make_uint4(0u, 0u, 0u, 0u);
-        uint32_t nal = 0u;
-        if (lane < leaf.size) {
-            nrec = __ldg(ix.erec + pos + lane);
-            nal = __ldg(ix.alive + ((pos + lane) >> 5));
-        }
+        if (lane < leaf.size) nrec = __ldg(ix.erec + pos + lane);
+        const float mqf = (float)mq;
+        const int ri = r < 1e9f ? (int)r : (1 << 30);   // edit distances are integers
         for (int b = 0; b < leaf.size; b += kWarp) {
             const int k = b + lane;
             const int e = pos + k;
             const uint4 rec = nrec;
-            const uint32_t al = nal;
-            if (b + kWarp + lane < leaf.size) {
-                nrec = __ldg(ix.erec + e + kWarp);
-                nal = __ldg(ix.alive + ((e + kWarp) >> 5));
-            }
+            if (b + kWarp + lane < leaf.size) nrec = __ldg(ix.erec + e + kWarp);
+            const float dis = __uint_as_float(rec.x), lenf = __uint_as_float(rec.w);
             bool pass = false;
-            if (k < leaf.size && ((al >> (e & 31)) & 1u))
-                pass = !pruning || fabsf(__uint_as_float(rec.x) - lr.dqp) <= r;
+            if (k < leaf.size) pass = pruning ? fabsf(dis - lr.dqp) <= r : dis == dis;
             ver += __popc(__ballot_sync(kFull, pass));
-            const int len = (int)rec.y;
-            // integer radius: edit distances are integers, r32 holds floor(r)
-            const int ri = r < 1e9f ? (int)r : (1 << 30);
-            bool cand = pass && abs(mq - len) <= ri;
+            bool cand = pass && fabsf(mqf - lenf) <= r;
             // the histogram bound never exceeds max(|q|, |o|): skip it when that fits
-            if (cand && ix.ehist && max(mq, len) > ri) {
+            if (cand && ix.ehist && fmaxf(mqf, lenf) > r) {
                 const uint4 h0 = __ldg(ix.ehist + 2 * e), h1 = __ldg(ix.ehist + 2 * e + 1);
-                cand = hist_lb(qh0, qh1, h0, h1, mq - len) <= ri;
+                cand = hist_lb(qh0, qh1, h0, h1, mq - (int)rec.y) <= ri;
             }
             const unsigned cb = __ballot_sync(kFull, cand);
             if (cand) {
                 const int slot = qn + __popc(cb & ((1u << lane) - 1u));
                 qu[slot] = e;
                 qw[slot] = (int32_t)rec.z;
-                ql[slot] = len;
+                ql[slot] = (int)rec.y;
             }
             qn += __popc(cb);
             __syncwarp();
@@ -517,6 +511,15 @@ __global__ void __launch_bounds__(256, 3) k_leaf_edit(IndexView ix, QueryView qv
             atomicAdd(work + kWorkRows, nrows);
         }
     }
+}
+
+// erec.x = dis of live entries, NaN of tombstoned ones (every test fails)
+__global__ void k_erec_alive(uint4 *erec, const float *dis, const uint32_t *alive, int64_t n)
+{
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n) return;
+    const bool al = (alive[e >> 5] >> (e & 31)) & 1u;
+    erec[e].x = al ? __float_as_uint(dis[e]) : 0x7fc00000u;
 }
 
 // Packed sort key for exact small-integer distances: query | distance |
@@ -1339,100 +1342,129 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
                  unsigned long long *verified_stat, int stats_on, unsigned long long *work, uint32_t acc_cols,
                  int nmax, unsigned *fhist, const float *r0, const int32_t *ks)
 {
+    // Software pipeline over this CTA's items (static order it_i = bid + i*G):
+    //   iteration i: cp.async operands of item i+1 | global loads of item i+2's
+    //   row/column metadata and item i+3's descriptor (into registers) |
+    //   epilogue of item i | store the loaded metadata | barrier | MMA i+1.
+    // Every global-load latency is hidden behind an epilogue; one block
+    // barrier per item.
     extern __shared__ __align__(1024) uint8_t smraw[];
     __shared__ uint64_t mbar[2];
     __shared__ uint32_t tmem_slot;
-    // per column: {dis (NaN when tombstoned), dis^2 + 2 se, 8 rel dis^2, 0}
-    __shared__ float4 s_col[2][256];
-    __shared__ int s_rq[2][128];         // per stage: the item's query ids
-    __shared__ float4 s_rf[2][128];      // {dqp, r (at staging; radii only shrink), |q|, probe radius}
-    __shared__ int s_next[2];
+    __shared__ int4 s_item[4];           // {leaf, start, count, size}, ring by i % 4
+    __shared__ int s_pos[4];
+    __shared__ float4 s_col[3][256];     // ring by i % 3: {dis | NaN, y - z, y + z, dis}
+    __shared__ int s_rq[3][128];         // query ids (-1: no row)
+    __shared__ float4 s_rf[3][128];      // {dqp, r at load time (radii only shrink), |q|, probe radius}
+    (void)item_cursor;
     const uint32_t pad = (1024u - (tc::smem_u32(smraw) & 1023u)) & 1023u;
     uint8_t *sm = smraw + pad;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int nkb = ix.Dk >> 6;                        // 128-byte K-blocks per row
-    const int c16 = ix.Dk >> 3;                        // 16-byte chunks per row
+    const int nkb = ix.Dk >> 6;
+    const int c16 = ix.Dk >> 3;
     const size_t a_bytes = (size_t)nkb * 16384;
     const size_t stage_bytes = a_bytes + (size_t)nkb * nmax * 128;
+    const int G = gridDim.x;
+    auto idx = [&](int i) { return (int)blockIdx.x + i * G; };
     if (warp == 0) tc::tmem_alloc(&tmem_slot, 2 * acc_cols);
     if (tid == 0) {
         tc::mbar_init(&mbar[0], 1);
         tc::mbar_init(&mbar[1], 1);
         tc::fence_mbar_init();
     }
+    // descriptors of items 0..2
+    if (tid < 3) {
+        int4 d = make_int4(0, 0, 0, 0);
+        int p0 = 0;
+        if (idx(tid) < nitems) {
+            const Item it = items[idx(tid)];
+            d = make_int4(it.leaf, it.start, it.count, ix.node[it.leaf].size);
+            p0 = ix.npos[it.leaf];
+        }
+        s_item[tid] = d;
+        s_pos[tid] = p0;
+    }
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tmem = tmem_slot;
 
-
-    // operands + metadata of item `it` into stage `st` (async copies)
-    auto stage = [&](int st, int it) {
-        const Item item = items[it];
-        const NodeRec leaf = ix.node[item.leaf];
-        const int pos = ix.npos[item.leaf];
-        const int N = max(16, (leaf.size + 15) & ~15);
+    // metadata loads of item i (registers), then the store into ring slot i % 3
+    struct Meta {
+        int q;
+        float4 rf;
+        float dis, se;
+        bool al;
+    };
+    auto meta_load = [&](int i, Meta &m) {
+        const int4 d = s_item[i & 3];
+        const int pos = s_pos[i & 3];
+        m.q = -1;
+        m.rf = make_float4(0.f, -1.f, 0.f, 0.f);
+        m.dis = 0.f;
+        m.se = 0.f;
+        m.al = false;
+        if (idx(i) >= nitems) return;
+        if (tid < 128 && tid < d.z) {
+            const Row lr = srows[d.y + tid];
+            m.q = lr.q;
+            m.rf = make_float4(lr.dqp, __ldcg(r32 + lr.q), qv.qn[lr.q], r0 ? r0[lr.q] : 0.f);
+        }
+        if (tid < d.w) {
+            m.dis = __ldg(ix.dis + pos + tid);
+            m.se = __ldg(ix.vse + pos + tid);
+            m.al = is_alive(ix.alive, pos + tid);
+        }
+    };
+    auto meta_store = [&](int i, const Meta &m) {
+        const int sl = i % 3;
+        const int4 d = s_item[i & 3];
+        const int N = max(16, (d.w + 15) & ~15);
+        if (tid < 128) {
+            s_rq[sl][tid] = m.q;
+            s_rf[sl][tid] = m.rf;
+        }
+        if (tid < N) {
+            float4 col = make_float4(__int_as_float(0x7fc00000), 0.f, 0.f, 0.f);   // padding: NaN fails
+            if (tid < d.w) {
+                const float y = fmaf(m.dis, m.dis, 2.f * m.se), z = 8.f * ix.rel * m.dis * m.dis;
+                if (m.al) col.x = m.dis;
+                col.y = y - z;
+                col.z = y + z;
+                col.w = m.dis;
+            }
+            s_col[sl][tid] = col;
+        }
+    };
+    // operands of item i into smem stage i & 1 (async)
+    auto stage = [&](int i) {
+        const int st = i & 1;
+        const int4 d = s_item[i & 3];
+        const int pos = s_pos[i & 3];
+        const int N = max(16, (d.w + 15) & ~15);
         uint8_t *A = sm + st * stage_bytes;
         uint8_t *B = A + a_bytes;
-        // c16 is 8 or 16 (Dk 64 / 128): thread -> fixed chunk, rows step by 512 / c16
         const int lc = c16 == 16 ? 4 : 3;
         const int c = tid & (c16 - 1), row0 = tid >> lc, rstep = kM2Threads >> lc;
         const uint32_t aoff = (uint32_t)(c >> 3) * 16384u, boff = (uint32_t)(c >> 3) * (uint32_t)N * 128u;
-        // all query-id loads first (independent, in flight together), then the
-        // copies: a load -> cp.async chain per row would serialise L2 latencies
-        constexpr int kMaxRowsPerThread = 128 / (kM2Threads / 16);   // c16 = 16: 4 rows; c16 = 8: 2
-        int qrow[kMaxRowsPerThread];
-#pragma unroll
-        for (int u = 0; u < kMaxRowsPerThread; u++) {
-            const int row = row0 + u * rstep;
-            qrow[u] = (row < 128 && row < item.count) ? srows[item.start + row].q : -1;
-        }
-#pragma unroll
-        for (int u = 0; u < kMaxRowsPerThread; u++) {
-            const int row = row0 + u * rstep;
-            if (row < 128)
-                tc::cp_async16(tc::smem_u32(A + aoff + tc::sw128_offset(row, c & 7)),
-                               qv.qbf + (size_t)max(qrow[u], 0) * c16 + c, qrow[u] >= 0 ? 16u : 0u);
+        const int *rq = s_rq[i % 3];
+        for (int row = row0; row < 128; row += rstep) {
+            const int q = rq[row];
+            tc::cp_async16(tc::smem_u32(A + aoff + tc::sw128_offset(row, c & 7)), qv.qbf + (size_t)max(q, 0) * c16 + c,
+                           q >= 0 ? 16u : 0u);
         }
         for (int row = row0; row < N; row += rstep) {
-            const bool ok = row < leaf.size;
+            const bool ok = row < d.w;
             tc::cp_async16(tc::smem_u32(B + boff + tc::sw128_offset(row, c & 7)),
                            ix.vcent + (size_t)(pos + (ok ? row : 0)) * c16 + c, ok ? 16u : 0u);
         }
         tc::cp_async_commit();
-        if (tid < 128) {
-            // row metadata, prefetched one item ahead of the epilogue
-            int q = 0;
-            float4 f = make_float4(0.f, -1.f, 0.f, 0.f);
-            if (tid < item.count) {
-                const Row lr = srows[item.start + tid];
-                q = lr.q;
-                f = make_float4(lr.dqp, __ldcg(r32 + q), qv.qn[q], r0 ? r0[q] : 0.f);
-            }
-            s_rq[st][tid] = q;
-            s_rf[st][tid] = f;
-        }
-        for (int j = tid; j < N; j += kM2Threads) {   // padding columns: NaN fails every test
-            // {dis (NaN if tombstoned), y - z, y + z, dis} with y = dis^2 + 2 se
-            // and z = 8 rel dis^2 (the dis^2 part of the error band)
-            float4 col = make_float4(__int_as_float(0x7fc00000), 0.f, 0.f, 0.f);
-            if (j < leaf.size) {
-                const float dis = __ldg(ix.dis + pos + j);
-                const float se = __ldg(ix.vse + pos + j);
-                const float y = fmaf(dis, dis, 2.f * se), z = 8.f * ix.rel * dis * dis;
-                if (is_alive(ix.alive, pos + j)) col.x = dis;
-                col.y = y - z;
-                col.z = y + z;
-                col.w = dis;
-            }
-            s_col[st][j] = col;
-        }
     };
-    auto mma = [&](int st, int it) {
+    auto mma = [&](int i) {
         if (tid != 0) return;
         tc::fence_after_sync();
-        const Item item = items[it];
-        const int N = max(16, (ix.node[item.leaf].size + 15) & ~15);
+        const int st = i & 1;
+        const int N = max(16, (s_item[i & 3].w + 15) & ~15);
         const uint32_t idesc = tc::idesc_bf16(128, N);
         const uint32_t a0 = tc::smem_u32(sm + st * stage_bytes), b0 = a0 + (uint32_t)a_bytes;
         for (int kb = 0; kb < nkb; kb++) {
@@ -1446,46 +1478,54 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
         tc::mma_commit(&mbar[st]);
     };
 
-    // item claims run one iteration ahead through s_next[2] (iteration i
-    // reads slot i & 1, thread 0 fills slot (i + 1) & 1), so each iteration
-    // needs a single block barrier
-    if (tid == 0) s_next[0] = (int)atomicAdd(item_cursor, 1ull);
+    // prologue: metadata of items 0 and 1, operands + MMA of item 0
+    {
+        Meta m0, m1;
+        meta_load(0, m0);
+        meta_load(1, m1);
+        meta_store(0, m0);
+        meta_store(1, m1);
+    }
     __syncthreads();
-    int cur = s_next[0];
-    if (cur < nitems) {
-        stage(0, cur);
-        if (tid == 0) s_next[1] = (int)atomicAdd(item_cursor, 1ull);
+    if (idx(0) < nitems) {
+        stage(0);
         tc::cp_async_wait_all();
         tc::fence_async_smem();
         __syncthreads();
-        mma(0, cur);
+        mma(0);
     }
     uint32_t phase[2] = {0u, 0u};
-    int s = 0, iter = 1;
     unsigned long long pairs = 0;
-    while (cur < nitems) {
-        const int nxt = s_next[iter & 1];
-        if (nxt < nitems) {
-            stage(s ^ 1, nxt);
-            if (tid == 0) s_next[(iter + 1) & 1] = (int)atomicAdd(item_cursor, 1ull);
+    for (int i = 0; idx(i) < nitems; i++) {
+        const int s = i & 1;
+        const bool has1 = idx(i + 1) < nitems;
+        if (has1) stage(i + 1);
+        Meta mnext;
+        meta_load(i + 2, mnext);
+        int4 dn = make_int4(0, 0, 0, 0);
+        int pn = 0;
+        if (tid == 0 && idx(i + 3) < nitems) {
+            const Item it = items[idx(i + 3)];
+            dn = make_int4(it.leaf, it.start, it.count, ix.node[it.leaf].size);
+            pn = ix.npos[it.leaf];
         }
-        iter++;
         tc::mbar_wait(&mbar[s], phase[s]);
         phase[s] ^= 1u;
         tc::fence_after_sync();
-        // ---- epilogue of item `cur` (stage s, accumulator s) ----
+        // ---- epilogue of item i (stage s, accumulator s, metadata slot i % 3) ----
         // thread = one query row (TMEM lane) x every 4th 16-column chunk;
         // per column: lemma 1, approximate d^2, error band, ~12 instructions
         {
-            const Item item = items[cur];
-            const int size = ix.node[item.leaf].size;
-            const int pos = ix.npos[item.leaf];
+            const int sl = i % 3;
+            const int4 d = s_item[i & 3];
+            const int size = d.w;
+            const int pos = s_pos[i & 3];
             const int N = max(16, (size + 15) & ~15);
             const int qrow = 32 * (warp & 3) + lane;
             const int part = warp >> 2;
-            const bool valid = qrow < item.count;
-            const int q = s_rq[s][qrow];
-            const float4 rf = s_rf[s][qrow];
+            const int q = s_rq[sl][qrow];
+            const bool valid = q >= 0;
+            const float4 rf = s_rf[sl][qrow];
             const float dqp = rf.x, qnorm = rf.z;
             float r = rf.y;
             // folded thresholds: with y - z, y + z per column,
@@ -1504,7 +1544,7 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
                 T1 = R2 + kq - dq2 + mg;
                 T2 = R2 - kq - dq2 - mg;
             };
-            set_r(r);
+            set_r(r);   // loaded two items ago: stale radii are larger, i.e. conservative
             float hinv = 0.f;   // kNN histogram: bins per unit distance
             if (fhist && valid) {
                 const float R0 = rf.w;
@@ -1518,7 +1558,7 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
                 uint32_t cm = 0, fm = 0;
 #pragma unroll
                 for (int jj = 0; jj < 16; jj++) {
-                    const float4 col = s_col[s][c0 + jj];   // broadcast LDS.128
+                    const float4 col = s_col[sl][c0 + jj];   // broadcast LDS.128
                     const bool pass = lemma1_pass(ix, col.x, dqp, rrow);
                     const float m2a = fmaf(-2.f, acc[jj], col.y);
                     const float m2b = fmaf(-2.f, acc[jj], col.z);
@@ -1527,8 +1567,7 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
                     cm |= (uint32_t)cand << jj;
                     fm |= (uint32_t)(cand && fmaf(cA, col.w, m2b) <= T2) << jj;
                 }
-                if (c0 + 16 > size) cm &= (1u << (size - c0 > 0 ? size - c0 : 0)) - 1u, fm &= cm;
-                if (!valid) cm = fm = 0;
+                if (!valid) cm = fm = 0, ver = 0;
                 // warp-aggregated append of the chunk's candidates
                 const unsigned nc = __popc(cm);
                 unsigned incl = nc;
@@ -1545,7 +1584,7 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
                     for (int jj = 0; jj < 16; jj++) {
                         if (!((cm >> jj) & 1u)) continue;
                         if (base < cb.cap) {
-                            const float4 col = s_col[s][c0 + jj];
+                            const float4 col = s_col[sl][c0 + jj];
                             cb.q[base] = q;
                             cb.e[base] = pos + c0 + jj;
                             // d^2 lower bound, rounded down a little
@@ -1561,7 +1600,7 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
 #pragma unroll
                     for (int jj = 0; jj < 16; jj++) {
                         if (!((fm >> jj) & 1u)) continue;
-                        const float4 col = s_col[s][c0 + jj];
+                        const float4 col = s_col[sl][c0 + jj];
                         const float d2u = fmaf(cA, col.w, fmaf(-2.f, acc[jj], col.z)) + dq2 + kq +
                                           ldexpf(dq2 + qnorm * qnorm, -18);
                         const float dub = sqrtf(fmaxf(d2u, 0.f)) * (1.f + 1e-6f) + 1e-30f;
@@ -1577,19 +1616,22 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
             if (valid && stats_on && ver) atomicAdd(verified_stat + q, (unsigned long long)ver);
             pairs += ver;
             if (work && tid == 0) {
-                atomicAdd(work + kWorkEntries, (unsigned long long)size * item.count);
-                atomicAdd(work + kWorkRows, (unsigned long long)item.count);
+                atomicAdd(work + kWorkEntries, (unsigned long long)size * d.z);
+                atomicAdd(work + kWorkRows, (unsigned long long)d.z);
                 atomicAdd(work + kWorkSteps, (unsigned long long)128 * N * ix.Dk);   // MMA MACs issued
             }
+        }
+        // metadata of item i+2 and the descriptor of item i+3 (loads done by now)
+        meta_store(i + 2, mnext);
+        if (tid == 0) {
+            s_item[(i + 3) & 3] = dn;
+            s_pos[(i + 3) & 3] = pn;
         }
         tc::cp_async_wait_all();
         tc::fence_async_smem();
         tc::fence_before_sync();
         __syncthreads();
-        if (nxt >= nitems) break;
-        mma(s ^ 1, nxt);
-        s ^= 1;
-        cur = nxt;
+        if (has1) mma(i + 1);
     }
     if (work) {
         for (int o = 16; o > 0; o >>= 1) pairs += __shfl_down_sync(kFull, pairs, o);
@@ -2399,7 +2441,7 @@ struct Search {
         }
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
-        const unsigned grid = (unsigned)std::min<int>(nitems, sms);
+        const unsigned grid = (unsigned)std::min<int>(nitems, sms);   // items i, i + grid, ... per CTA
         size_t cap = std::max<size_t>((size_t)1 << 22, (size_t)ix->cand_hint.load());
         DBuf<unsigned long long> cnt(2, st);   // [0] item cursor, [1] candidates
         for (int attempt = 0;; attempt++) {
@@ -2546,7 +2588,7 @@ struct Search {
             }
             HitBuf hb{hq.p, he.p, hd.p, (unsigned long long)hq.n, counter.p + 1};
             // one warp per ~contiguous run of rows; enough warps to fill the GPU
-            unsigned grid = grid_for((m + kRowChunk - 1) / kRowChunk, kLeafWarps, 148u * 3u);   // 3 resident per SM
+            unsigned grid = grid_for((m + kRowChunk - 1) / kRowChunk, kLeafWarps, 148u * 4u);   // 4 resident per SM
             CK(cudaMemsetAsync(counter.p, 0, sizeof(unsigned long long), st));
             timed("k_leaf_edit", [&] {
                 k_leaf_edit<<<grid, 32 * kLeafWarps, 0, st>>>(iv, qv, rows, m, pruning, r32.p, hb, verified.p,
@@ -3274,7 +3316,10 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
                 float d = (float)t->dis[ord[(size_t)e]];
                 uint32_t db;
                 std::memcpy(&db, &d, 4);
-                rec[(size_t)e] = make_uint4(db, (uint32_t)lens[(size_t)e], wstart[(size_t)e], 0u);
+                const float lf = (float)lens[(size_t)e];
+                uint32_t lb;
+                std::memcpy(&lb, &lf, 4);
+                rec[(size_t)e] = make_uint4(db, (uint32_t)lens[(size_t)e], wstart[(size_t)e], lb);
             }
             for (int64_t i = ix->leaf_first; i < (int64_t)ix->leaf_first + ix->leaf_count; i++) {
                 if (t->size[i] <= 0) continue;
@@ -3284,6 +3329,8 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
             }
             ix->erec.alloc(rec.size(), st);
             h2d(ix->erec.p, rec.data(), rec.size(), st);
+            k_erec_alive<<<grid_for(n, 256), 256, 0, st>>>(ix->erec.p, ix->dis.p, ix->alive.p, n);
+            LAUNCH_CHECK();
             if (ix->A > kHistMinAlphabet) {
                 // 32 byte-buckets of symbol counts per entry (saturating)
                 std::vector<uint8_t> hb((size_t)n * 32, 0);
@@ -3398,6 +3445,10 @@ extern "C" int gts_index_set_tombstones(gts_index *ix, const uint8_t *tomb, void
         if (tomb[ix->ord[(size_t)e]] == 0) alive[(size_t)(e >> 5)] |= 1u << (e & 31);
     cudaStream_t st = (cudaStream_t)stream;
     h2d(ix->alive.p, alive.data(), alive.size(), st);
+    if (ix->erec.p) {
+        k_erec_alive<<<grid_for(ix->n, 256), 256, 0, st>>>(ix->erec.p, ix->dis.p, ix->alive.p, ix->n);
+        LAUNCH_CHECK();
+    }
     CK(cudaStreamSynchronize(st));
     return GTS_OK;
     ABI_END
