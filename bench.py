@@ -451,7 +451,7 @@ def run_ours(args, rank, world, local_rank):
         return None
     qps = 2 * nq * world / (ms / 1e3)
     # the dominant leaf-verification kernel of this workload (whichever ran)
-    cands = ("k_leafgroup_edit", "k_leaf_edit") if eng.edit else ("k_leafgroup_mma2", "k_leafgroup_mma", "k_leafgroup_vec", "k_verify")
+    cands = ("k_leafgroup_edit", "k_leaf_edit") if eng.edit else ("k_leafgroup_mma2", "k_leafgroup_mma", "k_leafgroup_tile", "k_leafgroup_vec", "k_verify")
     kname = max(cands, key=lambda k: prof["kernels"].get(k, {"ms": 0.0})["ms"])
     kver = dict(prof["kernels"].get(kname, {"ms": 0.0, "count": 0}), name=kname)
     work = prof["work"]
@@ -591,6 +591,17 @@ def roofline(eng, prof, kver, step_ms_prof):
             "unit": "TFLOP/s", "frac": round(achieved / tf, 5) if achieved else None, "traffic": None,
             "work_unit": f"2*D = {2 * D} bf16 tensor flops per lemma-1-passing (query, entry) pair",
             "peak_source": "MEASURED_PEAKS.json bf16" if peaks else "fallback 1590 TFLOP/s (B200_PROFILING.md)"})
+    if kver["name"] == "k_leafgroup_tile":
+        # register-tiled fp32 distances for every (query, entry) pair of an item:
+        # 2 fp32 ops per dimension (L1: sub, |.|-add; L2: sub, fma counted once)
+        ops = work["entries"] * 2 * D
+        pk = 148 * 128 * 1.965e9 / 1e12
+        achieved = ops / t / 1e12 if t else None
+        return dict(common, **{
+            "bound": "fp32", "achieved": round(achieved, 3) if achieved else None, "peak": round(pk, 2),
+            "unit": "Tops/s", "frac": round(achieved / pk, 4) if achieved else None, "traffic": None,
+            "work_unit": f"2*D = {2 * D} fp32 lane-ops per (query, entry) pair of an item",
+            "peak_source": "B200 nominal fp32 issue: 148 SMs x 128 lanes x 1.965 GHz (one op per lane per clock)"})
     hbm = peaks.get("hbm_gbs", 6650.0)
     bytes_alg = work["entries"] * 8 + work["pairs"] * 4 * D
     achieved = bytes_alg / t / 1e9 if t else None

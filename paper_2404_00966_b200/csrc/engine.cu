@@ -1044,6 +1044,183 @@ __global__ void __launch_bounds__(256) k_leafgroup_vec(IndexView ix, QueryView q
 }
 
 // ---------------------------------------------------------------------------
+// Register-tiled CUDA-core verification (L1, and L2 off the tensor-core
+// path).  Item = (leaf, <= 128 query rows); the block stages the leaf's
+// entries AND the item's query vectors in shared memory (rows padded by 16
+// bytes: conflict-free LDS.128), then every thread computes a 4 x 4 tile of
+// (query, entry) fp32 distances: lane -> query rows lane + 32a, warp -> entry
+// chunks of 4.  Per 4 dimensions that is 8 LDS.128 (4 per-lane query rows, 4
+// broadcast entry rows) for 64 pair-dimensions, so the FP32 pipes, not
+// shared memory, bound it.  Filters and outputs are those of
+// k_leafgroup_vec: lemma 1 (the verified count), fp32 screen with slack,
+// exact float64 recheck in numpy order, kNN histogram shrink.
+// ---------------------------------------------------------------------------
+// screened (query, entry) candidates awaiting the exact float64 recheck
+struct CandBuf {
+    int32_t *q, *e;
+    float *lb;                 // lower bound of the compared quantity (d^2 for L2, d for L1)
+    unsigned long long cap;
+    unsigned long long *counter;
+};
+
+template <int MET>
+__global__ void __launch_bounds__(256) k_leafgroup_tile(IndexView ix, QueryView qv, const Row *__restrict__ srows,
+                                                        const Item *__restrict__ items, int nitems, int pruning,
+                                                        float *r32, double *r64, CandBuf cb,
+                                                        unsigned long long *verified_stat, int stats_on,
+                                                        unsigned long long *work, unsigned *fhist, const float *r0,
+                                                        const int32_t *ks)
+{
+    extern __shared__ float4 tile_smem4[];
+    const int stride = ix.Dp + 4;
+    float *ent = reinterpret_cast<float *>(tile_smem4);                 // [max_leaf][stride]
+    float *qs = ent + (size_t)ix.max_leaf * stride;                       // [128][stride]
+    float *s_dis = qs + (size_t)128 * stride;                             // [max_leaf] (NaN: tombstoned)
+    float *s_dqp = s_dis + ix.max_leaf;                                   // [128]
+    float *s_r = s_dqp + 128;                                             // [128]
+    int *s_q = reinterpret_cast<int *>(s_r + 128);                        // [128]
+    unsigned *s_ver = reinterpret_cast<unsigned *>(s_q + 128);            // [128]
+    unsigned *s_nh = s_ver + 128;                                         // [128]
+    const int lane = lane_id(), warp = threadIdx.x >> 5;
+    const int d4 = ix.Dp >> 2;
+    unsigned long long w_entries = 0, w_rows = 0;
+    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+        const Item item = items[it];
+        const int size = ix.node[item.leaf].size;
+        const int pos = ix.npos[item.leaf];
+        __syncthreads();
+        if (threadIdx.x < 128) {
+            const int a = threadIdx.x;
+            int q = -1;
+            float dqp = 0.f, r = -1.f;
+            if (a < item.count) {
+                const Row lr = srows[item.start + a];
+                q = lr.q;
+                dqp = lr.dqp;
+                r = __ldcg(r32 + q);
+            }
+            s_q[a] = q;
+            s_dqp[a] = dqp;
+            s_r[a] = r;
+            s_ver[a] = 0;
+            s_nh[a] = 0;
+        }
+        for (int j = threadIdx.x; j < size; j += blockDim.x) {
+            const bool al = is_alive(ix.alive, pos + j);
+            s_dis[j] = al ? __ldg(ix.dis + pos + j) : __int_as_float(0x7fc00000);
+        }
+        for (int t = threadIdx.x; t < size * d4; t += blockDim.x) {
+            const int e = t / d4, c = t - e * d4;
+            *reinterpret_cast<float4 *>(ent + e * stride + 4 * c) =
+                __ldg(reinterpret_cast<const float4 *>(ix.vec32 + (size_t)(pos + e) * ix.Dp) + c);
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < 128 * d4; t += blockDim.x) {
+            const int a = t / d4, c = t - a * d4;
+            const int q = s_q[a];
+            *reinterpret_cast<float4 *>(qs + a * stride + 4 * c) =
+                q >= 0 ? __ldg(reinterpret_cast<const float4 *>(qv.vec32 + (size_t)q * ix.Dp) + c)
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        __syncthreads();
+        const int nchunks = (size + 3) >> 2;
+        unsigned ver[4] = {0u, 0u, 0u, 0u};
+        for (int ch = warp; ch < nchunks; ch += 8) {
+            const int e0 = ch * 4;
+            float acc[4][4];
+#pragma unroll
+            for (int a = 0; a < 4; a++)
+#pragma unroll
+                for (int b = 0; b < 4; b++) acc[a][b] = 0.f;
+            const float *qrow = qs + lane * stride;
+            const float *erow = ent + e0 * stride;
+            for (int c = 0; c < d4; c++) {
+                float4 x[4], y[4];
+#pragma unroll
+                for (int a = 0; a < 4; a++) x[a] = *reinterpret_cast<const float4 *>(qrow + a * 32 * stride + 4 * c);
+#pragma unroll
+                for (int b = 0; b < 4; b++) y[b] = *reinterpret_cast<const float4 *>(erow + b * stride + 4 * c);
+#pragma unroll
+                for (int a = 0; a < 4; a++)
+#pragma unroll
+                    for (int b = 0; b < 4; b++) {
+                        const float d0 = x[a].x - y[b].x, d1 = x[a].y - y[b].y;
+                        const float d2 = x[a].z - y[b].z, d3 = x[a].w - y[b].w;
+                        if (MET == kMetricL1)
+                            acc[a][b] += (fabsf(d0) + fabsf(d1)) + (fabsf(d2) + fabsf(d3));
+                        else
+                            acc[a][b] += (d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3);
+                    }
+            }
+#pragma unroll
+            for (int a = 0; a < 4; a++) {
+                const int row = lane + 32 * a;
+                const int q = s_q[row];
+                if (q < 0) continue;
+                const float dqp = s_dqp[row];
+                const float r = s_r[row];
+                const float rrow = lemma1_rrow(ix, dqp, r);
+                bool any_ub = false;
+#pragma unroll
+                for (int b = 0; b < 4; b++) {
+                    const int j = e0 + b;
+                    if (j >= size) continue;
+                    const float dis = s_dis[j];
+                    if (!(dis == dis)) continue;   // tombstoned
+                    if (pruning && !lemma1_pass(ix, dis, dqp, rrow)) continue;
+                    ver[a]++;
+                    const float d = MET == kMetricL1 ? acc[a][b] : sqrtf(acc[a][b]);
+                    const float sl = slack(ix, d, 0.f);
+                    if (!(d - sl <= r)) continue;
+                    // candidate: exact float64 check later (k_recheck) against the final radius
+                    const unsigned long long o = atomicAdd(cb.counter, 1ull);
+                    if (o < cb.cap) {
+                        const float lb = fmaxf(d - sl, 0.f) * (1.f - 1e-6f);
+                        cb.q[o] = q;
+                        cb.e[o] = pos + j;
+                        cb.lb[o] = MET == kMetricL2 ? lb * lb : lb;
+                    }
+                    if (fhist && d + sl <= r) {
+                        // the true distance is <= d + slack: a valid upper bound for the shrink
+                        fhist_add(fhist, r0, q, (double)(d + sl) * (1.0 + 1e-6));
+                        any_ub = true;
+                    }
+                }
+                if (any_ub) {
+                    // shrink once per tile row; later tiles of this block see it via s_r
+                    __threadfence();
+                    fhist_shrink(fhist, r0, ks, r32, r64, q);
+                    atomicMin(reinterpret_cast<int *>(s_r + row), __float_as_int(__ldcg(r32 + q)));
+                }
+            }
+        }
+#pragma unroll
+        for (int a = 0; a < 4; a++)
+            if (ver[a]) atomicAdd(s_ver + lane + 32 * a, ver[a]);
+        __syncthreads();
+        if (threadIdx.x < 128) {
+            const int q = s_q[threadIdx.x];
+            const unsigned v = q >= 0 ? s_ver[threadIdx.x] : 0u;
+            if (stats_on && v) atomicAdd(verified_stat + q, (unsigned long long)v);
+            if (work) {
+                // one work-counter atomic per warp (a per-row atomic on one
+                // address serialises the profiling pass)
+                const unsigned wsum = __reduce_add_sync(kFull, v);
+                if (lane == 0 && wsum) atomicAdd(work + kWorkPairs, (unsigned long long)wsum);
+            }
+        }
+        if (threadIdx.x == 0) {
+            w_entries += (unsigned long long)size * item.count;
+            w_rows += (unsigned long long)item.count;
+        }
+    }
+    if (work && threadIdx.x == 0) {
+        atomicAdd(work + kWorkEntries, w_entries);
+        atomicAdd(work + kWorkRows, w_rows);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Tensor-core verification for dense L2 (north_star: "norm-expansion MMA with
 // an exact recheck").  One work item = (leaf, up to 128 queries): a
 // kind::f16 (bf16 in, fp32 accumulate) tcgen05 MMA of M=128 queries x
@@ -1329,12 +1506,6 @@ __global__ void __launch_bounds__(kMmaThreads, 3) k_leafgroup_mma(IndexView ix, 
 // ---------------------------------------------------------------------------
 constexpr int kM2Threads = 512;   // 16 warps: 4 per TMEM lane quadrant
 
-struct CandBuf {
-    int32_t *q, *e;
-    float *lb;                 // lower bound of d^2 (approximate d^2 - error band)
-    unsigned long long cap;
-    unsigned long long *counter;
-};
 
 __global__ void __launch_bounds__(kM2Threads, 1)
 k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, const Item *__restrict__ items, int nitems,
@@ -1495,7 +1666,7 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
         mma(0);
     }
     uint32_t phase[2] = {0u, 0u};
-    unsigned long long pairs = 0;
+    unsigned long long pairs = 0, w_entries = 0, w_rows = 0, w_macs = 0;
     for (int i = 0; idx(i) < nitems; i++) {
         const int s = i & 1;
         const bool has1 = idx(i + 1) < nitems;
@@ -1615,10 +1786,10 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
             }
             if (valid && stats_on && ver) atomicAdd(verified_stat + q, (unsigned long long)ver);
             pairs += ver;
-            if (work && tid == 0) {
-                atomicAdd(work + kWorkEntries, (unsigned long long)size * d.z);
-                atomicAdd(work + kWorkRows, (unsigned long long)d.z);
-                atomicAdd(work + kWorkSteps, (unsigned long long)128 * N * ix.Dk);   // MMA MACs issued
+            if (tid == 0) {
+                w_entries += (unsigned long long)size * d.z;
+                w_rows += (unsigned long long)d.z;
+                w_macs += (unsigned long long)128 * N * ix.Dk;   // MMA MACs issued
             }
         }
         // metadata of item i+2 and the descriptor of item i+3 (loads done by now)
@@ -1636,6 +1807,11 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
     if (work) {
         for (int o = 16; o > 0; o >>= 1) pairs += __shfl_down_sync(kFull, pairs, o);
         if (lane == 0) atomicAdd(work + kWorkPairs, pairs);
+        if (tid == 0) {
+            atomicAdd(work + kWorkEntries, w_entries);
+            atomicAdd(work + kWorkRows, w_rows);
+            atomicAdd(work + kWorkSteps, w_macs);
+        }
     }
     tc::fence_before_sync();
     __syncthreads();
@@ -1643,37 +1819,42 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
     if (warp == 0) tc::tmem_dealloc(tmem, 2 * acc_cols);
 }
 
-// Exact float64 recheck of the tensor-core candidates against the final
-// radius (kNN radii only ever shrink, so the candidates are a superset).
-// Candidates whose d^2 lower bound is already outside the final radius are
-// dropped first.  8 lanes per candidate: lane j accumulates numpy's pairwise
-// partial r[j] = sum over i = j (mod 8) in order, then the lanes combine
-// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) and add the D % 8 tail sequentially --
-// the same float64 operations as pw_sum64 for D <= 128 (metrics.py:127-133).
-__global__ void k_recheck_l2(IndexView ix, QueryView qv, CandBuf cb, unsigned long long ncand, const float *r32,
-                             const double *r64, HitBuf out)
+// Exact float64 recheck of screened candidates against the final radius
+// (kNN radii only ever shrink, so the candidates are a superset).
+// Candidates whose lower bound (d^2 for L2, d for L1) is already outside the
+// final radius are dropped first.  8 lanes per candidate: lane j accumulates
+// numpy's pairwise partial r[j] = sum over i = j (mod 8) in order, then the
+// lanes combine ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) and add the D % 8 tail
+// sequentially -- the same float64 operations as pw_sum64 for D <= 128
+// (metrics.py:127-133); larger D runs pw_sum64 on the group's first lane.
+template <int MET>
+__global__ void k_recheck(IndexView ix, QueryView qv, CandBuf cb, unsigned long long ncand, const float *r32,
+                          const double *r64, HitBuf out)
 {
-    const int lane = lane_id(), sub = lane >> 3, j = lane & 7;
+    const int lane = lane_id(), j = lane & 7;
     const unsigned long long i = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
     bool live = false;
     int q = 0, e = 0;
     if (i < ncand) {
         q = cb.q[i];
         const float r = __ldcg(r32 + q);
-        live = !(cb.lb[i] > r * r * (1.f + 1e-6f));
+        const float lim = MET == kMetricL2 ? r * r * (1.f + 1e-6f) : r * (1.f + 1e-6f);
+        live = !(cb.lb[i] > lim);
         e = cb.e[i];
     }
     double d64 = 0.0;
-    if (__any_sync(kFull, live)) {
-        const int D = ix.D;
+    const int D = ix.D;
+    if (D > 128) {
+        if (live && j == 0) d64 = vdist64<MET>(ix, qv, q, e);
+    } else if (__any_sync(kFull, live)) {
         const float *o32 = ix.vec64 ? nullptr : ix.vec32 + (size_t)e * ix.Dp;
         const double *o64 = ix.vec64 ? ix.vec64 + (size_t)e * D : nullptr;
         const double *qq = qv.vec64 + (size_t)q * D;
-        const int nb = D - D % 8;
+        const int nb = D < 8 ? 0 : D - D % 8;
         double acc = 0.0;
         if (live && j < nb) {
-            acc = term64<kMetricL2>(o64 ? o64[j] : (double)o32[j], qq[j]);
-            for (int t = j + 8; t < nb; t += 8) acc = __dadd_rn(acc, term64<kMetricL2>(o64 ? o64[t] : (double)o32[t], qq[t]));
+            acc = term64<MET>(o64 ? o64[j] : (double)o32[j], qq[j]);
+            for (int t = j + 8; t < nb; t += 8) acc = __dadd_rn(acc, term64<MET>(o64 ? o64[t] : (double)o32[t], qq[t]));
         }
         // combine within the 8-lane group in numpy's order
         const double a1 = __shfl_xor_sync(kFull, acc, 1);
@@ -1683,12 +1864,14 @@ __global__ void k_recheck_l2(IndexView ix, QueryView qv, CandBuf cb, unsigned lo
         const double a4 = __shfl_xor_sync(kFull, p4, 4);
         double res = (j & 4) ? __dadd_rn(a4, p4) : __dadd_rn(p4, a4);
         if (live && j == 0) {
-            if (nb == 0) res = 0.0;
-            for (int t = nb; t < D; t++) {
-                const double v = term64<kMetricL2>(o64 ? o64[t] : (double)o32[t], qq[t]);
-                res = (t == 0) ? v : __dadd_rn(res, v);
+            if (nb == 0) {
+                // n < 8: numpy sums sequentially from 0.0
+                res = 0.0;
+                for (int t = 0; t < D; t++) res = __dadd_rn(res, term64<MET>(o64 ? o64[t] : (double)o32[t], qq[t]));
+            } else {
+                for (int t = nb; t < D; t++) res = __dadd_rn(res, term64<MET>(o64 ? o64[t] : (double)o32[t], qq[t]));
             }
-            d64 = __dsqrt_rn(res);
+            d64 = MET == kMetricL1 ? res : __dsqrt_rn(res);
         }
     }
     const bool hit = live && j == 0 && d64 <= __ldcg(r64 + q);
@@ -1701,7 +1884,6 @@ __global__ void k_recheck_l2(IndexView ix, QueryView qv, CandBuf cb, unsigned lo
         const unsigned long long o = base + __popc(hb & ((1u << lane) - 1u));
         if (o < out.cap) { out.q[o] = q; out.e[o] = e; out.d[o] = d64; }
     }
-    (void)sub;
 }
 
 struct CacheView {
@@ -2442,32 +2624,48 @@ struct Search {
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
         const unsigned grid = (unsigned)std::min<int>(nitems, sms);   // items i, i + grid, ... per CTA
+        DBuf<unsigned long long> cur(1, st);
+        with_candidates<kMetricL2>([&](const CandBuf &cb, int first) {
+            CK(cudaMemsetAsync(cur.p, 0, sizeof(unsigned long long), st));
+            timed("k_leafgroup_mma2", [&] {
+                const int on = first && stats_on;
+                k_leafgroup_mma2<<<grid, kM2Threads, smb, st>>>(iv, qv, srows, items, nitems, cur.p, r32.p, r64.p, cb,
+                                                             verified.p, on, on ? work.p : nullptr, cols, nmax,
+                                                             on ? fhist.p : nullptr, r0.p, ks.p);
+            });
+            LAUNCH_CHECK();
+        });
+    }
+
+    // Run a screening kernel that appends (query, entry, lower bound) candidates,
+    // growing the buffer and re-running (stats off: counts and histograms must
+    // not double) on overflow, then recheck them exactly (k_recheck<MET>).
+    template <int MET, class Launch>
+    void with_candidates(Launch &&launch)
+    {
         size_t cap = std::max<size_t>((size_t)1 << 22, (size_t)ix->cand_hint.load());
-        DBuf<unsigned long long> cnt(2, st);   // [0] item cursor, [1] candidates
+        DBuf<unsigned long long> cnt(1, st);
         for (int attempt = 0;; attempt++) {
             if (cq.n < cap) {
                 cq.alloc(cap, st);
                 ce.alloc(cap, st);
                 clb.alloc(cap, st);
             }
-            CK(cudaMemsetAsync(cnt.p, 0, 2 * sizeof(unsigned long long), st));
-            CandBuf cb{cq.p, ce.p, clb.p, (unsigned long long)cq.n, cnt.p + 1};
-            const int first = attempt == 0 ? stats_on : 0;   // a re-run must not count twice
-            timed("k_leafgroup_mma2", [&] {
-                k_leafgroup_mma2<<<grid, kM2Threads, smb, st>>>(iv, qv, srows, items, nitems, cnt.p, r32.p, r64.p, cb,
-                                                             verified.p, first, first ? work.p : nullptr, cols,
-                                                             nmax, first ? fhist.p : nullptr, r0.p, ks.p);
-            });
-            LAUNCH_CHECK();
-            CK(cudaMemcpyAsync(h_counter + 2, cnt.p + 1, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+            CK(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), st));
+            CandBuf cb{cq.p, ce.p, clb.p, (unsigned long long)cq.n, cnt.p};
+            launch(cb, attempt == 0 ? 1 : 0);
+            CK(cudaMemcpyAsync(h_counter + 2, cnt.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
             const unsigned long long nc = h_counter[2];
-            ix->cand_hint = std::max<unsigned long long>(ix->cand_hint.load(), nc);
+            {
+                unsigned long long c0 = ix->cand_hint.load();
+                while (nc > c0 && !ix->cand_hint.compare_exchange_weak(c0, nc)) {}
+            }
             if (nc > cq.n) { cap = (size_t)nc + nc / 4; continue; }
             if (nc) {
                 HitBuf hb{hq.p, he.p, hd.p, (unsigned long long)hq.n, counter.p + 1};
-                timed("k_recheck_l2", [&] {
-                    k_recheck_l2<<<grid_for((int64_t)nc * 8, 256), 256, 0, st>>>(iv, qv, cb, nc, r32.p, r64.p, hb);
+                timed("k_recheck", [&] {
+                    k_recheck<MET><<<grid_for((int64_t)nc * 8, 256), 256, 0, st>>>(iv, qv, cb, nc, r32.p, r64.p, hb);
                 });
                 LAUNCH_CHECK();
             }
@@ -2513,6 +2711,33 @@ struct Search {
             });
             LAUNCH_CHECK();
             return;
+        }
+        {
+            // register-tiled kernel when the leaf + 128 query rows fit
+            const size_t tsm = ((size_t)ix->max_leaf * (ix->Dp + 4) + (size_t)128 * (ix->Dp + 4) + ix->max_leaf +
+                                6 * 128) * sizeof(float);
+            if (tsm <= 200 * 1024 && std::getenv("GTS_VEC_ROWWARP") == nullptr) {
+                static bool tattr[3] = {false, false, false};
+                if (!tattr[MET]) {
+                    CK(cudaFuncSetAttribute(k_leafgroup_tile<MET>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            200 * 1024));
+                    tattr[MET] = true;
+                }
+                int per = 0;
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_leafgroup_tile<MET>, 256, tsm));
+                const unsigned tgrid = (unsigned)std::min<int64_t>(nitems, (int64_t)148 * std::max(per, 1));
+                with_candidates<MET>([&](const CandBuf &cb, int first) {
+                    const int on = first && stats_on;
+                    timed("k_leafgroup_tile", [&] {
+                        k_leafgroup_tile<MET><<<tgrid, 256, tsm, st>>>(iv, qv, srows.p, items.p, nitems, pruning,
+                                                                      r32.p, r64.p, cb, verified.p, on,
+                                                                      on ? work.p : nullptr, on ? fhist.p : nullptr,
+                                                                      r0.p, ks.p);
+                    });
+                    LAUNCH_CHECK();
+                });
+                return;
+            }
         }
         static bool attr_set[3] = {false, false, false};
         if (!attr_set[MET]) {
