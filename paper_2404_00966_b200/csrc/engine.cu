@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(256, 4) k_leaf_edit(IndexView ix, QueryView qv
                                                       int64_t m, int pruning, float *r32,
                                                       HitBuf out, unsigned long long *verified_stat, int stats_on,
                                                       unsigned long long *work, unsigned long long *cursor,
-                                                      unsigned *hist, const int32_t *__restrict__ ks)
+                                                      unsigned *hist, const int32_t *__restrict__ ks, int claim)
 {
     __shared__ uint32_t peq_s[kLeafWarps][kWarpPeqWords];
     __shared__ int32_t queue[kLeafWarps][3][64];   // entry, first text word, length
@@ -416,12 +416,17 @@ __global__ void __launch_bounds__(256, 4) k_leaf_edit(IndexView ix, QueryView qv
         __syncwarp();
     };
 
+    // a warp claims `claim` consecutive rows (rows are in query order): with
+    // a large claim one warp walks most of a query's leaves in sequence, so
+    // the kNN radius shrunk by its own early hits filters the later leaves
     for (;;) {
-        unsigned long long start = 0;
-        if (lane == 0) start = atomicAdd(cursor, (unsigned long long)kRowChunk);
-        start = __shfl_sync(kFull, start, 0);
-        if ((int64_t)start >= m) break;
-        const int64_t stop = min(m, (int64_t)start + kRowChunk);
+        unsigned long long cstart = 0;
+        if (lane == 0) cstart = atomicAdd(cursor, (unsigned long long)claim);
+        cstart = __shfl_sync(kFull, cstart, 0);
+        if ((int64_t)cstart >= m) break;
+        const int64_t cstop = min(m, (int64_t)cstart + claim);
+    for (int64_t start = (int64_t)cstart; start < cstop; start += kRowChunk) {
+        const int64_t stop = min(cstop, start + kRowChunk);
         nrows += (unsigned long long)(stop - (int64_t)start);
         // lanes fetch the chunk's row and leaf records in one parallel batch
         Row pr{0, 0, 0.f, 0};
@@ -499,6 +504,7 @@ __global__ void __launch_bounds__(256, 4) k_leaf_edit(IndexView ix, QueryView qv
         if (lane == 0 && stats_on && ver) atomicAdd(verified_stat + lr.q, (unsigned long long)ver);
         pairs += ver;
         entries += leaf.size;
+    }
     }
     }
     if (qn) run_batch(qn);
@@ -1497,7 +1503,7 @@ __global__ void __launch_bounds__(kMmaThreads, 3) k_leafgroup_mma(IndexView ix, 
 //  * two smem stages and two TMEM accumulators: item i+1's operands are in
 //    flight (cp.async) while item i's epilogue runs.
 //  * the epilogue only screens; pairs whose approximate d^2 is within the
-//    error band of r^2 go to a candidate list, and k_recheck_l2 recomputes
+//    error band of r^2 go to a candidate list, and k_recheck recomputes
 //    them exactly in float64 (numpy order) against the FINAL radius, so no
 //    thread of an item stalls the block on a float64 recompute.
 //  * kNN: candidates whose d^2 UPPER bound is inside the radius feed the
@@ -2608,7 +2614,7 @@ struct Search {
     }
 
     // tensor-core screen (k_leafgroup_mma2) + exact float64 recheck of the
-    // candidate pairs (k_recheck_l2)
+    // candidate pairs (k_recheck)
     void launch_mma2(const Row *srows, const Item *items, int nitems, int stats_on)
     {
         const int nmax = std::max(16, (ix->max_leaf + 15) & ~15);
@@ -2813,13 +2819,19 @@ struct Search {
             }
             HitBuf hb{hq.p, he.p, hd.p, (unsigned long long)hq.n, counter.p + 1};
             // one warp per ~contiguous run of rows; enough warps to fill the GPU
+            // rows per cursor claim: 16 (GTS_EDIT_CLAIM overrides).  Larger kNN
+            // claims (one warp walking a query's leaves in order) did not cut
+            // the DP work -- the probe radius is already near the final one --
+            // and cost balance (words: 88.7 vs 83.6 ms)
+            static const int env_claim = std::getenv("GTS_EDIT_CLAIM") ? std::atoi(std::getenv("GTS_EDIT_CLAIM")) : 0;
+            const int claim = env_claim > 0 ? std::max(kRowChunk, env_claim) : kRowChunk;
             unsigned grid = grid_for((m + kRowChunk - 1) / kRowChunk, kLeafWarps, 148u * 4u);   // 4 resident per SM
             CK(cudaMemsetAsync(counter.p, 0, sizeof(unsigned long long), st));
             timed("k_leaf_edit", [&] {
                 k_leaf_edit<<<grid, 32 * kLeafWarps, 0, st>>>(iv, qv, rows, m, pruning, r32.p, hb, verified.p,
                                                              stats_on, stats_on ? work.p : nullptr, counter.p,
                                                              // a re-run (stats_on == 0) must not count twice
-                                                             stats_on ? hist.p : nullptr, ks.p);
+                                                             stats_on ? hist.p : nullptr, ks.p, claim);
             });
             LAUNCH_CHECK();
             break;
