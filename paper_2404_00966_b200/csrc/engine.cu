@@ -2649,7 +2649,11 @@ struct Search {
     template <int MET, class Launch>
     void with_candidates(Launch &&launch)
     {
-        size_t cap = std::max<size_t>((size_t)1 << 22, (size_t)ix->cand_hint.load());
+        // the hint is the largest count seen; 50% headroom, since kNN counts vary
+        // from call to call (the shrinking radius is order-dependent) and an
+        // overflow costs a full re-run of the screening kernel
+        const size_t hint = (size_t)ix->cand_hint.load();
+        size_t cap = std::max<size_t>((size_t)1 << 22, hint + hint / 2);
         DBuf<unsigned long long> cnt(1, st);
         for (int attempt = 0;; attempt++) {
             if (cq.n < cap) {
@@ -2667,7 +2671,7 @@ struct Search {
                 unsigned long long c0 = ix->cand_hint.load();
                 while (nc > c0 && !ix->cand_hint.compare_exchange_weak(c0, nc)) {}
             }
-            if (nc > cq.n) { cap = (size_t)nc + nc / 4; continue; }
+            if (nc > cq.n) { cap = (size_t)nc + nc / 2; reruns++; continue; }
             if (nc) {
                 HitBuf hb{hq.p, he.p, hd.p, (unsigned long long)hq.n, counter.p + 1};
                 timed("k_recheck", [&] {
@@ -2678,6 +2682,7 @@ struct Search {
             return;
         }
     }
+    int reruns = 0;         // screening launches re-run after a buffer overflow (trace)
     DBuf<int32_t> cq, ce;   // tensor-core candidate pairs
     DBuf<float> clb;        // their d^2 lower bounds
 
@@ -2781,6 +2786,7 @@ struct Search {
         dispatch_verify(rows, m, 1);
         unsigned long long after = read_counter(1);
         if (after > hq.n) {
+            reruns++;
             // grow the hit buffer and redo this launch (stats already counted)
             size_t ncap = (size_t)std::max<unsigned long long>(after * 2, hq.n * 2);
             DBuf<int32_t> nq_(ncap, st), ne_(ncap, st);
@@ -3266,8 +3272,9 @@ gts_result *run_search(gts_index *ix, const gts_queries *q, int mode, const doub
     }
     if (trace) {
         const double t3 = now_ms();
-        fprintf(stderr, "[gts] %s nq=%lld setup=%.2fms run=%.2fms collect=%.2fms hits=%llu\n", mode ? "knn" : "range",
-                (long long)nq, t1 - t0, t2 - t1, t3 - t2, (unsigned long long)s.hits);
+        fprintf(stderr, "[gts] %s nq=%lld setup=%.2fms run=%.2fms collect=%.2fms hits=%llu reruns=%d\n",
+                mode ? "knn" : "range", (long long)nq, t1 - t0, t2 - t1, t3 - t2, (unsigned long long)s.hits,
+                s.reruns);
         if (g_phase_dev) {
             unsigned long long ph[3];
             cudaMemcpy(ph, g_phase_dev, sizeof(ph), cudaMemcpyDeviceToHost);
@@ -3417,6 +3424,25 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
         if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
             uint64_t thr = UINT64_MAX;
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            // Prime the pool once: map a large block up front so batch-sized
+            // scratch (frontier tables, hit / candidate buffers, sort space:
+            // GBs for 100k-query kNN) is carved from mapped memory instead of
+            // growing the pool -- mapping new physical memory mid-call costs
+            // 100s of ms.  GTS_POOL_PRIME_GB overrides (0 = off).
+            const char *env = std::getenv("GTS_POOL_PRIME_GB");
+            size_t free_b = 0, total_b = 0;
+            cudaMemGetInfo(&free_b, &total_b);
+            size_t want = env ? (size_t)std::atoll(env) << 30 : std::min<size_t>((size_t)24 << 30, total_b / 6);
+            uint64_t reserved = 0;
+            cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+            if (want > reserved && want < free_b / 2) {
+                void *p = nullptr;
+                if (cudaMallocAsync(&p, want, 0) == cudaSuccess) {
+                    cudaFreeAsync(p, 0);
+                    cudaStreamSynchronize(0);
+                }
+                cudaGetLastError();
+            }
         }
     }
     if (!ds || !t || !out) fail(GTS_EINVAL, "null argument");
