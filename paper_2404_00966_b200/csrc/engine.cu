@@ -331,8 +331,10 @@ __global__ void __launch_bounds__(256, 4) k_leaf_edit(IndexView ix, QueryView qv
                                                       int64_t m, int pruning, float *r32,
                                                       HitBuf out, unsigned long long *verified_stat, int stats_on,
                                                       unsigned long long *work, unsigned long long *cursor,
-                                                      unsigned *hist, const int32_t *__restrict__ ks, int claim)
+                                                      unsigned *hist, const int32_t *__restrict__ ks, int claim,
+                                                      int tstride)
 {
+    extern __shared__ uint32_t le_text[];   // [kLeafWarps][32][tstride] when tstride > 0
     __shared__ uint32_t peq_s[kLeafWarps][kWarpPeqWords];
     __shared__ int32_t queue[kLeafWarps][3][64];   // entry, first text word, length
     const int lane = lane_id(), wib = threadIdx.x >> 5;
@@ -358,6 +360,9 @@ __global__ void __launch_bounds__(256, 4) k_leaf_edit(IndexView ix, QueryView qv
         unsigned *hq_ = hist + (size_t)cur_q * kHistBins;
         if (ha && dA < kHistBins) atomicAdd(hq_ + dA, 1u);
         if (hb2 && dB < kHistBins) atomicAdd(hq_ + dB, 1u);
+        // the k-th bound can only drop below r through a hit strictly below r
+        // (hits at d == r, the common case once r has converged, leave it)
+        if (!__any_sync(kFull, (ha && (float)dA < r) || (hb2 && (float)dB < r))) return;
         __syncwarp();
         __threadfence_block();
         // warp prefix over the 256 bins (8 per lane) -> smallest t with count(d <= t) >= k
@@ -403,12 +408,31 @@ __global__ void __launch_bounds__(256, 4) k_leaf_edit(IndexView ix, QueryView qv
     auto run_batch = [&](int cnt) {
         const bool va = lane < cnt;
         int ea = -1, da = 0;
-        if (va) {
+        const int wq = (mq + 31) >> 5;
+        if (tstride && staged && wq <= 2 && mq > 0) {
+            // stage each lane's text in shared memory (odd word stride: the
+            // per-symbol byte loads of 32 lanes hit distinct banks), then run
+            // the DP with LDS.U8 symbols -- no ALU-pipe symbol extraction
+            uint32_t *tx = le_text + (size_t)wib * kWarp * tstride + (size_t)lane * tstride;
+            int na = 0;
+            if (va) {
+                ea = qu[lane];
+                na = ql[lane];
+                const uint32_t *tA = ix.str + (uint32_t)qw[lane];
+                for (int w = 0; w < ((na + 3) >> 2); w++) tx[w] = __ldg(tA + w);
+            }
+            __syncwarp();
+            if (va) {
+                const uint8_t *t1 = reinterpret_cast<const uint8_t *>(tx);
+                da = na == 0 ? mq : (wq == 1 ? myers_smem_aw<1>(peq_w, mq, t1, na) : myers_smem_aw<2>(peq_w, mq, t1, na));
+                steps += (unsigned long long)wq * (unsigned long long)na;
+            }
+        } else if (va) {
             ea = qu[lane];
             const int na = ql[lane];
             const uint32_t *tA = ix.str + (uint32_t)qw[lane];
             da = staged ? edit_peq(peq_w, mq, tA, na) : edit_peq_global(peq_g, mq, tA, na);
-            steps += (unsigned long long)((mq + 31) >> 5) * (unsigned long long)na;
+            steps += (unsigned long long)wq * (unsigned long long)na;
         }
         const bool ha = va && (float)da <= r;
         emit(ha, ea, da);
@@ -953,7 +977,6 @@ __global__ void __launch_bounds__(256) k_expand_grouped(IndexView ix, QueryView 
     }
 }
 
-constexpr int kFHistBins = 64;
 __device__ __forceinline__ void fhist_add(unsigned *hist, const float *r0, int q, double d);
 __device__ __forceinline__ void fhist_shrink(unsigned *hist, const float *r0, const int32_t *ks, float *r32,
                                              double *r64, int q);
@@ -1241,12 +1264,12 @@ __global__ void __launch_bounds__(256) k_leafgroup_tile(IndexView ix, QueryView 
 // ~64 KB of shared memory per CTA: three CTAs per SM overlap each other's
 // staging, MMA and epilogue.
 // ---------------------------------------------------------------------------
-// kNN shrinking bound for float metrics: per-query 64-bin histogram of the
+// kNN shrinking bound for float metrics: per-query 256-bin histogram of the
 // exact distances found so far over [0, r0] (r0 = the probe radius).  The
 // upper edge of the bin where the count reaches k bounds the k-th distance
 // from above (k distinct real objects lie at or below it), so the radius can
 // only shrink to values that still admit every true answer and its ties.
-constexpr int kFHist = 64;
+constexpr int kFHist = 256;   // bins over [0, r0]: the final radius is one bin above the k-th distance
 
 __device__ __forceinline__ void fhist_add(unsigned *hist, const float *r0, int q, double d)
 {
@@ -2808,7 +2831,7 @@ struct Search {
     }
 
     DBuf<unsigned> hist;   // kNN edit: per-query distance histogram (shrinking bound)
-    DBuf<unsigned> fhist;  // kNN vectors: per-query 64-bin histogram over [0, r0]
+    DBuf<unsigned> fhist;  // kNN vectors: per-query 256-bin histogram over [0, r0]
     DBuf<float> r0;        // kNN vectors: the probe radius (histogram scale)
 
     void dispatch_verify(const Row *rows, int64_t m, int stats_on)
@@ -2832,12 +2855,18 @@ struct Search {
             static const int env_claim = std::getenv("GTS_EDIT_CLAIM") ? std::atoi(std::getenv("GTS_EDIT_CLAIM")) : 0;
             const int claim = env_claim > 0 ? std::max(kRowChunk, env_claim) : kRowChunk;
             unsigned grid = grid_for((m + kRowChunk - 1) / kRowChunk, kLeafWarps, 148u * 4u);   // 4 resident per SM
+            // texts staged in smem for the DP when strings are short (words);
+            // GTS_EDIT_SMEM_TEXT=0 disables
+            static const char *env_tx = std::getenv("GTS_EDIT_SMEM_TEXT");
+            int tstride = 0;
+            if (ix->max_len <= 64 && !(env_tx && env_tx[0] == '0')) tstride = (((ix->max_len + 3) >> 2) | 1);
+            const size_t dyn = (size_t)tstride * kWarp * kLeafWarps * sizeof(uint32_t);
             CK(cudaMemsetAsync(counter.p, 0, sizeof(unsigned long long), st));
             timed("k_leaf_edit", [&] {
-                k_leaf_edit<<<grid, 32 * kLeafWarps, 0, st>>>(iv, qv, rows, m, pruning, r32.p, hb, verified.p,
-                                                             stats_on, stats_on ? work.p : nullptr, counter.p,
-                                                             // a re-run (stats_on == 0) must not count twice
-                                                             stats_on ? hist.p : nullptr, ks.p, claim);
+                k_leaf_edit<<<grid, 32 * kLeafWarps, dyn, st>>>(iv, qv, rows, m, pruning, r32.p, hb, verified.p,
+                                                               stats_on, stats_on ? work.p : nullptr, counter.p,
+                                                               // a re-run (stats_on == 0) must not count twice
+                                                               stats_on ? hist.p : nullptr, ks.p, claim, tstride);
             });
             LAUNCH_CHECK();
             break;

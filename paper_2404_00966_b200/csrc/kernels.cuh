@@ -261,6 +261,45 @@ __device__ __forceinline__ int myers_smem(const uint32_t *peq, int m, const uint
     return score;
 }
 
+// Text in shared memory (one byte per symbol, LDS.U8), masks in the
+// per-query [A][W] layout of the row-wise kernel (block b of symbol c at
+// peq[c * W + b]); the address is an IMAD through kTwo.
+template <int W>
+__device__ __forceinline__ int myers_smem_aw(const uint32_t *peq, int m, const uint8_t *t, int n)
+{
+    uint32_t P[W], M[W];
+#pragma unroll
+    for (int b = 0; b < W; b++) { P[b] = ~0u; M[b] = 0u; }
+    const uint32_t scale = kTwo * kTwo * W;
+    auto step = [&](uint32_t c) {
+        const uint32_t *pe = reinterpret_cast<const uint32_t *>(reinterpret_cast<const char *>(peq) + c * scale);
+        if (W == 1) {
+            myers_step1(pe[0], P[0], M[0]);
+        } else {
+            uint32_t hp = 1u, hm = 0u;
+#pragma unroll
+            for (int b = 0; b < W; b++) myers_stepb(pe[b], P[b], M[b], hp, hm);
+        }
+    };
+    int j = 0;
+    for (; j + 4 <= n; j += 4) {
+        const uint32_t c0 = t[j], c1 = t[j + 1], c2 = t[j + 2], c3 = t[j + 3];
+        step(c0);
+        step(c1);
+        step(c2);
+        step(c3);
+    }
+    for (; j < n; j++) step(t[j]);
+    const uint32_t lastmask = (m & 31) ? ((1u << (m & 31)) - 1u) : ~0u;
+    int score = n;
+#pragma unroll
+    for (int b = 0; b < W; b++) {
+        const uint32_t mk = (b == W - 1) ? lastmask : ~0u;
+        score += __popc(P[b] & mk) - __popc(M[b] & mk);
+    }
+    return score;
+}
+
 __device__ __noinline__ int myers_generic(const uint32_t *peq, int W, int m, const uint32_t *__restrict__ t4, int n)
 {
     uint32_t P[kMaxWords], M[kMaxWords];

@@ -23,7 +23,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
 
 METRICS = [
-    ("gpu__time_duration.sum", "duration (us)"),
+    ("gpu__time_duration.sum", "duration"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput % of peak"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue slots active %"),
     ("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "ALU pipe %"),
@@ -71,11 +71,12 @@ def full_capture(path):
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(io.StringIO(raw)))
     h, v = r[0], r[2] if len(r) > 2 else r[1]
+    units = r[1] if len(r) > 2 else [""] * len(h)
     name = v[h.index("Kernel Name")] if "Kernel Name" in h else "?"
-    lines = [f"kernel: `{name[:120]}`", "", "| metric | value |", "|---|---:|"]
+    lines = [f"kernel: `{name[:120]}`", "", "| metric | value | unit |", "|---|---:|---|"]
     for m, label in METRICS:
         if m in h:
-            lines.append(f"| {label} (`{m}`) | {v[h.index(m)]} |")
+            lines.append(f"| {label} (`{m}`) | {v[h.index(m)]} | {units[h.index(m)]} |")
     st = [(x, float(v[h.index(x)])) for x in h
           if x.startswith("smsp__average_warps_issue_stalled") and x.endswith("per_issue_active.ratio")]
     lines += ["", "top stall reasons (warps stalled per issued instruction):", "",
