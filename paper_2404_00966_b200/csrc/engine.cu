@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(256) k_verify(IndexView ix, QueryView qv, cons
                 if (!pruning) pass = true;
                 else {
                     const float de = __ldg(ix.dis + e);
-                    pass = lemma1_pass(ix, de, lr.dqp, lemma1_rrow(ix, lr.dqp, r));
+                    pass = lemma1_in(de, lemma1_range(ix, lr.dqp, r));
                 }
             }
             ver += __popc(__ballot_sync(kFull, pass));
@@ -1026,7 +1026,7 @@ __global__ void __launch_bounds__(256) k_leafgroup_vec(IndexView ix, QueryView q
                     if (!pruning) pass = true;
                     else {
                         const float de = __ldg(ix.dis + e);
-                        pass = lemma1_pass(ix, de, lr.dqp, lemma1_rrow(ix, lr.dqp, r));
+                        pass = lemma1_in(de, lemma1_range(ix, lr.dqp, r));
                     }
                 }
                 ver += __popc(__ballot_sync(kFull, pass));
@@ -1093,7 +1093,7 @@ struct CandBuf {
 };
 
 template <int MET>
-__global__ void __launch_bounds__(256) k_leafgroup_tile(IndexView ix, QueryView qv, const Row *__restrict__ srows,
+__global__ void __launch_bounds__(256, 3) k_leafgroup_tile(IndexView ix, QueryView qv, const Row *__restrict__ srows,
                                                         const Item *__restrict__ items, int nitems, int pruning,
                                                         float *r32, double *r64, CandBuf cb,
                                                         unsigned long long *verified_stat, int stats_on,
@@ -1105,11 +1105,11 @@ __global__ void __launch_bounds__(256) k_leafgroup_tile(IndexView ix, QueryView 
     float *ent = reinterpret_cast<float *>(tile_smem4);                 // [max_leaf][stride]
     float *qs = ent + (size_t)ix.max_leaf * stride;                       // [128][stride]
     float *s_dis = qs + (size_t)128 * stride;                             // [max_leaf] (NaN: tombstoned)
-    float *s_dqp = s_dis + ix.max_leaf;                                   // [128]
-    float *s_r = s_dqp + 128;                                             // [128]
+    float *s_lo = s_dis + ix.max_leaf;                                    // [128] lemma-1 window, per row
+    float *s_r = s_lo + 128;                                              // [128]
     int *s_q = reinterpret_cast<int *>(s_r + 128);                        // [128]
     unsigned *s_ver = reinterpret_cast<unsigned *>(s_q + 128);            // [128]
-    unsigned *s_nh = s_ver + 128;                                         // [128]
+    float *s_hi = reinterpret_cast<float *>(s_ver + 128);                 // [128]
     const int lane = lane_id(), warp = threadIdx.x >> 5;
     const int d4 = ix.Dp >> 2;
     unsigned long long w_entries = 0, w_rows = 0;
@@ -1128,11 +1128,14 @@ __global__ void __launch_bounds__(256) k_leafgroup_tile(IndexView ix, QueryView 
                 dqp = lr.dqp;
                 r = __ldcg(r32 + q);
             }
+            // the window is fixed for the item (a kNN shrink narrows only the
+            // screen; the wider window is conservative)
+            const float2 rg = lemma1_range(ix, dqp, r);
             s_q[a] = q;
-            s_dqp[a] = dqp;
+            s_lo[a] = rg.x;
+            s_hi[a] = rg.y;
             s_r[a] = r;
             s_ver[a] = 0;
-            s_nh[a] = 0;
         }
         for (int j = threadIdx.x; j < size; j += blockDim.x) {
             const bool al = is_alive(ix.alive, pos + j);
@@ -1186,9 +1189,8 @@ __global__ void __launch_bounds__(256) k_leafgroup_tile(IndexView ix, QueryView 
                 const int row = lane + 32 * a;
                 const int q = s_q[row];
                 if (q < 0) continue;
-                const float dqp = s_dqp[row];
                 const float r = s_r[row];
-                const float rrow = lemma1_rrow(ix, dqp, r);
+                const float2 rg = make_float2(s_lo[row], s_hi[row]);
                 bool any_ub = false;
 #pragma unroll
                 for (int b = 0; b < 4; b++) {
@@ -1196,7 +1198,7 @@ __global__ void __launch_bounds__(256) k_leafgroup_tile(IndexView ix, QueryView 
                     if (j >= size) continue;
                     const float dis = s_dis[j];
                     if (!(dis == dis)) continue;   // tombstoned
-                    if (pruning && !lemma1_pass(ix, dis, dqp, rrow)) continue;
+                    if (pruning && !lemma1_in(dis, rg)) continue;
                     ver[a]++;
                     const float d = MET == kMetricL1 ? acc[a][b] : sqrtf(acc[a][b]);
                     const float sl = slack(ix, d, 0.f);
@@ -1264,12 +1266,12 @@ __global__ void __launch_bounds__(256) k_leafgroup_tile(IndexView ix, QueryView 
 // ~64 KB of shared memory per CTA: three CTAs per SM overlap each other's
 // staging, MMA and epilogue.
 // ---------------------------------------------------------------------------
-// kNN shrinking bound for float metrics: per-query 256-bin histogram of the
+// kNN shrinking bound for float metrics: per-query 64-bin histogram of the
 // exact distances found so far over [0, r0] (r0 = the probe radius).  The
 // upper edge of the bin where the count reaches k bounds the k-th distance
 // from above (k distinct real objects lie at or below it), so the radius can
 // only shrink to values that still admit every true answer and its ties.
-constexpr int kFHist = 256;   // bins over [0, r0]: the final radius is one bin above the k-th distance
+constexpr int kFHist = 64;   // bins over [0, r0] (256 bins: fewer hits but a 4x longer scan per shrink, 12% slower on 128-d)
 
 __device__ __forceinline__ void fhist_add(unsigned *hist, const float *r0, int q, double d)
 {
@@ -1464,7 +1466,7 @@ __global__ void __launch_bounds__(kMmaThreads, 3) k_leafgroup_mma(IndexView ix, 
                 const int j = c0 + jj;
                 if (j >= leaf.size || !s_al[j]) continue;
                 const float dis = s_dis[j];
-                if (!lemma1_pass(ix, dis, dqp, lemma1_rrow(ix, dqp, r))) continue;   // lemma 1
+                if (!lemma1_in(dis, lemma1_range(ix, dqp, r))) continue;   // lemma 1
                 ver++;
                 bool cand = inf_r;
                 if (!cand) {
@@ -1553,7 +1555,7 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
     __shared__ uint32_t tmem_slot;
     __shared__ int4 s_item[4];           // {leaf, start, count, size}, ring by i % 4
     __shared__ int s_pos[4];
-    __shared__ float4 s_col[3][256];     // ring by i % 3: {dis | NaN, y - z, y + z, dis}
+    __shared__ float4 s_col[3][256];     // ring by i % 3 (see meta_store)
     __shared__ int s_rq[3][128];         // query ids (-1: no row)
     __shared__ float4 s_rf[3][128];      // {dqp, r at load time (radii only shrink), |q|, probe radius}
     (void)item_cursor;
@@ -1625,11 +1627,16 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
             s_rf[sl][tid] = m.rf;
         }
         if (tid < N) {
-            float4 col = make_float4(__int_as_float(0x7fc00000), 0.f, 0.f, 0.f);   // padding: NaN fails
+            // {dis | NaN, y - z | NaN, y + z, dis}: NaN (tombstone / padding)
+            // fails the lemma-1 window and the screen
+            const float nan = __int_as_float(0x7fc00000);
+            float4 col = make_float4(nan, nan, 0.f, INFINITY);
             if (tid < d.w) {
                 const float y = fmaf(m.dis, m.dis, 2.f * m.se), z = 8.f * ix.rel * m.dis * m.dis;
-                if (m.al) col.x = m.dis;
-                col.y = y - z;
+                if (m.al) {
+                    col.x = m.dis;
+                    col.y = y - z;
+                }
                 col.z = y + z;
                 col.w = m.dis;
             }
@@ -1736,15 +1743,18 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
             const float dq2 = dqp * dqp;
             const float cA = ldexpf(dqp + qnorm, -7) + ldexpf(qnorm, -18) + 4.f * ix.abs_eps;
             const float kq = 8.f * ix.rel * dq2 + 4.f * ix.abs_eps * (dqp + ix.abs_eps);
-            float rrow, T1, T2;
+            float T1, T2;
             auto set_r = [&](float rr) {
                 const float R2 = rr * rr * (1.f + 1e-6f);
                 const float mg = ldexpf(dq2 + qnorm * qnorm + R2, -18);
-                rrow = lemma1_rrow(ix, dqp, rr);
                 T1 = R2 + kq - dq2 + mg;
                 T2 = R2 - kq - dq2 - mg;
             };
             set_r(r);   // loaded two items ago: stale radii are larger, i.e. conservative
+            // lemma-1 window for the item (a kNN shrink inside it narrows only
+            // the screen; the wider window counts a few more entries as
+            // verified, which float-metric stats allow)
+            const float2 rg = lemma1_range(ix, dqp, r);
             float hinv = 0.f;   // kNN histogram: bins per unit distance
             if (fhist && valid) {
                 const float R0 = rf.w;
@@ -1752,21 +1762,30 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
             }
             unsigned ver = 0;
             const uint32_t lane_base = tmem + s * acc_cols + ((uint32_t)((warp & 3) * 32) << 16);
+            const float4 *cols = s_col[sl];
             for (int c0 = 16 * part; c0 < N; c0 += 64) {
                 float acc[16];
                 tc::tmem_ld16(lane_base + (uint32_t)c0, acc);   // warp-collective
-                uint32_t cm = 0, fm = 0;
+                uint32_t win = 0, cm = 0;
 #pragma unroll
                 for (int jj = 0; jj < 16; jj++) {
-                    const float4 col = s_col[sl][c0 + jj];   // broadcast LDS.128
-                    const bool pass = lemma1_pass(ix, col.x, dqp, rrow);
+                    const float4 col = cols[c0 + jj];   // broadcast LDS.128
                     const float m2a = fmaf(-2.f, acc[jj], col.y);
-                    const float m2b = fmaf(-2.f, acc[jj], col.z);
-                    const bool cand = pass && fmaf(-cA, col.w, m2a) <= T1;
-                    ver += pass;
-                    cm |= (uint32_t)cand << jj;
-                    fm |= (uint32_t)(cand && fmaf(cA, col.w, m2b) <= T2) << jj;
+                    win |= (uint32_t)lemma1_in(col.x, rg) << jj;
+                    cm |= (uint32_t)(fmaf(-cA, col.w, m2a) <= T1) << jj;
                 }
+                ver += __popc(win);
+                uint32_t fm = 0;
+                if (hinv > 0.f && (cm & win)) {
+                    // kNN: candidates whose d^2 upper bound is inside the radius
+#pragma unroll
+                    for (int jj = 0; jj < 16; jj++) {
+                        const float4 col = cols[c0 + jj];
+                        fm |= (uint32_t)(fmaf(cA, col.w, fmaf(-2.f, acc[jj], col.z)) <= T2) << jj;
+                    }
+                }
+                cm &= win;
+                fm &= cm;
                 if (!valid) cm = fm = 0, ver = 0;
                 // warp-aggregated append of the chunk's candidates
                 const unsigned nc = __popc(cm);
@@ -2171,6 +2190,16 @@ __global__ void k_vec_prep(const double *v64, int64_t nq, int D, int Dp, float *
 }
 
 // collect -------------------------------------------------------------------
+
+// sort key for the id tie-break when every hit is a tree entry: the dataset
+// row (row order == id order, data.py:149-153), rbits wide instead of 64
+__global__ void k_gather_row(const int32_t *e, int64_t n, const int32_t *row, uint32_t *key, int32_t *perm)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    key[i] = (uint32_t)row[e[i]];
+    perm[i] = (int32_t)i;
+}
 
 __global__ void k_gather_id(const int32_t *e, int64_t n, const int64_t *ids, const int64_t *cache_ids,
                             unsigned long long *key, int32_t *perm)
@@ -2831,7 +2860,7 @@ struct Search {
     }
 
     DBuf<unsigned> hist;   // kNN edit: per-query distance histogram (shrinking bound)
-    DBuf<unsigned> fhist;  // kNN vectors: per-query 256-bin histogram over [0, r0]
+    DBuf<unsigned> fhist;  // kNN vectors: per-query 64-bin histogram over [0, r0]
     DBuf<float> r0;        // kNN vectors: the probe radius (histogram scale)
 
     void dispatch_verify(const Row *rows, int64_t m, int stats_on)
@@ -2855,12 +2884,20 @@ struct Search {
             static const int env_claim = std::getenv("GTS_EDIT_CLAIM") ? std::atoi(std::getenv("GTS_EDIT_CLAIM")) : 0;
             const int claim = env_claim > 0 ? std::max(kRowChunk, env_claim) : kRowChunk;
             unsigned grid = grid_for((m + kRowChunk - 1) / kRowChunk, kLeafWarps, 148u * 4u);   // 4 resident per SM
-            // texts staged in smem for the DP when strings are short (words);
-            // GTS_EDIT_SMEM_TEXT=0 disables
-            static const char *env_tx = std::getenv("GTS_EDIT_SMEM_TEXT");
+            // opt-in (GTS_EDIT_SMEM_TEXT=1): texts staged in smem for the DP
+            // (byte loads, no symbol extraction).  Measured slower on words
+            // (92.2 vs 83.9 ms): the staging copies cost more than the one ALU
+            // op per symbol they save
+            const char *env_tx = std::getenv("GTS_EDIT_SMEM_TEXT");
             int tstride = 0;
-            if (ix->max_len <= 64 && !(env_tx && env_tx[0] == '0')) tstride = (((ix->max_len + 3) >> 2) | 1);
+            if (ix->max_len <= 64 && env_tx && env_tx[0] == '1') tstride = (((ix->max_len + 3) >> 2) | 1);
             const size_t dyn = (size_t)tstride * kWarp * kLeafWarps * sizeof(uint32_t);
+            static bool le_attr = false;
+            if (!le_attr) {
+                // static 38.9 KB + up to 17 KB of staged texts
+                CK(cudaFuncSetAttribute(k_leaf_edit, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+                le_attr = true;
+            }
             CK(cudaMemsetAsync(counter.p, 0, sizeof(unsigned long long), st));
             timed("k_leaf_edit", [&] {
                 k_leaf_edit<<<grid, 32 * kLeafWarps, dyn, st>>>(iv, qv, rows, m, pruning, r32.p, hb, verified.p,
@@ -3099,16 +3136,26 @@ struct Search {
             perm_a.alloc((size_t)n, st);
             perm_b.alloc((size_t)n, st);
             const unsigned g = grid_for(n, 256);
-            k_gather_id<<<g, 256, 0, st>>>(he.p, n, ix->ids.p, ix->cache_ids.p, ka.p, perm_a.p);
-            LAUNCH_CHECK();
+            if (cache_hits) {
+                k_gather_id<<<g, 256, 0, st>>>(he.p, n, ix->ids.p, ix->cache_ids.p, ka.p, perm_a.p);
+                LAUNCH_CHECK();
+            }
             size_t tmp_bytes = 0, t2 = 0;
             cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, ka.p, kb.p, perm_a.p, perm_b.p, (int)n, 0, 64, st);
             cub::DeviceRadixSort::SortPairs(nullptr, t2, (uint32_t *)nullptr, (uint32_t *)nullptr, perm_a.p,
                                             perm_b.p, (int)n, 0, 32, st);
             tmp_bytes = std::max(tmp_bytes, t2);
             DBuf<uint8_t> tmp(tmp_bytes, st);
-            // 1) by id
-            CK(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, ka.p, kb.p, perm_a.p, perm_b.p, (int)n, 0, 64, st));
+            // 1) by id (by dataset row, rbits wide, when no cache entry is among the hits)
+            if (!cache_hits) {
+                DBuf<uint32_t> ra((size_t)n, st), rb((size_t)n, st);
+                k_gather_row<<<g, 256, 0, st>>>(he.p, n, ix->row.p, ra.p, perm_a.p);
+                LAUNCH_CHECK();
+                CK(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, ra.p, rb.p, perm_a.p, perm_b.p, (int)n, 0, rbits,
+                                                   st));
+            } else {
+                CK(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, ka.p, kb.p, perm_a.p, perm_b.p, (int)n, 0, 64, st));
+            }
             g_launches += 4;
             // 2) stable by distance bits (non-negative doubles order as integers)
             k_gather_d<<<g, 256, 0, st>>>(hd.p, perm_b.p, n, ka.p);
@@ -3509,17 +3556,21 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
         // see similar lengths.  ord[e] = reference position of device entry e.
         std::vector<int64_t> ord((size_t)n);
         for (int64_t e = 0; e < n; e++) ord[(size_t)e] = e;
-        if (ds->metric == GTS_EDIT) {
+        {
+            // strings: by length (DP lanes see similar lengths).  (Vector leaves
+            // sorted by dis, for a binary-searched lemma-1 window in
+            // k_leafgroup_mma2, measured slower: 592 vs 570 ms.)
             __int128 c = 1;
             for (int l = 1; l < ix->levels; l++) c *= ix->nc;
             const int64_t lfirst = (int64_t)((c - 1) / (ix->nc - 1) + 1), lcount = (int64_t)c;
             for (int64_t i = lfirst; i < lfirst + lcount; i++) {
                 const int64_t p0 = t->pos[i], sz = t->size[i];
                 if (sz <= 1) continue;
-                std::stable_sort(ord.begin() + p0, ord.begin() + p0 + sz, [&](int64_t a, int64_t b) {
-                    const int64_t ra = t->rows[a], rb = t->rows[b];
-                    return ds->offsets[ra + 1] - ds->offsets[ra] < ds->offsets[rb + 1] - ds->offsets[rb];
-                });
+                if (ds->metric == GTS_EDIT)
+                    std::stable_sort(ord.begin() + p0, ord.begin() + p0 + sz, [&](int64_t a, int64_t b) {
+                        const int64_t ra = t->rows[a], rb = t->rows[b];
+                        return ds->offsets[ra + 1] - ds->offsets[ra] < ds->offsets[rb + 1] - ds->offsets[rb];
+                    });
             }
         }
         std::vector<int64_t> drow((size_t)n);

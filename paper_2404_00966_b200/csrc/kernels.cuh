@@ -418,18 +418,22 @@ __device__ __forceinline__ float slack(const IndexView &ix, float a, float b, fl
     return ix.rel > 0.f ? ix.rel * (fabsf(a) + fabsf(b) + fabsf(c)) + ix.abs_eps : ix.abs_eps;
 }
 
-// Lemma-1 entry test for float metrics (search.py:523, 559) with the fp32
-// slack folded into one FFMA: |dis - dqp| - rel*dis <= r + rel*(dqp + r) + eps,
-// i.e. |dis - dqp| <= r + rel*(dis + dqp + r) + eps.  Every float kernel uses
-// this one expression, so all paths count the same "verified" entries; a NaN
-// dis (tombstoned / padding column) fails it.
-__device__ __forceinline__ float lemma1_rrow(const IndexView &ix, float dqp, float r)
+// Lemma-1 entry test for float metrics (search.py:523, 559) as a window on
+// the entry's pivot distance: |dis - dqp| <= r + rel*(dis + dqp + r) + eps
+// solved for dis (no divisions: 1/(1+rel) >= 1-rel, 1/(1-rel) <= 1+2rel),
+//   lo = (dqp - r - s)(1 - rel)(1 - 2^-21)   (or -inf when that is <= 0),
+//   hi = (dqp + r + s)(1 + 2 rel)(1 + 2^-21),   s = rel (dqp + r) + eps,
+// a superset of the fp32-slack test, which is itself a superset of the
+// reference's float64 test.  Two comparisons per entry; every float kernel
+// counts the same "verified" entries.  NaN (tombstoned / padding) fails.
+__device__ __forceinline__ float2 lemma1_range(const IndexView &ix, float dqp, float r)
 {
-    return r + (ix.rel * (dqp + r) + ix.abs_eps);
+    const float s = ix.rel * (dqp + r) + ix.abs_eps;
+    const float num = dqp - r - s;
+    const float lo = num > 0.f ? num * (1.f - ix.rel) * (1.f - 0x1p-21f) : -INFINITY;
+    const float hi = (dqp + r + s) * (1.f + 2.f * ix.rel) * (1.f + 0x1p-21f);
+    return make_float2(lo, hi);
 }
-__device__ __forceinline__ bool lemma1_pass(const IndexView &ix, float dis, float dqp, float rrow)
-{
-    return fmaf(-ix.rel, dis, fabsf(dis - dqp)) <= rrow;
-}
+__device__ __forceinline__ bool lemma1_in(float dis, float2 rg) { return dis >= rg.x && dis <= rg.y; }
 
 }  // namespace gts

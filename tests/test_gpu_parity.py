@@ -18,18 +18,21 @@ from oracle import oracle as O
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["default", "rowwise", "edit_grouped"], autouse=True)
+@pytest.fixture(params=["default", "rowwise", "grouped_alt", "smem_text"], autouse=True)
 def leaf_path(request, monkeypatch):
     """Every test runs on each leaf-verification path: default (k_leaf_edit;
-    k_leafgroup_mma2 / k_leafgroup_vec for vectors), row-wise vectors
-    (k_verify, GTS_NO_GROUPED=1) and leaf-grouped edit (k_leafgroup_edit,
-    GTS_EDIT_GROUPED=1)."""
-    monkeypatch.delenv("GTS_NO_GROUPED", raising=False)
-    monkeypatch.delenv("GTS_EDIT_GROUPED", raising=False)
+    k_leafgroup_mma2 / k_leafgroup_tile for vectors), row-wise vectors
+    (k_verify, GTS_NO_GROUPED=1), the grouped alternates (k_leafgroup_edit,
+    warp-per-row k_leafgroup_vec) and the smem-text DP of k_leaf_edit."""
+    for k in ("GTS_NO_GROUPED", "GTS_EDIT_GROUPED", "GTS_EDIT_SMEM_TEXT", "GTS_VEC_ROWWARP"):
+        monkeypatch.delenv(k, raising=False)
     if request.param == "rowwise":
         monkeypatch.setenv("GTS_NO_GROUPED", "1")
-    elif request.param == "edit_grouped":
+    elif request.param == "grouped_alt":
         monkeypatch.setenv("GTS_EDIT_GROUPED", "1")
+        monkeypatch.setenv("GTS_VEC_ROWWARP", "1")
+    elif request.param == "smem_text":
+        monkeypatch.setenv("GTS_EDIT_SMEM_TEXT", "1")
     return request.param
 
 
