@@ -588,8 +588,9 @@ __global__ void k_seg_counts(const unsigned long long *key, int64_t n, int qshif
 // of one per (query, entry) pair.  Same filter / screen / float64 recheck as
 // k_verify (search.py:507-570).
 // ---------------------------------------------------------------------------
-struct Item {
-    int32_t leaf, start, count, pad;
+struct Item {                      // 32 B: a leaf (node) and a run of its grouped rows
+    int32_t leaf, start, count, size;   // size / pos: the node's, for kernels that stage it
+    int32_t pos, pad0, pad1, pad2;
 };
 constexpr int kItemQueries = 128;
 
@@ -628,13 +629,15 @@ __global__ void k_item_counts(const int *cnt, int nleaf, int per, int *nitem)
 }
 
 __global__ void k_make_items(const int *cnt, const int *off, const int *item_off, int nleaf, int leaf_first, int per,
-                             Item *items)
+                             const NodeRec *node, const int32_t *npos, Item *items)
 {
     int l = blockIdx.x * blockDim.x + threadIdx.x;
     if (l >= nleaf) return;
     const int c = cnt[l];
+    const int nd = leaf_first + l;
+    const int size = c ? node[nd].size : 0, pos = c ? npos[nd] : 0;
     for (int j = 0, s = 0; s < c; j++, s += per)
-        items[item_off[l] + j] = Item{leaf_first + l, off[l] + s, min(per, c - s), 0};
+        items[item_off[l] + j] = Item{nd, off[l] + s, min(per, c - s), size, pos, 0, 0, 0};
 }
 
 // ---------------------------------------------------------------------------
@@ -1093,7 +1096,7 @@ struct CandBuf {
 };
 
 template <int MET>
-__global__ void __launch_bounds__(256, 3) k_leafgroup_tile(IndexView ix, QueryView qv, const Row *__restrict__ srows,
+__global__ void __launch_bounds__(256, 4) k_leafgroup_tile(IndexView ix, QueryView qv, const Row *__restrict__ srows,
                                                         const Item *__restrict__ items, int nitems, int pruning,
                                                         float *r32, double *r64, CandBuf cb,
                                                         unsigned long long *verified_stat, int stats_on,
@@ -1554,6 +1557,7 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
     __shared__ uint64_t mbar[2];
     __shared__ uint32_t tmem_slot;
     __shared__ int4 s_item[4];           // {leaf, start, count, size}, ring by i % 4
+    __shared__ int4 s_itemraw[4][2];     // raw Item copies (cp.async) before they become s_item
     __shared__ int s_pos[4];
     __shared__ float4 s_col[3][256];     // ring by i % 3 (see meta_store)
     __shared__ int s_rq[3][128];         // query ids (-1: no row)
@@ -1574,14 +1578,14 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
         tc::mbar_init(&mbar[1], 1);
         tc::fence_mbar_init();
     }
-    // descriptors of items 0..2
+    // descriptors of items 0..2 ({leaf, start, count, size}, pos)
     if (tid < 3) {
         int4 d = make_int4(0, 0, 0, 0);
         int p0 = 0;
         if (idx(tid) < nitems) {
             const Item it = items[idx(tid)];
-            d = make_int4(it.leaf, it.start, it.count, ix.node[it.leaf].size);
-            p0 = ix.npos[it.leaf];
+            d = make_int4(it.leaf, it.start, it.count, it.size);
+            p0 = it.pos;
         }
         s_item[tid] = d;
         s_pos[tid] = p0;
@@ -1591,31 +1595,33 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
     tc::fence_after_sync();
     const uint32_t tmem = tmem_slot;
 
-    // metadata loads of item i (registers), then the store into ring slot i % 3
+    // metadata loads of item i (registers), then the store into ring slot i % 3.
+    // Threads 0..127 load row i's {q, dqp, r, |q|, r0}; threads 128..383
+    // column (tid - 128)'s {dis, se, alive}; one packed float4 + float each,
+    // so few registers stay live across the epilogue.
     struct Meta {
-        int q;
-        float4 rf;
-        float dis, se;
-        bool al;
+        float4 a;
+        float b;
     };
     auto meta_load = [&](int i, Meta &m) {
         const int4 d = s_item[i & 3];
         const int pos = s_pos[i & 3];
-        m.q = -1;
-        m.rf = make_float4(0.f, -1.f, 0.f, 0.f);
-        m.dis = 0.f;
-        m.se = 0.f;
-        m.al = false;
+        m.a = make_float4(0.f, -1.f, 0.f, 0.f);
+        m.b = __int_as_float(-1);
         if (idx(i) >= nitems) return;
-        if (tid < 128 && tid < d.z) {
-            const Row lr = srows[d.y + tid];
-            m.q = lr.q;
-            m.rf = make_float4(lr.dqp, __ldcg(r32 + lr.q), qv.qn[lr.q], r0 ? r0[lr.q] : 0.f);
-        }
-        if (tid < d.w) {
-            m.dis = __ldg(ix.dis + pos + tid);
-            m.se = __ldg(ix.vse + pos + tid);
-            m.al = is_alive(ix.alive, pos + tid);
+        if (tid < 128) {
+            if (tid < d.z) {
+                const Row lr = srows[d.y + tid];
+                m.b = __int_as_float(lr.q);
+                m.a = make_float4(lr.dqp, __ldcg(r32 + lr.q), qv.qn[lr.q], r0 ? r0[lr.q] : 0.f);
+            }
+        } else {
+            const int j = tid - 128;
+            if (j < d.w) {
+                m.a.x = __ldg(ix.dis + pos + j);
+                m.a.y = __ldg(ix.vse + pos + j);
+                m.a.z = is_alive(ix.alive, pos + j) ? 1.f : 0.f;
+            }
         }
     };
     auto meta_store = [&](int i, const Meta &m) {
@@ -1623,24 +1629,25 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
         const int4 d = s_item[i & 3];
         const int N = max(16, (d.w + 15) & ~15);
         if (tid < 128) {
-            s_rq[sl][tid] = m.q;
-            s_rf[sl][tid] = m.rf;
-        }
-        if (tid < N) {
+            s_rq[sl][tid] = __float_as_int(m.b);
+            s_rf[sl][tid] = m.a;
+        } else if (tid - 128 < N) {
+            const int j = tid - 128;
             // {dis | NaN, y - z | NaN, y + z, dis}: NaN (tombstone / padding)
             // fails the lemma-1 window and the screen
             const float nan = __int_as_float(0x7fc00000);
             float4 col = make_float4(nan, nan, 0.f, INFINITY);
-            if (tid < d.w) {
-                const float y = fmaf(m.dis, m.dis, 2.f * m.se), z = 8.f * ix.rel * m.dis * m.dis;
-                if (m.al) {
-                    col.x = m.dis;
+            if (j < d.w) {
+                const float dis = m.a.x, se = m.a.y;
+                const float y = fmaf(dis, dis, 2.f * se), z = 8.f * ix.rel * dis * dis;
+                if (m.a.z != 0.f) {
+                    col.x = dis;
                     col.y = y - z;
                 }
                 col.z = y + z;
-                col.w = m.dis;
+                col.w = dis;
             }
-            s_col[sl][tid] = col;
+            s_col[sl][j] = col;
         }
     };
     // operands of item i into smem stage i & 1 (async)
@@ -1709,12 +1716,12 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
         if (has1) stage(i + 1);
         Meta mnext;
         meta_load(i + 2, mnext);
-        int4 dn = make_int4(0, 0, 0, 0);
-        int pn = 0;
+        // descriptor of item i+3: a 32-byte async copy straight into smem
         if (tid == 0 && idx(i + 3) < nitems) {
-            const Item it = items[idx(i + 3)];
-            dn = make_int4(it.leaf, it.start, it.count, ix.node[it.leaf].size);
-            pn = ix.npos[it.leaf];
+            const Item *src = items + idx(i + 3);
+            tc::cp_async16(tc::smem_u32(&s_itemraw[(i + 3) & 3][0]), src, 16u);
+            tc::cp_async16(tc::smem_u32(&s_itemraw[(i + 3) & 3][1]), reinterpret_cast<const int4 *>(src) + 1, 16u);
+            tc::cp_async_commit();
         }
         tc::mbar_wait(&mbar[s], phase[s]);
         phase[s] ^= 1u;
@@ -1842,11 +1849,12 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
         }
         // metadata of item i+2 and the descriptor of item i+3 (loads done by now)
         meta_store(i + 2, mnext);
-        if (tid == 0) {
-            s_item[(i + 3) & 3] = dn;
-            s_pos[(i + 3) & 3] = pn;
-        }
         tc::cp_async_wait_all();
+        if (tid == 0) {
+            const int4 r0_ = s_itemraw[(i + 3) & 3][0], r1_ = s_itemraw[(i + 3) & 3][1];
+            s_item[(i + 3) & 3] = idx(i + 3) < nitems ? r0_ : make_int4(0, 0, 0, 0);   // {leaf, start, count, size}
+            s_pos[(i + 3) & 3] = r1_.x;
+        }
         tc::fence_async_smem();
         tc::fence_before_sync();
         __syncthreads();
@@ -2602,7 +2610,8 @@ struct Search {
         G.nitems = *h_nitems;
         if (G.nitems == 0) return;
         G.items.alloc((size_t)G.nitems, st);
-        k_make_items<<<grid_for(nleaf, 256), 256, 0, st>>>(cnt.p, off.p, ioff.p, nleaf, first, per, G.items.p);
+        k_make_items<<<grid_for(nleaf, 256), 256, 0, st>>>(cnt.p, off.p, ioff.p, nleaf, first, per, ix->node.p,
+                                                           ix->npos.p, G.items.p);
         LAUNCH_CHECK();
     }
 
