@@ -34,7 +34,10 @@
 
 typedef int64_t i64;
 
-enum { M_EDIT = 0, M_L1 = 1, M_L2 = 2 };
+#ifndef M_PI
+#define M_PI 3.14159265358979323846
+#endif
+enum { M_EDIT = 0, M_L1 = 1, M_L2 = 2, M_ANGULAR = 3 };
 enum { MODE_RANGE = 0, MODE_KNN = 1 };
 
 /* A payload collection: dataset or query batch (data.py:59-126). */
@@ -109,9 +112,41 @@ static double pw_sum(const double *a, i64 n)
     }
 }
 
+/* metrics.py:136-163 / 175-193 (angular_one_to_many / angular_row_pairs):
+ * norms = sqrt(pairwise sum of squares) (data.py:81-84), dots = pairwise sum
+ * of products, cos = clip(dot / (nx * nq), -1, 1), d = arccos(cos); zero
+ * vectors sit at pi from non-zero vectors and 0 from each other; d < 1e-6 with
+ * identical components -> 0.  The reference's one_to_many takes the query norm
+ * from np.dot (BLAS, summation order unspecified); this uses the pairwise sum
+ * for both norms, so query distances can differ from the reference in the
+ * last bits (tests compare them with a 1e-12 relative tolerance); row_pairs
+ * (the build) is the same computation bit for bit. */
+static double angular_dist(const double *x, const double *q, i64 D, double *tmp)
+{
+    for (i64 d = 0; d < D; d++) tmp[d] = x[d] * x[d];
+    const double nx = sqrt(pw_sum(tmp, D));
+    for (i64 d = 0; d < D; d++) tmp[d] = q[d] * q[d];
+    const double nq = sqrt(pw_sum(tmp, D));
+    if (nq == 0.0) return nx == 0.0 ? 0.0 : M_PI;
+    if (nx == 0.0) return M_PI;
+    for (i64 d = 0; d < D; d++) tmp[d] = x[d] * q[d];
+    const double dot = pw_sum(tmp, D);
+    double c = dot / (nx * nq);
+    if (c < -1.0) c = -1.0;
+    if (c > 1.0) c = 1.0;
+    double r = acos(c);
+    if (r < 1e-6) {
+        int eq = 1;
+        for (i64 d = 0; d < D && eq; d++) eq = x[d] == q[d];
+        if (eq) r = 0.0;
+    }
+    return r;
+}
+
 /* metrics.py:127-133 / 166-172: diff = x - q; L1 = sum|diff|, L2 = sqrt(sum diff^2) */
 static double vec_dist(i64 metric, const double *x, const double *q, i64 D, double *tmp)
 {
+    if (metric == M_ANGULAR) return angular_dist(x, q, D, tmp);
     for (i64 d = 0; d < D; d++) {
         double diff = x[d] - q[d];
         tmp[d] = (metric == M_L1) ? fabs(diff) : diff * diff;

@@ -42,11 +42,13 @@ from .tree import (
     parent_node_id,
     tree_height,
 )
+from .snapshot import SnapshotFormatError, load_snapshot, save_snapshot
 from .updates import StreamingIndex, UpdateError
 
 __version__ = "0.1.0"
 
 __all__ = [
+    "SnapshotFormatError", "load_snapshot", "save_snapshot",
     "ANGULAR", "EDIT", "L1", "L2", "METRIC_KINDS", "BatchSearcher", "BudgetError", "ConfigError",
     "CsrResult", "DataObject", "Dataset", "DEFAULT_MEMORY_UNITS", "FlatPivotTree", "MemoryBudget",
     "MetricMismatchError", "ParallelRuntime", "SearchStats", "StreamingIndex", "TreeConfig", "UpdateError",

@@ -47,8 +47,32 @@ static double pw_sum(const double *a, int64_t n)
     return pw_sum(a, n2) + pw_sum(a + n2, n - n2);
 }
 
+// angular_row_pairs (metrics.py:175-193) with the dataset's pairwise norms
+// (data.py:81-84): arccos(clip(dot / (|x| |q|))), zero-vector rules, and
+// identical vectors forced to 0.  libm's acos: the reference's numpy arccos
+// may differ in the last bits (see tests/test_angular.py).
+static double host_angular(const double *x, const double *q, int64_t D, double *tmp)
+{
+    for (int64_t d = 0; d < D; d++) tmp[d] = x[d] * x[d];
+    const double nx = std::sqrt(pw_sum(tmp, D));
+    for (int64_t d = 0; d < D; d++) tmp[d] = q[d] * q[d];
+    const double nq = std::sqrt(pw_sum(tmp, D));
+    if (nx == 0.0 || nq == 0.0) return (nx == 0.0 && nq == 0.0) ? 0.0 : M_PI;
+    for (int64_t d = 0; d < D; d++) tmp[d] = x[d] * q[d];
+    double c = pw_sum(tmp, D) / (nx * nq);
+    c = std::min(1.0, std::max(-1.0, c));
+    double r = std::acos(c);
+    if (r < 1e-6) {
+        bool eq = true;
+        for (int64_t d = 0; d < D && eq; d++) eq = x[d] == q[d];
+        if (eq) r = 0.0;
+    }
+    return r;
+}
+
 double host_vec_dist(int metric, const double *x, const double *q, int64_t D, double *tmp)
 {
+    if (metric == GTS_ANGULAR) return host_angular(x, q, D, tmp);
     for (int64_t d = 0; d < D; d++) {
         double diff = x[d] - q[d];
         tmp[d] = (metric == GTS_L1) ? std::fabs(diff) : diff * diff;
@@ -168,8 +192,8 @@ extern "C" int gts_build_tree(const gts_dataset *ds, int64_t root_row, int nthre
         if (n == 0) { t->levels = 0; t->split_rounds = 0; return GTS_OK; }
         if (root_row < 0 || root_row >= n) return set_error(GTS_EINVAL, "root_row out of range");
         const bool edit = ds->metric == GTS_EDIT;
-        if (!edit && ds->metric != GTS_L1 && ds->metric != GTS_L2)
-            return set_error(GTS_EMETRIC, "builder supports edit, l1, l2");
+        if (!edit && ds->metric != GTS_L1 && ds->metric != GTS_L2 && ds->metric != GTS_ANGULAR)
+            return set_error(GTS_EMETRIC, "builder supports edit, l1, l2, angular");
         if (nthreads > 0) omp_set_num_threads(nthreads);
         int64_t max_h, split;
         gts_tree_height(n, nc, &max_h, &split);

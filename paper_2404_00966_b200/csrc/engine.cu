@@ -1962,6 +1962,10 @@ __global__ void k_cache_scan(IndexView ix, QueryView qv, CacheView cv, int nq, c
     double d;
     if (MET == kMetricEdit) {
         d = (double)edit_peq(qv.peq + qv.peq_off[q], qlen(qv, q), cv.words + cv.sword[c], cv.slen[c]);
+    } else if (MET == kMetricAngular) {
+        const double *x = cv.vec64 + (size_t)c * ix.D, *q64 = qv.vec64 + (size_t)q * ix.D;
+        const double dot = pw_sum64<kMetricAngular>(nullptr, x, q64, 0, ix.D);
+        d = angular_finish(dot, norm64(x, ix.D), qv.qnorm64[q], nullptr, x, q64, ix.D);
     } else {
         const double s = pw_sum64<MET>(nullptr, cv.vec64 + (size_t)c * ix.D, qv.vec64 + (size_t)q * ix.D, 0, ix.D);
         d = MET == kMetricL1 ? s : __dsqrt_rn(s);
@@ -2270,8 +2274,13 @@ __global__ void k_pair_vec(int metric, int64_t np, int D, const double *a, const
 {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= np) return;
-    double s = metric == kMetricL1 ? pw_sum64<kMetricL1>(nullptr, a + i * D, b + i * D, 0, D)
-                                   : pw_sum64<kMetricL2>(nullptr, a + i * D, b + i * D, 0, D);
+    const double *x = a + i * D, *y = b + i * D;
+    if (metric == kMetricAngular) {   // angular_row_pairs (metrics.py:175-193)
+        const double dot = pw_sum64<kMetricAngular>(nullptr, x, y, 0, D);
+        out[i] = angular_finish(dot, norm64(x, D), norm64(y, D), nullptr, x, y, D);
+        return;
+    }
+    double s = metric == kMetricL1 ? pw_sum64<kMetricL1>(nullptr, x, y, 0, D) : pw_sum64<kMetricL2>(nullptr, x, y, 0, D);
     out[i] = metric == kMetricL1 ? s : __dsqrt_rn(s);
 }
 
@@ -2293,6 +2302,36 @@ using namespace gts;
 
 namespace gts {
 constexpr int kHistMinAlphabet = 8;   // symbol-histogram bound only pays on larger alphabets
+
+// numpy's pairwise sum (host; same order as pw_sum64 / the oracle)
+static double host_pw_sum(const double *a, int64_t n)
+{
+    if (n < 8) {
+        double r = 0.0;
+        for (int64_t i = 0; i < n; i++) r += a[i];
+        return r;
+    } else if (n <= 128) {
+        double r[8];
+        int64_t i;
+        for (int j = 0; j < 8; j++) r[j] = a[j];
+        for (i = 8; i < n - (n % 8); i += 8)
+            for (int j = 0; j < 8; j++) r[j] += a[i + j];
+        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < n; i++) res += a[i];
+        return res;
+    }
+    int64_t n2 = n / 2;
+    n2 -= n2 % 8;
+    return host_pw_sum(a, n2) + host_pw_sum(a + n2, n - n2);
+}
+
+// |x| as numpy computes the angular norms: sqrt((mat * mat).sum(axis=1))
+static double host_norm(const double *x, int64_t D, std::vector<double> &tmp)
+{
+    tmp.resize((size_t)std::max<int64_t>(D, 1));
+    for (int64_t d = 0; d < D; d++) tmp[(size_t)d] = x[d] * x[d];
+    return std::sqrt(host_pw_sum(tmp.data(), D));
+}
 // Pack strings (dense symbols, given per string as a code range mapped by
 // `sym`) 4 per 32-bit word, each string starting on a 16-byte boundary.
 template <class SymOf>
@@ -2345,6 +2384,8 @@ struct gts_index {
     DBuf<uint4> erec;
     DBuf<uint4> ehist;
     DBuf<uint4> vcent;   // bf16 x 8 per uint4
+    DBuf<float> vnorm32;   // angular: |o| per entry
+    DBuf<double> vnorm64;
     DBuf<float> vse;     // c . vcent_e per entry
     int Dk = 0;
     DBuf<int32_t> alpha;
@@ -2382,6 +2423,8 @@ struct gts_queries {
     DBuf<int64_t> peq_off;
     DBuf<uint4> qhist;
     DBuf<uint4> qbf;     // bf16 query rows (tensor-core L2 path)
+    DBuf<float> qnorm32;   // angular: |q|
+    DBuf<double> qnorm64;
     DBuf<float> qn;
 };
 
@@ -2413,6 +2456,8 @@ IndexView make_view(const gts_index *ix, const gts_queries *q)
     v.erec = ix->erec.p;
     v.ehist = ix->ehist.p;
     v.vcent = ix->vcent.p;
+    v.vnorm32 = ix->vnorm32.p;
+    v.vnorm64 = ix->vnorm64.p;
     v.vse = ix->vse.p;
     v.Dk = ix->Dk;
     v.D = ix->D;
@@ -2425,6 +2470,14 @@ IndexView make_view(const gts_index *ix, const gts_queries *q)
     if (ix->metric == GTS_EDIT) {
         v.rel = 0.f;
         v.abs_eps = 0.f;
+    } else if (ix->metric == GTS_ANGULAR) {
+        // fp32 cosine error eps_c <= (3D + 8) 2^-24 (dot and both norms; x2
+        // for inputs that are not fp32-exact); arccos turns it into at most
+        // sqrt(2 eps_c) (worst near cos = +-1), plus acosf's own error
+        const bool exact = ix->data_exact && (!q || q->exact);
+        const float ec = (float)(3 * ix->D + 8) * ldexpf(1.f, -24) * (exact ? 1.f : 2.f);
+        v.rel = 0.f;
+        v.abs_eps = 1.1f * sqrtf(2.f * ec) + 8e-6f;
     } else {
         // fp32 screening error model: relative (D+8)*2^-23 covers sequential
         // fp32 accumulation of D terms with margin; inputs that are not
@@ -2448,6 +2501,8 @@ QueryView make_qview(const gts_index *ix, const gts_queries *q)
     v.peq_off = q->peq_off.p;
     v.qhist = q->qhist.p;
     v.qbf = q->qbf.p;
+    v.qnorm32 = q->qnorm32.p;
+    v.qnorm64 = q->qnorm64.p;
     v.qn = q->qn.p;
     v.A = ix->A;
     return v;
@@ -2828,9 +2883,12 @@ struct Search {
     template <int MET>
     void launch_verify(const Row *rows, int64_t m, int stats_on)
     {
-        if (grouped_smem() && ix->Dp >= 8 && std::getenv("GTS_NO_GROUPED") == nullptr) {
-            launch_grouped<MET>(rows, m, stats_on);
-            return;
+        // angular: the row-wise kernel (fp32 cosine screen + float64 recheck)
+        if constexpr (MET != kMetricAngular) {
+            if (grouped_smem() && ix->Dp >= 8 && std::getenv("GTS_NO_GROUPED") == nullptr) {
+                launch_grouped<MET>(rows, m, stats_on);
+                return;
+            }
         }
         HitBuf hb{hq.p, he.p, hd.p, (unsigned long long)hq.n, counter.p + 1};
         unsigned grid = grid_for(m * 32, 256, 148u * 64u);
@@ -2918,6 +2976,7 @@ struct Search {
             break;
         }
         case GTS_L1: launch_verify<kMetricL1>(rows, m, stats_on); break;
+        case GTS_ANGULAR: launch_verify<kMetricAngular>(rows, m, stats_on); break;
         default: launch_verify<kMetricL2>(rows, m, stats_on); break;
         }
     }
@@ -2925,7 +2984,7 @@ struct Search {
     template <int MET>
     int64_t launch_expand(const Row *in, int64_t m, int own, Row *out, int layer)
     {
-        if (MET != kMetricEdit && ix->D >= 16 && std::getenv("GTS_NO_GROUPED") == nullptr) {
+        if ((MET == kMetricL1 || MET == kMetricL2) && ix->D >= 16 && std::getenv("GTS_NO_GROUPED") == nullptr) {
             // parent rows of this layer are nodes [first, first + count)
             int64_t c = 1;
             for (int l = 1; l < layer; l++) c *= ix->nc;
@@ -2963,6 +3022,7 @@ struct Search {
         switch (ix->metric) {
         case GTS_EDIT: return launch_expand<kMetricEdit>(in, m, own, out, layer);
         case GTS_L1: return launch_expand<kMetricL1>(in, m, own, out, layer);
+        case GTS_ANGULAR: return launch_expand<kMetricAngular>(in, m, own, out, layer);
         default: return launch_expand<kMetricL2>(in, m, own, out, layer);
         }
     }
@@ -3011,6 +3071,7 @@ struct Search {
             switch (ix->metric) {
             case GTS_EDIT: launch_probe<kMetricEdit>(); break;
             case GTS_L1: launch_probe<kMetricL1>(); break;
+            case GTS_ANGULAR: launch_probe<kMetricAngular>(); break;
             default: launch_probe<kMetricL2>(); break;
             }
             if (ix->metric != GTS_EDIT) {
@@ -3040,6 +3101,7 @@ struct Search {
         switch (ix->metric) {
         case GTS_EDIT: launch_root<kMetricEdit>(root.p); break;
         case GTS_L1: launch_root<kMetricL1>(root.p); break;
+        case GTS_ANGULAR: launch_root<kMetricAngular>(root.p); break;
         default: launch_root<kMetricL2>(root.p); break;
         }
         process(1, root.p, nq);
@@ -3066,6 +3128,7 @@ struct Search {
             switch (ix->metric) {
             case GTS_EDIT: launch_cache_scan<kMetricEdit>(); break;
             case GTS_L1: launch_cache_scan<kMetricL1>(); break;
+            case GTS_ANGULAR: launch_cache_scan<kMetricAngular>(); break;
             default: launch_cache_scan<kMetricL2>(); break;
             }
             const unsigned long long after = read_counter(1);
@@ -3268,6 +3331,19 @@ gts_queries *upload_queries(gts_index *ix, const gts_query_batch *qb, cudaStream
                 k_vec_prep<<<grid_for(nq * q->Dp, 256), 256, 0, st>>>(q->vec64.p, nq, q->D, q->Dp, q->vec32.p,
                                                                       flags.p, (int *)(flags.p + 1));
                 LAUNCH_CHECK();
+            }
+            if (ix->metric == GTS_ANGULAR && nq) {
+                std::vector<double> nrm((size_t)nq), tmp;
+                std::vector<float> nrm32((size_t)nq);
+                for (int64_t i = 0; i < nq; i++) {
+                    nrm[(size_t)i] = host_norm(qb->vectors + i * q->D, q->D, tmp);
+                    nrm32[(size_t)i] = (float)nrm[(size_t)i];
+                }
+                q->qnorm64.alloc((size_t)nq, st);
+                h2d(q->qnorm64.p, nrm.data(), (size_t)nq, st);
+                q->qnorm32.alloc((size_t)nq, st);
+                h2d(q->qnorm32.p, nrm32.data(), (size_t)nq, st);
+                CK(cudaStreamSynchronize(st));
             }
             if (ix->vcent.p && nq) {
                 q->qbf.alloc((size_t)nq * (ix->Dk / 8), st);
@@ -3531,8 +3607,8 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
         }
     }
     if (!ds || !t || !out) fail(GTS_EINVAL, "null argument");
-    if (ds->metric != GTS_EDIT && ds->metric != GTS_L1 && ds->metric != GTS_L2)
-        fail(GTS_EMETRIC, "metric %d not supported on the device path (edit, l1, l2)", ds->metric);
+    if (ds->metric != GTS_EDIT && ds->metric != GTS_L1 && ds->metric != GTS_L2 && ds->metric != GTS_ANGULAR)
+        fail(GTS_EMETRIC, "metric %d not supported on the device path (edit, l1, l2, angular)", ds->metric);
     if (ds->n > (1ll << 31) - 64) fail(GTS_EINVAL, "index larger than 2^31 entries; shard it");
     CK(cudaSetDevice(device));
     if (std::getenv("GTS_PHASES") && !g_phase_dev) {
@@ -3752,6 +3828,19 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
                 CK(cudaMemcpyAsync(ix->vcent.p, vc.data(), vc.size() * sizeof(__nv_bfloat16), cudaMemcpyHostToDevice, st));
                 ix->vse.alloc((size_t)n, st);
                 h2d(ix->vse.p, se.data(), (size_t)n, st);
+                CK(cudaStreamSynchronize(st));
+            }
+            if (ds->metric == GTS_ANGULAR) {
+                std::vector<double> nrm((size_t)n), tmp;
+                std::vector<float> nrm32((size_t)n);
+                for (int64_t e = 0; e < n; e++) {
+                    nrm[(size_t)e] = host_norm(ds->vectors + drow[(size_t)e] * ix->D, ix->D, tmp);
+                    nrm32[(size_t)e] = (float)nrm[(size_t)e];
+                }
+                ix->vnorm64.alloc((size_t)n, st);
+                h2d(ix->vnorm64.p, nrm.data(), (size_t)n, st);
+                ix->vnorm32.alloc((size_t)n, st);
+                h2d(ix->vnorm32.p, nrm32.data(), (size_t)n, st);
                 CK(cudaStreamSynchronize(st));
             }
             ix->vec32.alloc(v32.size(), st);
@@ -3996,7 +4085,7 @@ extern "C" int gts_pair_distances(int32_t metric, int64_t np, int64_t dim, const
     ABI_BEGIN
     cudaStream_t st = (cudaStream_t)stream;
     if (np == 0) return GTS_OK;
-    if (metric == GTS_L1 || metric == GTS_L2) {
+    if (metric == GTS_L1 || metric == GTS_L2 || metric == GTS_ANGULAR) {
         DBuf<double> a((size_t)(np * dim), st), b((size_t)(np * dim), st), o((size_t)np, st);
         h2d(a.p, a_vec, (size_t)(np * dim), st);
         h2d(b.p, b_vec, (size_t)(np * dim), st);

@@ -19,7 +19,8 @@ namespace gts {
 
 constexpr int kWarp = 32;
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kMetricEdit = 0, kMetricL1 = 1, kMetricL2 = 2;
+constexpr int kMetricEdit = 0, kMetricL1 = 1, kMetricL2 = 2, kMetricAngular = 3;
+constexpr int kMetricSq = 4;   // pw_sum64 term x*x (norms; the second operand is not read for its value)
 constexpr int kMaxWords = 128;      // edit patterns up to 4096 symbols
 constexpr uint8_t kNoSym = 0xff;    // query symbol absent from the index alphabet
 
@@ -48,6 +49,8 @@ struct IndexView {
     const uint4 *erec;       // [n] edit scan records {dis f32 bits, len, first text word, 0}
     const uint4 *ehist;      // [2n] 32 byte-buckets of symbol counts (symbol % 32), or null
     const uint4 *vcent;      // [n][Dk/8] bf16 vectors centred on their leaf pivot (tensor-core L2 path), or null
+    const float *vnorm32;    // angular: |o| per entry (fp32 screen), or null
+    const double *vnorm64;   // angular: |o| per entry, numpy's pairwise sum of squares
     const float *vse;        // [n] c . vcent_e (pivot . centred bf16 entry), tensor-core path
     int Dk;                  // D rounded up to 64 (one 128-byte bf16 row per K-block)
     int D, Dp, nc, levels;
@@ -64,6 +67,8 @@ struct QueryView {
     const int64_t *peq_off;
     const uint4 *qhist;    // [2nq] query symbol histograms (same buckets as ehist)
     const uint4 *qbf;      // [nq][Dk/8] bf16 query rows (tensor-core L2 path)
+    const float *qnorm32;  // angular: |q| (fp32 screen)
+    const double *qnorm64; // angular: |q|, pairwise sum of squares
     const float *qn;       // [nq] |q| rounded up
     int A;
 };
@@ -357,6 +362,8 @@ __device__ __forceinline__ float vdist32(const float *__restrict__ a, const floa
 template <int MET>
 __device__ __forceinline__ double term64(double x, double y)
 {
+    if (MET == kMetricAngular) return __dmul_rn(x, y);   // dot-product terms
+    if (MET == kMetricSq) return __dmul_rn(x, x);        // squared-norm terms
     double d = __dadd_rn(x, -y);
     return MET == kMetricL1 ? fabs(d) : __dmul_rn(d, d);
 }
@@ -390,13 +397,56 @@ __device__ double pw_sum64(const float *o32, const double *o64, const double *q,
     return __dadd_rn(pw_sum64<MET>(o32, o64, q, s, n2), pw_sum64<MET>(o32, o64, q, s + n2, n - n2));
 }
 
+// angular_one_to_many (metrics.py:136-163) from the dot product and the two
+// norms: zero vectors at pi from non-zero vectors and 0 from each other,
+// arccos(clip(dot / (|o| |q|))), and identical vectors forced to 0.
+__device__ __forceinline__ double angular_finish(double dot, double no, double nq, const float *o32,
+                                                 const double *o64, const double *qv64, int D)
+{
+    if (nq == 0.0) return no == 0.0 ? 0.0 : 3.141592653589793;
+    if (no == 0.0) return 3.141592653589793;
+    double c = __ddiv_rn(dot, __dmul_rn(no, nq));
+    c = fmin(1.0, fmax(-1.0, c));
+    double r = acos(c);
+    if (r < 1e-6) {
+        bool eq = true;
+        for (int i = 0; i < D && eq; i++) eq = (o64 ? o64[i] : (double)o32[i]) == qv64[i];
+        if (eq) r = 0.0;
+    }
+    return r;
+}
+
 template <int MET>
 __device__ __forceinline__ double vdist64(const IndexView &ix, const QueryView &qv, int q, int e)
 {
     const float *o32 = ix.vec64 ? nullptr : ix.vec32 + (size_t)e * ix.Dp;
     const double *o64 = ix.vec64 ? ix.vec64 + (size_t)e * ix.D : nullptr;
-    double s = pw_sum64<MET>(o32, o64, qv.vec64 + (size_t)q * ix.D, 0, ix.D);
+    const double *q64 = qv.vec64 + (size_t)q * ix.D;
+    double s = pw_sum64<MET>(o32, o64, q64, 0, ix.D);
+    if (MET == kMetricAngular) return angular_finish(s, ix.vnorm64[e], qv.qnorm64[q], o32, o64, q64, ix.D);
     return MET == kMetricL1 ? s : __dsqrt_rn(s);
+}
+
+// |x| in numpy's order: sqrt of the pairwise sum of squares (data.py:81-84)
+__device__ __forceinline__ double norm64(const double *x, int D)
+{
+    return __dsqrt_rn(pw_sum64<kMetricSq>(nullptr, x, x, 0, D));
+}
+
+// fp32 angular screen: arccos of the fp32 cosine (error bound: ix.abs_eps)
+__device__ __forceinline__ float angular32(const float *__restrict__ a, const float *__restrict__ b, int Dp, float na,
+                                           float nb)
+{
+    if (nb == 0.f) return na == 0.f ? 0.f : 3.14159265f;
+    if (na == 0.f) return 3.14159265f;
+    float acc = 0.f;
+    const float4 *a4 = reinterpret_cast<const float4 *>(a);
+    const float4 *b4 = reinterpret_cast<const float4 *>(b);
+    for (int i = 0; i < (Dp >> 2); i++) {
+        const float4 x = __ldg(a4 + i), y = __ldg(b4 + i);
+        acc += (x.x * y.x + x.y * y.y) + (x.z * y.z + x.w * y.w);
+    }
+    return acosf(fminf(1.f, fmaxf(-1.f, acc / (na * nb))));
 }
 
 // screening distance query q -> table entry e (exact integer for edit)
@@ -405,6 +455,8 @@ __device__ __forceinline__ float dist32(const IndexView &ix, const QueryView &qv
 {
     if (MET == kMetricEdit) {
         return (float)edit_peq(qv.peq + qv.peq_off[q], qlen(qv, q), ix.str + ix.sword[e], ix.slen[e]);
+    } else if (MET == kMetricAngular) {
+        return angular32(ix.vec32 + (size_t)e * ix.Dp, qv.vec32 + (size_t)q * ix.Dp, ix.Dp, ix.vnorm32[e], qv.qnorm32[q]);
     } else {
         return vdist32<MET>(ix.vec32 + (size_t)e * ix.Dp, qv.vec32 + (size_t)q * ix.Dp, ix.Dp);
     }

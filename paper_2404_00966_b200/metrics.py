@@ -81,8 +81,6 @@ def pair_distances(metric, a, b):
                                         _lib.ptr(cb, _lib._i32p), _lib.ptr(ob, _lib._i64p),
                                         _lib.ptr(out, _lib._f64p), None))
         return out
-    if metric == ANGULAR:
-        raise MetricMismatchError("angular distance is not on the device path yet (SURVEY.md §8(f) f4)")
     A = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
     B = np.ascontiguousarray(np.asarray(b, dtype=np.float64))
     if A.shape != B.shape or A.ndim != 2:

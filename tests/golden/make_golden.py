@@ -246,6 +246,60 @@ def gen_trees():
     gen_tree("edit_dna", ds, 4, 7, q, rng.integers(0, 60, 16).astype(float), rng.integers(1, 10, 16), 20)
 
 
+def gen_angular():
+    """Angular fixtures (metrics.py:136-193), generated separately so the
+    fixtures above stay byte-identical: pair distances incl. the zero-vector
+    and exact-equality rules, and one 16-d clustered tree with zero vectors
+    and duplicates."""
+    rng = np.random.default_rng(4321)
+    out = {}
+    for D in (2, 3, 16, 33, 128):
+        a = f32(rng.normal(size=(60, D)))
+        b = f32(rng.normal(size=(60, D)))
+        b[:6] = a[:6]                          # identical -> 0
+        b[6:10] = a[6:10] * 2.0                # parallel -> ~0 (not identical)
+        a[10:12] = 0.0                         # zero vs non-zero -> pi
+        a[12:14] = 0.0
+        b[12:14] = 0.0                         # zero vs zero -> 0
+        b[14:16] = -a[14:16]                   # antiparallel -> pi
+        na = np.sqrt((a * a).sum(axis=1))
+        nb = np.sqrt((b * b).sum(axis=1))
+        out[f"ang_{D}_a"], out[f"ang_{D}_b"] = a, b
+        out[f"ang_{D}_d"] = metrics.angular_row_pairs(a, b, na, nb)
+    np.savez_compressed(os.path.join(HERE, "metrics_angular.npz"), **out)
+    # 16-d clustered tree with zero rows and duplicates
+    mat = f32(generate_clustered(1500, 16, 12, seed=31, spread=0.08) - 0.5)
+    mat[:5] = 0.0
+    mat[5:15] = mat[100:110]
+    ds = Dataset.from_vectors(mat, metrics.ANGULAR)
+    q = vector_queries(mat, 40, rng)
+    q[0] = np.zeros(16)
+    q[1] = mat[7].copy()
+    gen_tree("angular_16d", ds, 5, 8, q, rng.uniform(0.0, 0.6, 40), rng.integers(1, 30, 40), 40)
+
+
+def gen_snapshots():
+    """GTSI snapshots written by the reference's save_snapshot (io.py:60-89):
+    a words tree with tombstones and an angular / L2 vector tree."""
+    from metrictree.io import save_snapshot
+    strs = generate_sequences(800, seed=41, min_len=1, max_len=20, alphabet="abcdefghij") + ["", "é漢"]
+    ids = np.arange(len(strs), dtype=np.int64) * 3 + 5          # non-contiguous ids
+    tree = build(Dataset.from_strings(strs, metrics.EDIT, ids=ids), TreeConfig(node_capacity=6, seed=3))
+    for oid in ids[::17]:
+        tree.tombstone[tree.entry_pos_of_id(int(oid))] = 1
+    save_snapshot(tree, os.path.join(HERE, "snap_words.gtsi"))
+    mat = f32(generate_clustered(700, 12, 7, seed=42, spread=0.1))
+    tree = build(Dataset.from_vectors(mat, metrics.L2), TreeConfig(node_capacity=5, seed=4))
+    save_snapshot(tree, os.path.join(HERE, "snap_l2.gtsi"))
+
+
 if __name__ == "__main__":
-    gen_metrics()
-    gen_trees()
+    if "--angular" in sys.argv:
+        gen_angular()
+    elif "--snapshots" in sys.argv:
+        gen_snapshots()
+    else:
+        gen_metrics()
+        gen_trees()
+        gen_angular()
+        gen_snapshots()

@@ -375,3 +375,33 @@ def test_streaming_index_vectors_and_new_symbols():
     want = O.brute(od, oq, O.RANGE, radii=np.full(4, 3.0))
     c, i, d = csr(got)
     assert np.array_equal(i, want.ids) and np.array_equal(d, want.dis)
+
+
+@pytest.mark.parametrize("name", ["snap_words", "snap_l2"])
+def test_snapshot_loaded_index_matches_brute(name):
+    """A reference-written GTSI snapshot (tests/golden, io.py:60-89) drives the
+    device index directly (stored tree, tombstones included)."""
+    import os
+    tree = P.load_snapshot(os.path.join(os.path.dirname(__file__), "golden", name + ".gtsi"))
+    ds = tree.dataset
+    rng = np.random.default_rng(9)
+    dead = np.zeros(ds.n, np.uint8)
+    dead[tree.rows[tree.tombstone == 1]] = 1
+    if ds.metric == P.EDIT:
+        q = string_queries(ds.strings, 20, rng, "abcdefghijz")
+        od, oq = O.Payloads.from_strings(ds.strings, ids=ds.ids), O.Payloads.from_strings(q)
+        radii = rng.integers(0, 5, 20).astype(float)
+    else:
+        q = list(f32(ds.mat[rng.integers(0, ds.n, 20)] + rng.normal(0, 0.02, (20, ds.dim))))
+        od, oq = O.Payloads(O.L2, vec=ds.mat, ids=ds.ids), O.Payloads(O.L2, vec=np.array(q))
+        radii = rng.uniform(0.05, 0.4, 20)
+    ks = rng.integers(1, 25, 20)
+    eng = P.BatchSearcher(tree)
+    ans, _ = eng.range_batch(q, radii)
+    c, i, d = csr(ans)
+    want = O.brute(od, oq, O.RANGE, radii=radii, dead_rows=dead)
+    assert np.array_equal(i, want.ids) and np.array_equal(d, want.dis)
+    ans, _ = eng.knn_batch(q, ks)
+    c, i, d = csr(ans)
+    want = O.brute(od, oq, O.KNN, ks=ks, dead_rows=dead)
+    assert np.array_equal(i, want.ids) and np.array_equal(d, want.dis)
