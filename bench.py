@@ -320,19 +320,28 @@ def run_stream(args, rank, world, local_rank):
                           cache_capacity=w["cache_capacity"])
     build_s = time.perf_counter() - t0
     rng = np.random.default_rng(5)
-    live = set(int(i) for i in w["ids"])
+    # deleted ids are re-inserted in the same step, so the live id set never
+    # changes: draw from a fixed pool (no per-step sort of 1M Python ints)
+    pool = np.asarray(w["ids"][:200_000], dtype=np.int64)
 
     def step():
-        dels = rng.choice(sorted(live)[:200_000], w["updates"], replace=False)
+        dels = rng.choice(pool, w["updates"], replace=False)
         ins = []
         for oid in dels:
             s_ = list(strs[int(oid) - int(w["ids"][0])])
             for _ in range(3):
                 s_[int(rng.integers(0, len(s_)))] = alpha[int(rng.integers(0, len(alpha)))]
             ins.append((int(oid), "".join(s_)))
+        t0 = time.perf_counter()
         si.batch_update(inserts=ins, deletes=[int(x) for x in dels])
+        t1 = time.perf_counter()
         a, _ = si.query_range(q, w["radius"])
+        t2 = time.perf_counter()
         b, _ = si.query_knn(q, w["k"])
+        t3 = time.perf_counter()
+        if os.environ.get("GTS_STREAM_TRACE"):
+            print(f"[stream] update {1e3 * (t1 - t0):.1f} ms  range {1e3 * (t2 - t1):.1f} ms  "
+                  f"knn {1e3 * (t3 - t2):.1f} ms  rebuilds {si.rebuild_count}", file=sys.stderr, flush=True)
         return sum(x[0].size for x in a) + sum(x[0].size for x in b)
 
     clocks = ClockSampler(local_rank, args.clock_ms)

@@ -504,7 +504,9 @@ __global__ void __launch_bounds__(256, 4) k_leaf_edit(IndexView ix, QueryView qv
             if (k < leaf.size) pass = pruning ? fabsf(dis - lr.dqp) <= r : dis == dis;
             ver += __popc(__ballot_sync(kFull, pass));
             bool cand = pass && fabsf(mqf - lenf) <= r;
-            // the histogram bound never exceeds max(|q|, |o|): skip it when that fits
+            // the histogram bound never exceeds max(|q|, |o|): skip it when that
+            // fits.  (Issuing these loads before the lemma-1 work, for every
+            // length-passing entry, measured slower: 86.8 vs 84 ms on words.)
             if (cand && ix.ehist && fmaxf(mqf, lenf) > r) {
                 const uint4 h0 = __ldg(ix.ehist + 2 * e), h1 = __ldg(ix.ehist + 2 * e + 1);
                 cand = hist_lb(qh0, qh1, h0, h1, mq - (int)rec.y) <= ri;
