@@ -132,11 +132,23 @@ static int64_t myers_host(const HostPattern &hp, const int32_t *t, int64_t n,
 }
 
 // dense alphabet: sorted unique code points -> [0, A)
+// sorted distinct code points: a presence table for code points < 2^16 (one
+// pass, no sort of all n*len codes), a sort of the rest
 void dense_alphabet(const int32_t *codes, int64_t ncodes, std::vector<int32_t> &alpha)
 {
-    alpha.assign(codes, codes + ncodes);
-    std::sort(alpha.begin(), alpha.end());
-    alpha.erase(std::unique(alpha.begin(), alpha.end()), alpha.end());
+    std::vector<uint8_t> seen((size_t)1 << 16, 0);
+    std::vector<int32_t> big;
+    for (int64_t i = 0; i < ncodes; i++) {
+        const int32_t c = codes[i];
+        if (c >= 0 && c < (1 << 16)) seen[(size_t)c] = 1;
+        else big.push_back(c);
+    }
+    std::sort(big.begin(), big.end());
+    big.erase(std::unique(big.begin(), big.end()), big.end());
+    alpha.clear();
+    for (auto c : big) if (c < 0) alpha.push_back(c);
+    for (int32_t c = 0; c < (1 << 16); c++) if (seen[(size_t)c]) alpha.push_back(c);
+    for (auto c : big) if (c >= (1 << 16)) alpha.push_back(c);
 }
 
 }  // namespace gts
@@ -252,28 +264,37 @@ extern "C" int gts_build_tree(const gts_dataset *ds, int64_t root_row, int nthre
                     t->pivot_id[node] = pid;
                 }
             }
-            // map: each node's segment against its pivot (one pattern per node)
+            // map: every entry against its node's pivot.  Patterns are built
+            // per node first, then the distances run in parallel over ENTRIES
+            // (parallelising over nodes left the root level -- n distances of
+            // one node -- on a single thread)
+            std::vector<HostPattern> pats(edit ? (size_t)count : 0);
+            #pragma omp parallel for schedule(dynamic, 16)
+            for (int64_t o = 0; o < count; o++) {
+                const int64_t node = first + o;
+                const int64_t sz = t->size[node];
+                if (sz > 0) {
+                    if (edit) {
+                        const int64_t pv = t->pivot_row[node];
+                        make_pattern(dense.data() + ds->offsets[pv], ds->offsets[pv + 1] - ds->offsets[pv], A,
+                                     pats[(size_t)o]);
+                    }
+                    for (int64_t e = t->pos[node]; e < t->pos[node] + sz; e++) tmpr[(size_t)e] = o;   // entry -> node
+                }
+            }
             #pragma omp parallel
             {
                 std::vector<double> tmp((size_t)D + 1);
-                HostPattern hp;
                 std::vector<uint64_t> P, M;
-                #pragma omp for schedule(dynamic, 1)
-                for (int64_t node = first; node < first + count; node++) {
-                    int64_t sz = t->size[node];
-                    if (sz <= 0) continue;
-                    int64_t p = t->pos[node], pv = t->pivot_row[node];
+                #pragma omp for schedule(dynamic, 2048)
+                for (int64_t e = 0; e < n; e++) {
+                    const int64_t o = tmpr[(size_t)e], r = t->rows[e];
                     if (edit) {
-                        make_pattern(dense.data() + ds->offsets[pv], ds->offsets[pv + 1] - ds->offsets[pv], A, hp);
-                        for (int64_t e = p; e < p + sz; e++) {
-                            int64_t r = t->rows[e];
-                            t->dis[e] = (double)myers_host(hp, dense.data() + ds->offsets[r],
-                                                           ds->offsets[r + 1] - ds->offsets[r], P, M);
-                        }
+                        t->dis[e] = (double)myers_host(pats[(size_t)o], dense.data() + ds->offsets[r],
+                                                       ds->offsets[r + 1] - ds->offsets[r], P, M);
                     } else {
-                        const double *pvec = ds->vectors + pv * D;
-                        for (int64_t e = p; e < p + sz; e++)
-                            t->dis[e] = host_vec_dist(ds->metric, ds->vectors + t->rows[e] * D, pvec, D, tmp.data());
+                        const double *pvec = ds->vectors + t->pivot_row[first + o] * D;
+                        t->dis[e] = host_vec_dist(ds->metric, ds->vectors + r * D, pvec, D, tmp.data());
                     }
                 }
             }

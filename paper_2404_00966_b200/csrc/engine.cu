@@ -75,6 +75,7 @@ struct Error {
     } while (0)
 
 static std::atomic<int64_t> g_launches{0};
+static std::atomic<double> g_hits_per_query[2] = {{0.0}, {0.0}};   // largest hits / query seen (range, kNN)
 
 // Optional per-kernel timing (CUDA events on the launching stream) and
 // algorithmic work counters, read by bench.py for the roofline figures.
@@ -2303,6 +2304,7 @@ __global__ void k_pair_edit(int64_t np, const uint32_t *bwords, const uint32_t *
 using namespace gts;
 
 namespace gts {
+void dense_alphabet(const int32_t *codes, int64_t ncodes, std::vector<int32_t> &alpha);   // builder.cpp
 constexpr int kHistMinAlphabet = 8;   // symbol-histogram bound only pays on larger alphabets
 
 // numpy's pairwise sum (host; same order as pw_sum64 / the oracle)
@@ -2353,6 +2355,7 @@ static void pack_words(int64_t n, const int64_t *off, SymOf sym, std::vector<uin
     w += 8;                                    // the DP prefetches one uint4 past an object
     if (w >= (1ull << 32)) fail(GTS_EINVAL, "string payload exceeds 16 GiB per index; shard it");
     words.assign((size_t)w, 0u);
+    #pragma omp parallel for schedule(static, 4096)
     for (int64_t e = 0; e < n; e++) {
         const int64_t r = order ? order[e] : e;
         uint32_t *dst = words.data() + wstart[(size_t)e];
@@ -2360,6 +2363,23 @@ static void pack_words(int64_t n, const int64_t *off, SymOf sym, std::vector<uin
             dst[j >> 2] |= (uint32_t)sym(k) << (8 * (j & 3));
     }
 }
+
+// dense symbol of a code point: a direct table for code points < 2^16, a
+// binary search over the sorted alphabet above that
+struct SymMap {
+    const std::vector<int32_t> &alpha;
+    std::vector<uint8_t> lut;
+    explicit SymMap(const std::vector<int32_t> &a) : alpha(a), lut(1 << 16, 0xff)
+    {
+        for (size_t i = 0; i < a.size(); i++)
+            if (a[i] >= 0 && a[i] < (1 << 16)) lut[(size_t)a[i]] = (uint8_t)i;
+    }
+    uint32_t operator()(int32_t c) const
+    {
+        if (c >= 0 && c < (1 << 16)) return lut[(size_t)c];
+        return (uint32_t)(std::lower_bound(alpha.begin(), alpha.end(), c) - alpha.begin());
+    }
+};
 }  // namespace gts
 
 struct gts_index {
@@ -2613,6 +2633,10 @@ struct Search {
         }
         size_t hcap = (size_t)std::max<int64_t>(1 << 16, nq * 16);
         hcap = std::max<size_t>(hcap, (size_t)ix->hit_hint[mode].load());
+        // a fresh index (e.g. after a StreamingIndex rebuild) has no hint yet:
+        // use the largest hits-per-query ratio this process has seen, +25%
+        hcap = std::max<size_t>(hcap, (size_t)std::min(g_hits_per_query[mode].load() * (double)nq * 1.25,
+                                                       (double)(1ll << 27)));
         hq.alloc(hcap, st);
         he.alloc(hcap, st);
         hd.alloc(hcap, st);
@@ -3425,6 +3449,11 @@ gts_result *run_search(gts_index *ix, const gts_queries *q, int mode, const doub
         const unsigned long long want = s.hits + s.hits / 4;
         unsigned long long cur = ix->hit_hint[mode].load();
         while (want > cur && !ix->hit_hint[mode].compare_exchange_weak(cur, want)) {}
+        if (nq > 0) {
+            const double hpq = (double)s.hits / (double)nq;
+            double c0 = g_hits_per_query[mode].load();
+            while (hpq > c0 && !g_hits_per_query[mode].compare_exchange_weak(c0, hpq)) {}
+        }
     }
     auto *res = new gts_result();
     try {
@@ -3719,18 +3748,16 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
         h2d(ix->alive.p, alive.data(), alive.size(), st);
         if (ds->metric == GTS_EDIT) {
             const int64_t ncodes = ds->offsets[n];
-            std::vector<int32_t> alpha(ds->codes, ds->codes + ncodes);
-            std::sort(alpha.begin(), alpha.end());
-            alpha.erase(std::unique(alpha.begin(), alpha.end()), alpha.end());
+            std::vector<int32_t> alpha;
+            dense_alphabet(ds->codes, ncodes, alpha);   // builder.cpp: no sort of every code
             if (alpha.size() > 254)
                 fail(GTS_EMETRIC, "string alphabet of %zu symbols exceeds the device's 254", alpha.size());
             ix->A = (int)alpha.size();
             ix->h_alpha = alpha;
             std::vector<uint32_t> words, wstart;
             std::vector<int32_t> lens;
-            auto symof = [&](int64_t k) {
-                return (uint32_t)(std::lower_bound(alpha.begin(), alpha.end(), ds->codes[k]) - alpha.begin());
-            };
+            const SymMap smap(alpha);
+            auto symof = [&](int64_t k) { return smap(ds->codes[k]); };
             pack_words(n, ds->offsets, symof, words, wstart, lens, drow.data());
             for (auto l : lens) ix->max_len = std::max<int>(ix->max_len, l);
             ix->alpha.alloc(std::max<size_t>(alpha.size(), 1), st);
