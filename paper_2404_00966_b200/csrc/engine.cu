@@ -312,21 +312,9 @@ constexpr int kLeafWarps = 8;          // warps per block of k_leaf_edit
 constexpr int kRowChunk = 16;          // rows a warp claims per cursor bump
 
 // match masks too large to stage (A*W > kWarpPeqWords): read from global
-// block-steps myers_fixed executes for a W-block pattern over n symbols with
-// the band cut-off (profiling counters only)
-__device__ __forceinline__ unsigned long long banded_steps(int W, int n, int band)
+__device__ __noinline__ int edit_peq_global(const uint32_t *peq, int m, const uint32_t *t4, int n)
 {
-    if (W <= 1 || W > 4 || band >= 32 * W) return (unsigned long long)W * (unsigned long long)n;
-    unsigned long long s = 0;
-    const int nfull = n >> 2;
-    for (int jw = 0; jw < nfull; jw++) s += 4ull * (unsigned)min(W, (4 * jw + 4 + band - 1) / 32 + 1);
-    s += (unsigned long long)(n & 3) * (unsigned)min(W, (n + band - 1) / 32 + 1);
-    return s;
-}
-
-__device__ __noinline__ int edit_peq_global(const uint32_t *peq, int m, const uint32_t *t4, int n, int band)
-{
-    return edit_peq(peq, m, t4, n, band);
+    return edit_peq(peq, m, t4, n);
 }
 constexpr int kWarpPeqWords = 1024;     // per-warp staged match masks (A*W <= 1024)
 
@@ -444,10 +432,8 @@ __global__ void __launch_bounds__(256, 4) k_leaf_edit(IndexView ix, QueryView qv
             ea = qu[lane];
             const int na = ql[lane];
             const uint32_t *tA = ix.str + (uint32_t)qw[lane];
-            // band = the radius: hits (d <= r) come out exact, misses stay > r
-            const int band = r < 1e9f ? (int)r : (1 << 30);
-            da = staged ? edit_peq(peq_w, mq, tA, na, band) : edit_peq_global(peq_g, mq, tA, na, band);
-            if (work) steps += banded_steps(wq, na, band);   // block-steps actually executed
+            da = staged ? edit_peq(peq_w, mq, tA, na) : edit_peq_global(peq_g, mq, tA, na);
+            steps += (unsigned long long)wq * (unsigned long long)na;
         }
         const bool ha = va && (float)da <= r;
         emit(ha, ea, da);

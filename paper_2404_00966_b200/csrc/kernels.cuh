@@ -181,60 +181,14 @@ __device__ __forceinline__ uint32_t tload(const uint32_t *p)
     return __ldg(p);
 }
 
-// Ukkonen band cut-off for multi-block patterns: with a threshold `band`
-// (the radius), a cell (i, j) can be <= band only if i <= j + band, so block
-// b (rows 32b+1 .. 32b+32) joins the recurrence only from the column where
-// its first row can enter the band.  Until then it keeps its column-0 state
-// (vertical deltas +1), an upper bound of its true column, and every cell
-// whose true value is <= band only depends on in-band cells: distances
-// <= band come out exact, larger ones come out >= the true value (so > band).
-// Activation is per 4-symbol word, at the word's last column (early is safe).
-template <int W>
-__device__ __forceinline__ void myers_char_nb(const uint32_t *peq, uint32_t c, int nb, uint32_t (&P)[W],
-                                              uint32_t (&M)[W])
-{
-    uint32_t hp = 1u, hm = 0u;
-#pragma unroll
-    for (int b = 0; b < W; b++)
-        if (b < nb) myers_stepb(peq[c * W + b], P[b], M[b], hp, hm);
-}
-
 template <int W, bool SMEM = false>
-__device__ __forceinline__ int myers_fixed(const uint32_t *peq, int m, const uint32_t *__restrict__ t4, int n,
-                                           int band = 1 << 30)
+__device__ __forceinline__ int myers_fixed(const uint32_t *peq, int m, const uint32_t *__restrict__ t4, int n)
 {
     uint32_t P[W], M[W];
 #pragma unroll
     for (int b = 0; b < W; b++) { P[b] = ~0u; M[b] = 0u; }
     const int nfull = n >> 2;
     uint32_t w = tload<SMEM>(t4);
-    if (W > 1 && band < 32 * W) {
-        for (int jw = 0; jw < nfull; jw++) {
-            const uint32_t nxt = tload<SMEM>(t4 + jw + 1);
-            const int nb = min(W, (4 * jw + 4 + band - 1) / 32 + 1);
-            myers_char_nb<W>(peq, w & 0xffu, nb, P, M);
-            myers_char_nb<W>(peq, __byte_perm(w, 0u, 0x4441), nb, P, M);
-            myers_char_nb<W>(peq, __byte_perm(w, 0u, 0x4442), nb, P, M);
-            myers_char_nb<W>(peq, w >> 24, nb, P, M);
-            w = nxt;
-        }
-        const int rem = n & 3;
-        if (rem) {
-            const int nb = min(W, (n + band - 1) / 32 + 1);
-            myers_char_nb<W>(peq, w & 0xffu, nb, P, M);
-            if (rem > 1) myers_char_nb<W>(peq, (w >> 8) & 0xffu, nb, P, M);
-            if (rem > 2) myers_char_nb<W>(peq, (w >> 16) & 0xffu, nb, P, M);
-        }
-        const int wl = (m + 31) >> 5;
-        const uint32_t lastmask = (m & 31) ? ((1u << (m & 31)) - 1u) : ~0u;
-        int score = n;
-#pragma unroll
-        for (int b = 0; b < W; b++) {
-            const uint32_t mk = b < wl - 1 ? ~0u : (b == wl - 1 ? lastmask : 0u);
-            score += __popc(P[b] & mk) - __popc(M[b] & mk);
-        }
-        return score;
-    }
     for (int jw = 0; jw < nfull; jw++) {
         const uint32_t nxt = tload<SMEM>(t4 + jw + 1);
         myers_word<W>(peq, w, P, M);
@@ -370,17 +324,15 @@ __device__ __noinline__ int myers_generic(const uint32_t *peq, int W, int m, con
 }
 
 // edit distance between pattern (m symbols, masks peq) and text (n symbols)
-// band: distances above it may come out as any value > band (see
-// myers_fixed); the default computes every distance exactly
-__device__ __forceinline__ int edit_peq(const uint32_t *peq, int m, const uint32_t *t4, int n, int band = 1 << 30)
+__device__ __forceinline__ int edit_peq(const uint32_t *peq, int m, const uint32_t *t4, int n)
 {
     if (m == 0) return n;
     if (n == 0) return m;
     switch ((m + 31) >> 5) {
     case 1: return myers_fixed<1>(peq, m, t4, n);
-    case 2: return myers_fixed<2>(peq, m, t4, n, band);
-    case 3: return myers_fixed<3>(peq, m, t4, n, band);
-    case 4: return myers_fixed<4>(peq, m, t4, n, band);
+    case 2: return myers_fixed<2>(peq, m, t4, n);
+    case 3: return myers_fixed<3>(peq, m, t4, n);
+    case 4: return myers_fixed<4>(peq, m, t4, n);
     default: return myers_generic(peq, (m + 31) >> 5, m, t4, n);
     }
 }
