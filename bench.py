@@ -725,8 +725,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="words")
-    ap.add_argument("--n", type=int, default=0)
-    ap.add_argument("--nq", type=int, default=0)
+    # --objects / --queries: the same, for use behind torchrun (which claims "--n")
+    ap.add_argument("--n", "--objects", dest="n", type=int, default=0)
+    ap.add_argument("--nq", "--queries", dest="nq", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--clock-ms", type=int, default=200, help="nvidia-smi sampling interval in the timed region")
     args = ap.parse_args()
@@ -734,6 +735,10 @@ def main():
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    # diagnostics: GTS_BENCH_ONE_DEVICE=1 puts every rank on cuda:0 (exercises
+    # the N>1 merge path on a one-GPU box; use GTS_DIST_BACKEND=gloo with it)
+    if os.environ.get("GTS_BENCH_ONE_DEVICE") == "1":
+        local_rank = 0
     if args.impl == "reference":
         out = run_reference(args, rank, world)
     else:
@@ -742,7 +747,7 @@ def main():
             import torch.distributed as dist
             torch.cuda.set_device(local_rank)
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            dist.init_process_group("nccl")
+            dist.init_process_group(os.environ.get("GTS_DIST_BACKEND", "nccl"))
         out = (run_stream if args.workload == "dna_stream" else run_ours)(args, rank, world, local_rank)
         if world > 1:
             import torch.distributed as dist
