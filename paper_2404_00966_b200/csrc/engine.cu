@@ -1277,15 +1277,32 @@ __global__ void __launch_bounds__(256, 4) k_leafgroup_tile(IndexView ix, QueryVi
 // upper edge of the bin where the count reaches k bounds the k-th distance
 // from above (k distinct real objects lie at or below it), so the radius can
 // only shrink to values that still admit every true answer and its ties.
-constexpr int kFHist = 64;   // bins over [0, r0] (256 bins: fewer hits but a 4x longer scan per shrink, 12% slower on 128-d)
+constexpr int kFHist = 64;   // bins per query (256 bins: a 4x longer scan per shrink, 12% slower on 128-d)
+// Bins are focused on the top of [0, r0], where the k-th distance lies when the
+// probe radius r0 is good: bin 0 = [0, L), bins 1..63 split [L, r0] evenly,
+// L = kFHistLo * r0.  Upper edges: L + t * w.  A k-th distance below L still
+// yields the valid bound L, just a coarser one.
+constexpr double kFHistLo = 0.75;
+
+__device__ __forceinline__ int fhist_bin(double d, double R0)
+{
+    const double L = kFHistLo * R0, w = (R0 - L) / (kFHist - 1);
+    const double x = d * (1.0 + 1e-9);
+    if (x < L) return 0;
+    return min(kFHist - 1, 1 + (int)((x - L) / w));
+}
+
+__device__ __forceinline__ double fhist_edge(int t, double R0)
+{
+    const double L = kFHistLo * R0, w = (R0 - L) / (kFHist - 1);
+    return (L + (double)t * w) * (1.0 + 1.0 / (1 << 20));
+}
 
 __device__ __forceinline__ void fhist_add(unsigned *hist, const float *r0, int q, double d)
 {
     const double R0 = (double)r0[q];
     if (!(d <= R0) || !(R0 > 0.0) || isinf(R0)) return;
-    int b = (int)(d / R0 * kFHist);
-    b = min(max(b, 0), kFHist - 1);
-    atomicAdd(hist + (size_t)q * kFHist + b, 1u);
+    atomicAdd(hist + (size_t)q * kFHist + fhist_bin(d, R0), 1u);
 }
 
 __device__ __forceinline__ void fhist_shrink(unsigned *hist, const float *r0, const int32_t *ks, float *r32,
@@ -1306,7 +1323,7 @@ __device__ __forceinline__ void fhist_shrink(unsigned *hist, const float *r0, co
         }
     }
     if (t < 0) return;
-    const double R = (double)(t + 1) / kFHist * R0 * (1.0 + 1.0 / (1 << 20));
+    const double R = fhist_edge(t, R0);
     if (R < r64[q]) {
         atomicMin(reinterpret_cast<unsigned long long *>(r64 + q), (unsigned long long)__double_as_longlong(R));
         float Rf = (float)R;
@@ -1833,8 +1850,7 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
                         const float d2u = fmaf(cA, col.w, fmaf(-2.f, acc[jj], col.z)) + dq2 + kq +
                                           ldexpf(dq2 + qnorm * qnorm, -18);
                         const float dub = sqrtf(fmaxf(d2u, 0.f)) * (1.f + 1e-6f) + 1e-30f;
-                        const int b = min((int)(dub * hinv * (1.f + 1e-6f)), kFHist - 1);
-                        atomicAdd(fhist + (size_t)q * kFHist + b, 1u);
+                        atomicAdd(fhist + (size_t)q * kFHist + fhist_bin((double)dub * (1.0 + 1e-6), rf.w), 1u);
                     }
                     __threadfence();
                     fhist_shrink(fhist, r0, ks, r32, r64, q);

@@ -1,3 +1,12 @@
+"""Exactness simulation of the Ukkonen band cut-off for the multi-block
+bit-parallel edit distance (lower blocks join late, upper blocks retire with
+their deltas folded into a boundary value).  It checks, on random strings and
+radii, that distances <= band come out exact and larger ones stay > band.
+The cut-off was measured slower on B200 and is not in the product path
+(DESIGN.md §4); this script documents the derivation.
+
+    python tools/band_sim.py
+"""
 import random
 M32 = 0xffffffff
 def stepb(Eq, Pv, Mv, hp, hm):
