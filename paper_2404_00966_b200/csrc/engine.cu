@@ -1670,22 +1670,32 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
         const int4 d = s_item[i & 3];
         const int pos = s_pos[i & 3];
         const int N = max(16, (d.w + 15) & ~15);
-        uint8_t *A = sm + st * stage_bytes;
-        uint8_t *B = A + a_bytes;
+        const uint32_t A = tc::smem_u32(sm + st * stage_bytes);
+        const uint32_t B = A + (uint32_t)a_bytes;
         const int lc = c16 == 16 ? 4 : 3;
         const int c = tid & (c16 - 1), row0 = tid >> lc, rstep = kM2Threads >> lc;
-        const uint32_t aoff = (uint32_t)(c >> 3) * 16384u, boff = (uint32_t)(c >> 3) * (uint32_t)N * 128u;
+        // rstep is a multiple of 8, so every row this thread copies has the
+        // same (row & 7) and the same SW128 chunk permutation: the smem
+        // address advances by rstep rows, the source by rstep (B) or by a
+        // 32-bit row index (A) -- a few instructions per 16-byte copy.
+        const uint32_t sw = tc::sw128_offset(row0, c & 7);
+        const uint32_t dstep = (uint32_t)rstep * 128u;
         const int *rq = s_rq[i % 3];
-        for (int row = row0; row < 128; row += rstep) {
+        const char *qsrc = reinterpret_cast<const char *>(qv.qbf + c);
+        const uint32_t qstride = (uint32_t)c16 * 16u;
+        uint32_t adst = A + (uint32_t)(c >> 3) * 16384u + sw;
+#pragma unroll 4
+        for (int row = row0; row < 128; row += rstep, adst += dstep) {
             const int q = rq[row];
-            tc::cp_async16(tc::smem_u32(A + aoff + tc::sw128_offset(row, c & 7)), qv.qbf + (size_t)max(q, 0) * c16 + c,
-                           q >= 0 ? 16u : 0u);
+            tc::cp_async16(adst, qsrc + (size_t)((uint32_t)max(q, 0) * (uint64_t)qstride), q >= 0 ? 16u : 0u);
         }
-        for (int row = row0; row < N; row += rstep) {
-            const bool ok = row < d.w;
-            tc::cp_async16(tc::smem_u32(B + boff + tc::sw128_offset(row, c & 7)),
-                           ix.vcent + (size_t)(pos + (ok ? row : 0)) * c16 + c, ok ? 16u : 0u);
-        }
+        // rows size..N-1 (padding) are zero-filled (src-size 0); their source
+        // addresses stay inside vcent's 16-row zero tail
+        const uint4 *bsrc = ix.vcent + (size_t)(pos + row0) * c16 + c;
+        const size_t sstep = (size_t)rstep * c16;
+        uint32_t bdst = B + (uint32_t)(c >> 3) * (uint32_t)N * 128u + sw;
+        for (int row = row0; row < N; row += rstep, bdst += dstep, bsrc += sstep)
+            tc::cp_async16(bdst, bsrc, row < d.w ? 16u : 0u);
         tc::cp_async_commit();
     };
     auto mma = [&](int i) {
@@ -1762,12 +1772,12 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
             // margin 2^-18 (dq2 + qn^2 + R2) covers the fp32 rounding of the
             // rearranged sums; the band itself has a 2x margin.
             const float dq2 = dqp * dqp;
-            const float cA = ldexpf(dqp + qnorm, -7) + ldexpf(qnorm, -18) + 4.f * ix.abs_eps;
+            const float cA = ((dqp + qnorm) * 0x1p-7f) + ((qnorm) * 0x1p-18f) + 4.f * ix.abs_eps;
             const float kq = 8.f * ix.rel * dq2 + 4.f * ix.abs_eps * (dqp + ix.abs_eps);
             float T1, T2;
             auto set_r = [&](float rr) {
                 const float R2 = rr * rr * (1.f + 1e-6f);
-                const float mg = ldexpf(dq2 + qnorm * qnorm + R2, -18);
+                const float mg = ((dq2 + qnorm * qnorm + R2) * 0x1p-18f);
                 T1 = R2 + kq - dq2 + mg;
                 T2 = R2 - kq - dq2 - mg;
             };
@@ -1808,15 +1818,16 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
                 cm &= win;
                 fm &= cm;
                 if (!valid) cm = fm = 0, ver = 0;
-                // warp-aggregated append of the chunk's candidates
-                const unsigned nc = __popc(cm);
-                unsigned incl = nc;
-                for (int o = 1; o < 32; o <<= 1) {
-                    const unsigned v = __shfl_up_sync(kFull, incl, o);
-                    if (lane >= o) incl += v;
-                }
-                const unsigned wtot = __shfl_sync(kFull, incl, 31);
-                if (wtot) {
+                // warp-aggregated append of the chunk's candidates (most
+                // chunks have none: one vote skips the scan)
+                if (__any_sync(kFull, cm)) {
+                    const unsigned nc = __popc(cm);
+                    unsigned incl = nc;
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const unsigned v = __shfl_up_sync(kFull, incl, o);
+                        if (lane >= o) incl += v;
+                    }
+                    const unsigned wtot = __shfl_sync(kFull, incl, 31);
                     unsigned long long base = 0;
                     if (lane == 31) base = atomicAdd(cb.counter, (unsigned long long)wtot);
                     base = __shfl_sync(kFull, base, 31) + (incl - nc);
@@ -1829,7 +1840,7 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
                             cb.e[base] = pos + c0 + jj;
                             // d^2 lower bound, rounded down a little
                             cb.lb[base] = (fmaf(-cA, col.w, fmaf(-2.f, acc[jj], col.y)) + dq2 - kq) * (1.f - 1e-5f) -
-                                          ldexpf(dq2 + qnorm * qnorm, -18);
+                                          ((dq2 + qnorm * qnorm) * 0x1p-18f);
                         }
                         base++;
                     }
@@ -1842,7 +1853,7 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
                         if (!((fm >> jj) & 1u)) continue;
                         const float4 col = s_col[sl][c0 + jj];
                         const float d2u = fmaf(cA, col.w, fmaf(-2.f, acc[jj], col.z)) + dq2 + kq +
-                                          ldexpf(dq2 + qnorm * qnorm, -18);
+                                          ((dq2 + qnorm * qnorm) * 0x1p-18f);
                         const float dub = sqrtf(fmaxf(d2u, 0.f)) * (1.f + 1e-6f) + 1e-30f;
                         const int b = min((int)(dub * hinv * (1.f + 1e-6f)), kFHist - 1);
                         atomicAdd(fhist + (size_t)q * kFHist + b, 1u);
@@ -3864,8 +3875,12 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
                         se[(size_t)e] = (float)acc;
                     }
                 }
-                ix->vcent.alloc(vc.size() / 8, st);
+                // + 16 zero rows: k_leafgroup_mma2 pads a leaf to a multiple of
+                // 16 rows and forms (never dereferences) those rows' addresses
+                const size_t tail = (size_t)16 * ix->Dk / 8;
+                ix->vcent.alloc(vc.size() / 8 + tail, st);
                 CK(cudaMemcpyAsync(ix->vcent.p, vc.data(), vc.size() * sizeof(__nv_bfloat16), cudaMemcpyHostToDevice, st));
+                CK(cudaMemsetAsync(ix->vcent.p + vc.size() / 8, 0, tail * sizeof(uint4), st));
                 ix->vse.alloc((size_t)n, st);
                 h2d(ix->vse.p, se.data(), (size_t)n, st);
                 CK(cudaStreamSynchronize(st));
