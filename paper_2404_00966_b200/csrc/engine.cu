@@ -2202,6 +2202,203 @@ __global__ void __launch_bounds__(256) k_probe(IndexView ix, QueryView qv, int n
     }
 }
 
+// Node-major kNN probe for L1 / L2 (k_probe_path -> sort -> k_probe_dist ->
+// k_probe_select): the same candidates (the ring path's node and its
+// next-nearest ring) and the same radius rule as k_probe<MET>, but each
+// candidate node is staged once per 64 queries that probe it instead of
+// once per query (k_probe read ~256 GB from L2 for 100k 128-d queries).
+constexpr int kPT = 64;    // query rows x entries per tile
+constexpr int kPD = 128;   // dimensions staged per pass
+
+template <int MET>
+__global__ void __launch_bounds__(256) k_probe_path(IndexView ix, QueryView qv, int q0, int nq, const int32_t *ks,
+                                                   uint32_t *keys, int32_t *vals)
+{
+    const int lane = lane_id();
+    const int qi = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (qi >= nq) return;
+    const int q = q0 + qi;
+    const int nc = ix.nc;
+    const int target = min(max(ks[q], kProbeTarget), kProbeCand);
+    int node = 1, anc = 1, anc2 = -1;
+    for (int lvl = 1; lvl < ix.levels; lvl++) {
+        const NodeRec self = ix.node[node];
+        const float dp = self.piv >= 0 ? dist32<MET>(ix, qv, q, self.piv) : 0.f;
+        float g1 = FLT_MAX, g2 = FLT_MAX;
+        int j1 = -1, j2 = -1;
+        for (int j = lane; j < nc; j += 32) {
+            const NodeRec c = ix.node[(node - 1) * nc + 2 + j];
+            if (c.size <= 0) continue;
+            const float g = fmaxf(fmaxf(c.mn - dp, dp - c.mx), 0.f);
+            if (j1 < 0 || g < g1) { g2 = g1; j2 = j1; g1 = g; j1 = j; }
+            else if (j2 < 0 || g < g2) { g2 = g; j2 = j; }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const float og1 = __shfl_xor_sync(kFull, g1, o), og2 = __shfl_xor_sync(kFull, g2, o);
+            const int oj1 = __shfl_xor_sync(kFull, j1, o), oj2 = __shfl_xor_sync(kFull, j2, o);
+            const bool a_first = oj1 < 0 || (j1 >= 0 && (g1 < og1 || (g1 == og1 && j1 < oj1)));
+            const float fg = a_first ? g1 : og1;
+            const int fj = a_first ? j1 : oj1;
+            float sg = a_first ? og1 : g1;
+            int sj = a_first ? oj1 : j1;
+            if (j2 >= 0 && (sj < 0 || g2 < sg || (g2 == sg && j2 < sj))) { sg = g2; sj = j2; }
+            if (oj2 >= 0 && (sj < 0 || og2 < sg || (og2 == sg && oj2 < sj))) { sg = og2; sj = oj2; }
+            g1 = fg; j1 = fj; g2 = sg; j2 = sj;
+        }
+        const int child = (node - 1) * nc + 2 + (j1 >= 0 ? j1 : 0);
+        if (ix.node[child].size >= target) {   // deepest path node holding >= target entries
+            anc = child;
+            anc2 = j2 >= 0 ? (node - 1) * nc + 2 + j2 : -1;
+        }
+        node = child;
+    }
+    if (lane == 0) {
+        keys[2 * qi] = (uint32_t)anc;
+        vals[2 * qi] = 2 * qi;
+        keys[2 * qi + 1] = anc2 >= 0 ? (uint32_t)anc2 : 0xffffffffu;   // sorts last, skipped
+        vals[2 * qi + 1] = 2 * qi + 1;
+    }
+}
+
+// Distances of 64 sorted (query, node) rows to their node's entries, 4x4
+// register tiles; out[qi][slot], slot = entry index (+ size of the first node
+// for the second one), +inf for tombstones, capped at kProbeCand per query.
+template <int MET>
+__global__ void __launch_bounds__(256) k_probe_dist(IndexView ix, QueryView qv, int q0, const uint32_t *skeys,
+                                                   const int32_t *svals, int nrows, const uint32_t *keys, float *out)
+{
+    extern __shared__ float4 pd_smem4[];
+    float *qs = reinterpret_cast<float *>(pd_smem4);   // [kPT][kPD + 4]
+    float *es = qs + kPT * (kPD + 4);                  // [kPT][kPD + 4]
+    __shared__ int s_node[kPT], s_q[kPT], s_base[kPT];
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int rbase = blockIdx.x * kPT;
+    if (tid < kPT) {
+        const int r = rbase + tid;
+        int node = -1, qi = -1, base = 0;
+        if (r < nrows && skeys[r] != 0xffffffffu) {
+            node = (int)skeys[r];
+            const int v = svals[r];
+            qi = v >> 1;
+            if (v & 1) base = ix.node[keys[2 * qi]].size;
+        }
+        s_node[tid] = node;
+        s_q[tid] = qi;
+        s_base[tid] = base;
+    }
+    __syncthreads();
+    const int S = kPD + 4;
+    int r0 = 0;
+    while (r0 < kPT && s_node[r0] >= 0) {
+        const int node = s_node[r0];
+        int r1 = r0 + 1;
+        while (r1 < kPT && s_node[r1] == node) r1++;
+        const int pos = ix.npos[node], size = ix.node[node].size;
+        for (int e0 = 0; e0 < size; e0 += kPT) {
+            float acc[4][4];
+#pragma unroll
+            for (int a = 0; a < 4; a++)
+#pragma unroll
+                for (int b = 0; b < 4; b++) acc[a][b] = 0.f;
+            for (int d0 = 0; d0 < ix.Dp; d0 += kPD) {
+                const int dl = min(kPD, ix.Dp - d0);   // multiple of 4
+                const int c4 = dl >> 2;
+                for (int t = tid; t < kPT * c4; t += blockDim.x) {
+                    const int i = t / c4, c = t - i * c4;
+                    const int row = r0 + i;
+                    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (row < r1)
+                        v = __ldg(reinterpret_cast<const float4 *>(qv.vec32 + (size_t)(q0 + s_q[row]) * ix.Dp + d0) + c);
+                    *reinterpret_cast<float4 *>(qs + i * S + 4 * c) = v;
+                    float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (e0 + i < size)
+                        w = __ldg(reinterpret_cast<const float4 *>(ix.vec32 + (size_t)(pos + e0 + i) * ix.Dp + d0) + c);
+                    *reinterpret_cast<float4 *>(es + i * S + 4 * c) = w;
+                }
+                __syncthreads();
+                // rows ty + 16a of this run (relative to r0), entries tx + 16b
+                for (int c = 0; c < dl; c += 4) {
+                    float4 x[4], y[4];
+#pragma unroll
+                    for (int a = 0; a < 4; a++) x[a] = *reinterpret_cast<const float4 *>(qs + (ty + 16 * a) * S + c);
+#pragma unroll
+                    for (int b = 0; b < 4; b++) y[b] = *reinterpret_cast<const float4 *>(es + (tx + 16 * b) * S + c);
+#pragma unroll
+                    for (int a = 0; a < 4; a++)
+#pragma unroll
+                        for (int b = 0; b < 4; b++) {
+                            const float u0 = x[a].x - y[b].x, u1 = x[a].y - y[b].y;
+                            const float u2 = x[a].z - y[b].z, u3 = x[a].w - y[b].w;
+                            if (MET == kMetricL1)
+                                acc[a][b] += (fabsf(u0) + fabsf(u1)) + (fabsf(u2) + fabsf(u3));
+                            else
+                                acc[a][b] += (u0 * u0 + u1 * u1) + (u2 * u2 + u3 * u3);
+                        }
+                }
+                __syncthreads();
+            }
+#pragma unroll
+            for (int a = 0; a < 4; a++) {
+                const int row = r0 + ty + 16 * a;
+                if (row >= r1) continue;
+                const int qi = s_q[row];
+#pragma unroll
+                for (int b = 0; b < 4; b++) {
+                    const int e = e0 + tx + 16 * b;
+                    const int slot = s_base[row] + e;
+                    if (e >= size || slot >= kProbeCand) continue;
+                    const float d = MET == kMetricL1 ? acc[a][b] : sqrtf(acc[a][b]);
+                    out[(size_t)qi * kProbeCand + slot] = is_alive(ix.alive, pos + e) ? d : INFINITY;
+                }
+            }
+        }
+        r0 = r1;
+    }
+}
+
+// k-th smallest candidate distance per query -> radius (as k_probe)
+template <int MET>
+__global__ void __launch_bounds__(256) k_probe_select(IndexView ix, int q0, int nq, const int32_t *ks, const uint32_t *keys,
+                                                     const float *dist, float *r32, double *r64)
+{
+    __shared__ uint32_t cand[kProbeCand];
+    __shared__ unsigned hist[256];
+    __shared__ int sh[4];
+    __shared__ int s_live;
+    for (int qi = blockIdx.x; qi < nq; qi += gridDim.x) {
+        const int q = q0 + qi;
+        if (threadIdx.x == 0) s_live = 0;
+        __syncthreads();
+        const uint32_t a2 = keys[2 * qi + 1];
+        const int n = min(ix.node[keys[2 * qi]].size + (a2 != 0xffffffffu ? ix.node[a2].size : 0), kProbeCand);
+        const float *src = dist + (size_t)qi * kProbeCand;
+        int live = 0;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const float d = src[i];
+            cand[i] = __float_as_uint(d);
+            live += d < INFINITY;
+        }
+        if (live) atomicAdd(&s_live, live);
+        __syncthreads();
+        const int k = ks[q];
+        const int nl = s_live;
+        __syncthreads();
+        if (nl >= k && k >= 1) {
+            const uint32_t kth = block_kth(cand, n, k, hist, sh);
+            if (threadIdx.x == 0) {
+                float t = __uint_as_float(kth);
+                t = t + slack(ix, t, 0.f);   // d64 <= d32 + slack
+                r32[q] = t;
+                r64[q] = (double)t;
+            }
+        } else if (threadIdx.x == 0) {
+            r32[q] = INFINITY;
+            r64[q] = INFINITY;
+        }
+        __syncthreads();
+    }
+}
+
 // query preparation --------------------------------------------------------
 
 __global__ void k_map_symbols(const int32_t *codes, int64_t n, const int32_t *alpha, int A, uint8_t *out)
@@ -3163,10 +3360,49 @@ struct Search {
     template <int MET>
     void launch_probe()
     {
+        // node-major for wide vectors; low-dimensional probes are cheap per query
+        if ((MET == kMetricL1 || MET == kMetricL2) && ix->D >= 16 && std::getenv("GTS_PROBE_PERQUERY") == nullptr) {
+            launch_probe_grouped<MET>();
+            return;
+        }
         timed("k_probe", [&] {
             k_probe<MET><<<grid_for(nq, 1, 148u * 16u), 256, 0, st>>>(iv, qv, (int)nq, ks.p, r32.p, r64.p);
         });
         LAUNCH_CHECK();
+    }
+
+    template <int MET>
+    void launch_probe_grouped()
+    {
+        const int64_t qchunk = std::min<int64_t>(nq, 1 << 17);   // <= 4 GiB of candidate distances
+        const size_t pd_smem = (size_t)2 * kPT * (kPD + 4) * sizeof(float);
+        static bool attr = false;
+        if (!attr) {
+            CK(cudaFuncSetAttribute(k_probe_dist<kMetricL1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pd_smem));
+            CK(cudaFuncSetAttribute(k_probe_dist<kMetricL2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pd_smem));
+            attr = true;
+        }
+        DBuf<uint32_t> keys((size_t)2 * qchunk, st), skeys((size_t)2 * qchunk, st);
+        DBuf<int32_t> vals((size_t)2 * qchunk, st), svals((size_t)2 * qchunk, st);
+        DBuf<float> dist((size_t)qchunk * kProbeCand, st);
+        size_t tmp_bytes = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys.p, skeys.p, vals.p, svals.p, (int)(2 * qchunk), 0, 32, st);
+        DBuf<uint8_t> tmp(tmp_bytes, st);
+        for (int64_t q0 = 0; q0 < nq; q0 += qchunk) {
+            const int nqc = (int)std::min<int64_t>(qchunk, nq - q0);
+            const int nrows = 2 * nqc;
+            timed("k_probe", [&] {
+                k_probe_path<MET><<<grid_for((int64_t)nqc * 32, 256), 256, 0, st>>>(iv, qv, (int)q0, nqc, ks.p, keys.p,
+                                                                                  vals.p);
+                CK(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, keys.p, skeys.p, vals.p, svals.p, nrows, 0, 32, st));
+                k_probe_dist<MET><<<(unsigned)((nrows + kPT - 1) / kPT), 256, pd_smem, st>>>(
+                    iv, qv, (int)q0, skeys.p, svals.p, nrows, keys.p, dist.p);
+                k_probe_select<MET><<<grid_for(nqc, 1, 148u * 16u), 256, 0, st>>>(iv, (int)q0, nqc, ks.p, keys.p, dist.p,
+                                                                                  r32.p, r64.p);
+            });
+            LAUNCH_CHECK();
+            g_launches += 2;   // path, dist, select (+ the CUB sort)
+        }
     }
 
     void run()
