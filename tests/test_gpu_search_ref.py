@@ -146,3 +146,35 @@ def test_tombstoned_entries_never_returned():
     assert_matches(answers, O.brute(od, oq, O.KNN, ks=np.full(15, 6), dead_rows=dead_rows))
     for ids, _ in answers:
         assert not (set(ids.tolist()) & dead)
+
+
+@pytest.mark.parametrize("probe", ["node_major", "per_query"])
+@pytest.mark.parametrize("metric,dim,n,nc", [(P.L2, 64, 20000, 4), (P.L1, 32, 6000, 6)])
+def test_knn_probe_paths_exact_with_tombstones(probe, metric, dim, n, nc, monkeypatch):
+    """kNN radius probe: node-major (k_probe_path/dist/select, D >= 16) and
+    per-query (k_probe) both give exact answers, with tombstoned entries in
+    the probed nodes and k from 1 to beyond a node's size."""
+    if probe == "per_query":
+        monkeypatch.setenv("GTS_PROBE_PERQUERY", "1")
+    else:
+        monkeypatch.delenv("GTS_PROBE_PERQUERY", raising=False)
+    rng = np.random.default_rng(37)
+    # (20000, 4): the probe node sits two levels down (5000 -> 1250 entries)
+    # and takes its sibling ring; (6000, 6): level-1 nodes hold < 1024, so
+    # the root itself is probed
+    mat = P.generate_clustered(n, dim, 12, seed=38, spread=0.05)
+    ds = P.Dataset.from_vectors(mat, metric)
+    tree = P.build(ds, P.TreeConfig(node_capacity=nc, seed=2))
+    dead = rng.choice(n, n // 7, replace=False)
+    for obj in dead:
+        tree.tombstone[tree.entry_pos_of_id(int(obj))] = 1
+    dead_rows = np.zeros(n, np.uint8)
+    dead_rows[dead] = 1
+    qi = rng.integers(0, n, 40)
+    queries = [mat[i] + rng.normal(0, 0.01, dim) for i in qi]
+    od = O.Payloads({P.L1: 1, P.L2: 2}[metric], vec=mat)
+    oq = O.Payloads({P.L1: 1, P.L2: 2}[metric], vec=np.array(queries))
+    eng = P.BatchSearcher(tree)
+    for k in (1, 10, 100, 1500):
+        got, _ = eng.knn_batch(queries, k)
+        assert_matches(got, O.brute(od, oq, O.KNN, ks=np.full(40, k), dead_rows=dead_rows))
