@@ -130,6 +130,21 @@ def make_workload(name, rank, args):
     return w
 
 
+def bench_config(args, w, world):
+    """The `config` object -- identical in both arms (same workload, sizes,
+    tree geometry and budget)."""
+    from oracle import oracle as O   # tree_height only (pure arithmetic, tree.py:60-78)
+    _, split = O.tree_height(w["n"], 20)
+    return {
+        "workload": f"{args.workload} (BASELINE.json configs[{w['config_index']}])",
+        "n_per_gpu": w["n"], "nq": w["nq"], "radius": w["radius"], "k": w["k"], "node_capacity": 20,
+        "levels": split + 1, "memory_units": 1 << 24,
+        "l2_policy": "index payload+tables exceed nothing: words (~25 MB) stay L2-resident by design; "
+                     "no flush between steps (device-resident index is the operating point)",
+        "parallelism": f"dp{world} (one shard per GPU)",
+    }
+
+
 # ---------------------------------------------------------------------------
 # clocks
 # ---------------------------------------------------------------------------
@@ -299,6 +314,19 @@ class Engine:
         for h in hs:
             self.L.gts_result_free(h)
 
+    def fetch(self, h, stream):
+        """Host copy of a result CSR: (offsets, ids, dis)."""
+        nq, tot = self.info(h)
+        off = np.zeros(nq + 1, np.int64)
+        ids = np.zeros(max(tot, 1), np.int64)
+        dis = np.zeros(max(tot, 1), np.float64)
+        p = self._lib.ptr
+        self._lib.check(self.L.gts_result_copy(h, p(off, self._lib._i64p), p(ids, self._lib._i64p),
+                                               p(dis, self._lib._f64p), None, None, C.c_void_p(stream)))
+        import torch
+        torch.cuda.synchronize()
+        return off, ids[:tot], dis[:tot]
+
 
 def run_stream(args, rank, world, local_rank):
     """configs[3]: StreamingIndex (the user-facing API) on 1M DNA strings; a
@@ -421,6 +449,8 @@ def run_ours(args, rank, world, local_rank):
     hs = eng.step_device(sp)
     torch.cuda.synchronize()
     totals = [eng.info(h)[1] for h in hs]
+    # the answers of the timed batch (range, kNN), kept for the parity check
+    gpu_answers = [eng.fetch(h, sp) for h in hs]
     eng.free(hs)
 
     # timed region (value): inputs resident in HBM.  Each step ends with a
@@ -490,14 +520,7 @@ def run_ours(args, rank, world, local_rank):
         "vs_baseline": None,
         "dtype": "u8 symbols / int32 bit-parallel DP" if eng.edit else "f32 screen + f64 exact recheck",
         "data": "synthetic",
-        "config": {
-            "workload": f"{args.workload} (BASELINE.json configs[{w['config_index']}])",
-            "n_per_gpu": w["n"], "nq": nq, "radius": w["radius"], "k": w["k"], "node_capacity": 20,
-            "levels": eng.levels, "memory_units": 1 << 24,
-            "l2_policy": "index payload+tables exceed nothing: words (~25 MB) stay L2-resident by design; "
-                         "no flush between steps (device-resident index is the operating point)",
-            "parallelism": f"dp{world} (one shard per GPU)",
-        },
+        "config": bench_config(args, w, world),
         "range_answers_per_step": totals[0],
         "knn_answers_per_step": totals[1],
         "distance_evals_per_s": round(work["pairs"] / (step_ms_prof / 1e3), 1) if step_ms_prof else None,
@@ -511,7 +534,7 @@ def run_ours(args, rank, world, local_rank):
     }
     out["roofline"] = roofline(eng, prof, kver, step_ms_prof)
     if world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(w, args)
+        out["cpu_baseline"], out["parity"] = cpu_baseline(w, args, gpu_answers)
     return out
 
 
@@ -661,25 +684,86 @@ def oracle_queries(O, w, idx):
 
 
 def time_oracle(O, data, tree, w, n_range, n_knn, threads, seed=0):
+    """Time the oracle port's BatchSearcher on a sample of the batch; returns
+    {mode: (count, seconds, query indices, oracle Result)}."""
     rng = np.random.default_rng(seed)
     out = {}
     for mode, cnt, name in ((O.RANGE, n_range, "range"), (O.KNN, n_knn, "knn")):
-        idx = rng.choice(w["nq"], size=min(cnt, w["nq"]), replace=False)
+        idx = np.sort(rng.choice(w["nq"], size=min(cnt, w["nq"]), replace=False))
         qs = oracle_queries(O, w, idx)
         t0 = time.perf_counter()
-        O.search(tree, data, qs, mode, radii=np.full(len(idx), w["radius"]), ks=np.full(len(idx), w["k"]),
-                 threads=threads)
-        out[name] = (len(idx), time.perf_counter() - t0)
+        res = O.search(tree, data, qs, mode, radii=np.full(len(idx), w["radius"]), ks=np.full(len(idx), w["k"]),
+                       threads=threads)
+        out[name] = (len(idx), time.perf_counter() - t0, idx, res)
     return out
 
 
-def cpu_baseline(w, args):
+def parity_check(O, data, w, t, gpu_answers, threads):
+    """Compare the GPU answers of the timed batch with the oracle on the
+    sampled queries: range = the reference engine's id and
+    distance lists exactly; kNN = the reference engine's distance list exactly
+    and the canonical brute-force (distance, id) top-k (oracle.brute_knn,
+    oracle.py:30-36) exactly.  Float distances are compared bit for bit; the
+    north-star tolerance (ids within 1e-5 relative of r / the k-th distance,
+    distances within 1e-5 relative) is reported separately as `tolerated`."""
+    checked = mism = tol = 0
+    worst = []
+    for name, gi in (("range", 0), ("knn", 1)):
+        if name not in t:
+            continue
+        _, _, idx, ref = t[name]
+        off, ids, dis = gpu_answers[gi]
+        brute = None
+        if name == "knn":
+            brute = O.brute(data, oracle_queries(O, w, idx), O.KNN, ks=np.full(len(idx), w["k"]), threads=threads)
+        ref_ans = ref.answers()
+        br_ans = brute.answers() if brute is not None else None
+        for j, q in enumerate(idx):
+            g_ids, g_dis = ids[off[q]:off[q + 1]], dis[off[q]:off[q + 1]]
+            r_ids, r_dis = ref_ans[j]
+            checked += 1
+            if name == "range":
+                ok = np.array_equal(g_ids, r_ids) and np.array_equal(g_dis, r_dis)
+                bound = w["radius"]
+            else:
+                b_ids, b_dis = br_ans[j]
+                ok = (np.array_equal(g_dis, r_dis) and np.array_equal(g_ids, b_ids)
+                      and np.array_equal(g_dis, b_dis))
+                bound = float(r_dis[-1]) if r_dis.size else 0.0
+            if ok:
+                continue
+            # north-star float tolerance: ids may differ only within 1e-5 relative
+            # of the radius / k-th distance, distances within 1e-5 relative
+            within = False
+            if w["metric"] != "edit" and g_ids.size and r_ids.size:
+                band = 1e-5 * max(bound, 1e-30)
+                gd = dict(zip(g_ids.tolist(), g_dis.tolist()))
+                rd = dict(zip(r_ids.tolist(), r_dis.tolist()))
+                sym = set(gd) ^ set(rd)
+                within = all(abs((gd.get(i, rd.get(i))) - bound) <= band for i in sym) and all(
+                    abs(gd[i] - rd[i]) <= 1e-5 * max(abs(rd[i]), 1e-30) for i in set(gd) & set(rd))
+            if within:
+                tol += 1
+            else:
+                mism += 1
+                if len(worst) < 4:
+                    worst.append({"mode": name, "query": int(q), "gpu": [g_ids[:8].tolist(), g_dis[:8].tolist()],
+                                  "oracle": [r_ids[:8].tolist(), r_dis[:8].tolist()]})
+    out = {"checked": checked, "mismatches": mism, "tolerated": tol,
+           "against": "oracle port BatchSearcher (range ids+distances, kNN distances) + oracle brute force "
+                      "(kNN canonical (distance, id) top-k), on the cpu_baseline sample of the timed batch"}
+    if worst:
+        out["first_mismatches"] = worst
+    return out
+
+
+def cpu_baseline(w, args, gpu_answers=None):
     O, data, tree, build_s = oracle_setup(w)
     threads = os.cpu_count() or 1
     n_range, n_knn = (256, 64) if w["metric"] == "edit" else ((1000, 1000) if w["n"] <= 100_000 else (32, 32))
     t = time_oracle(O, data, tree, w, n_range, n_knn, threads)
     per_q = (t["range"][1] / t["range"][0] + t["knn"][1] / t["knn"][0]) / 2
-    return {
+    cb = {
         "value": round(1.0 / per_q, 3), "unit": "queries/s", "cores": threads, "kind": "port",
         "sample": f"{t['range'][0]} range + {t['knn'][0]} kNN queries of the same batch on the same 1-shard index "
                   f"(oracle/gts_oracle.c = restated reference BatchSearcher, {threads} threads over query slices); "
@@ -687,6 +771,8 @@ def cpu_baseline(w, args):
                   f"value = 1 / mean per-query time at the bench's 1:1 range:kNN mix",
         "oracle_build_s": round(build_s, 2),
     }
+    par = parity_check(O, data, w, t, gpu_answers, threads) if gpu_answers is not None else None
+    return cb, par
 
 
 def run_reference(args, rank, world):
@@ -710,8 +796,7 @@ def run_reference(args, rank, world):
         "impl": "reference", "metric": "range+kNN queries/sec", "value": round(v, 3), "unit": "queries/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot_t / args.steps * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64/int64 (CPU)",
-        "data": "synthetic", "config": {"workload": f"{args.workload} (BASELINE.json configs[{w['config_index']}])",
-                                        "n_per_gpu": w["n"], "nq": w["nq"], "radius": w["radius"], "k": w["k"]},
+        "data": "synthetic", "config": bench_config(args, w, world),
         "cpu_baseline": {"value": round(v, 3), "unit": "queries/s", "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": round(v, 3), "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "oracle_build_s": round(build_s, 2),
@@ -754,6 +839,11 @@ def main():
             dist.destroy_process_group()
     if out is not None:
         print(json.dumps(out), flush=True)
+        par = out.get("parity")
+        if par and par.get("mismatches"):
+            sys.stderr.write(f"PARITY FAILURE: {par['mismatches']} of {par['checked']} sampled queries differ "
+                             "from the oracle\n")
+            sys.exit(3)
 
 
 if __name__ == "__main__":
