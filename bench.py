@@ -94,39 +94,59 @@ def string_queries(codes, off, nq, seed, alphabet):
     return qcodes.astype(np.int32), qoff
 
 
-def make_workload(name, rank, args):
+def make_workload(name, rank, args, world=1, keep_full=False):
+    """Synthetic data of the named shape.  The collection (n objects, seed 12)
+    and the query batch (seed 13) do not depend on the rank: with N ranks the
+    collection is split into N contiguous id ranges (one shard per GPU,
+    strong scaling over one fixed collection) and every rank holds the same
+    replicated batch.  w["n"] is this rank's shard size, w["n_total"] the
+    collection's; keep_full keeps the whole collection (rank 0's parity
+    check at N > 1)."""
     w = dict(WORKLOADS[name])
     if args.n:
         w["n"] = args.n
     if args.nq:
         w["nq"] = args.nq
-    seed = 12 + 1000 * rank
+    n_total = w["n"]
+    lo, hi = n_total * rank // world, n_total * (rank + 1) // world
+    seed = 12
+    full = {}
     if w["metric"] == "edit":
-        codes, off = gen_strings(w["n"], seed, w["min_len"], w["max_len"], w["alphabet"])
-        qcodes, qoff = string_queries(codes, off, w["nq"], 13, w["alphabet"] if True else None)
-        w.update(codes=codes, off=off, qcodes=qcodes, qoff=qoff)
+        codes, off = gen_strings(n_total, seed, w["min_len"], w["max_len"], w["alphabet"])
+        qcodes, qoff = string_queries(codes, off, w["nq"], 13, w["alphabet"])
+        if keep_full:
+            full = dict(codes=codes, off=off)
+        w.update(codes=codes[off[lo]:off[hi]], off=off[lo:hi + 1] - off[lo], qcodes=qcodes, qoff=qoff)
     elif "clusters" in w:
         # clustered vectors: centers U[0,1)^D, members N(center, spread); queries are
         # members + N(0, noise) (SURVEY.md §8(d) C3/C5); fp32-representable
         rng = np.random.default_rng(seed)
-        D, n = w["dim"], w["n"]
+        D = w["dim"]
         centers = rng.uniform(0.0, 1.0, size=(w["clusters"], D)).astype(np.float32)
-        mat = np.empty((n, D), dtype=np.float32)
+        mat = np.empty((n_total, D), dtype=np.float32)
         step = 1 << 20
-        for a in range(0, n, step):
-            b = min(n, a + step)
+        for a in range(0, n_total, step):
+            b = min(n_total, a + step)
             assign = rng.integers(0, w["clusters"], size=b - a)
             mat[a:b] = centers[assign] + rng.normal(0.0, w["spread"], size=(b - a, D)).astype(np.float32)
         qr = np.random.default_rng(13)
-        qi = qr.integers(0, n, size=w["nq"])
+        qi = qr.integers(0, n_total, size=w["nq"])
         q = mat[qi] + qr.normal(0.0, w["noise"], size=(w["nq"], D)).astype(np.float32)
-        w.update(mat=mat.astype(np.float64), q=q.astype(np.float32).astype(np.float64))
+        if keep_full:
+            full = dict(mat=mat.astype(np.float64))
+        w.update(mat=mat[lo:hi].astype(np.float64), q=q.astype(np.float32).astype(np.float64))
     else:
         rng = np.random.default_rng(seed)
-        mat = rng.uniform(0.0, 1.0, size=(w["n"], w["dim"])).astype(np.float32).astype(np.float64)
+        mat = rng.uniform(0.0, 1.0, size=(n_total, w["dim"])).astype(np.float32).astype(np.float64)
         q = np.random.default_rng(13).uniform(0.0, 1.0, size=(w["nq"], w["dim"])).astype(np.float32).astype(np.float64)
-        w.update(mat=mat, q=q)
-    w["ids"] = np.arange(w["n"], dtype=np.int64) + rank * w["n"]
+        if keep_full:
+            full = dict(mat=mat)
+        w.update(mat=mat[lo:hi], q=q)
+    w["ids"] = np.arange(lo, hi, dtype=np.int64)
+    w["n"], w["n_total"], w["shard"] = hi - lo, n_total, (lo, hi)
+    if keep_full:
+        full["ids"] = np.arange(n_total, dtype=np.int64)
+        w["full"] = full
     return w
 
 
@@ -134,14 +154,17 @@ def bench_config(args, w, world):
     """The `config` object -- identical in both arms (same workload, sizes,
     tree geometry and budget)."""
     from oracle import oracle as O   # tree_height only (pure arithmetic, tree.py:60-78)
-    _, split = O.tree_height(w["n"], 20)
+    n_total = w.get("n_total", w["n"])
+    _, split = O.tree_height(max(n_total // world, 1), 20)
     return {
         "workload": f"{args.workload} (BASELINE.json configs[{w['config_index']}])",
-        "n_per_gpu": w["n"], "nq": w["nq"], "radius": w["radius"], "k": w["k"], "node_capacity": 20,
-        "levels": split + 1, "memory_units": 1 << 24,
+        "n": n_total, "n_per_gpu": n_total // world, "nq": w["nq"], "radius": w["radius"], "k": w["k"],
+        "node_capacity": 20, "levels_per_shard": split + 1, "memory_units": 1 << 24,
         "l2_policy": "index payload+tables exceed nothing: words (~25 MB) stay L2-resident by design; "
                      "no flush between steps (device-resident index is the operating point)",
-        "parallelism": f"dp{world} (one shard per GPU)",
+        "parallelism": (f"{world} shards (contiguous id ranges, one GTS tree per GPU), replicated query batch; "
+                        "kNN probe radii all-reduced (MIN), answers all-to-all'd to query owners and merged "
+                        "on device" if world > 1 else "one GPU, one tree"),
     }
 
 
@@ -424,17 +447,8 @@ def run_ours(args, rank, world, local_rank):
         if world > 1:
             dist.barrier()
 
-    merger = None
-    if world > 1:
-        from paper_2404_00966_b200.sharded import ShardMerger
-        merger = ShardMerger(nq, torch.device("cuda", local_rank))
-
     def one_step():
-        hs = eng.step_device(sp)
-        if merger is not None:
-            with torch.cuda.stream(stream):
-                merger.merge_handles(eng, hs, eng.ks, sp)
-        eng.free(hs)
+        eng.free(eng.step_device(sp))
 
     clocks = ClockSampler(local_rank, args.clock_ms)
     # no Python garbage-collector pauses inside timed steps (a gen-2 pass over
@@ -493,12 +507,12 @@ def run_ours(args, rank, world, local_rank):
     _lib.lib().gts_profile_enable(0)
 
     # e2e through the host C ABI with pinned buffers
-    e2e_ms, h2d, d2h = run_e2e(eng, w, args, sp, merger, world, max(totals))
+    e2e_ms, h2d, d2h = run_e2e(eng, w, args, sp, max(totals))
     gc.enable()
 
     if rank != 0:
         return None
-    qps = 2 * nq * world / (ms / 1e3)
+    qps = 2 * nq / (ms / 1e3)
     # the dominant leaf-verification kernel of this workload (whichever ran)
     cands = ("k_leafgroup_edit", "k_leaf_edit") if eng.edit else ("k_leafgroup_mma2", "k_leafgroup_mma", "k_leafgroup_tile", "k_leafgroup_vec", "k_verify")
     kname = max(cands, key=lambda k: prof["kernels"].get(k, {"ms": 0.0})["ms"])
@@ -508,7 +522,7 @@ def run_ours(args, rank, world, local_rank):
     out = {
         "metric": "range+kNN queries/sec",
         "value": round(qps, 3),
-        "unit": "queries/s" if world == 1 else "shard-queries/s",
+        "unit": "queries/s",
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
@@ -516,7 +530,7 @@ def run_ours(args, rank, world, local_rank):
         "wall_ms_per_step": round(wall_ms, 4),
         "step_ms": step_ms,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "u8 symbols / int32 bit-parallel DP" if eng.edit else "f32 screen + f64 exact recheck",
         "data": "synthetic",
@@ -528,7 +542,7 @@ def run_ours(args, rank, world, local_rank):
         "index_upload_s": round(eng.upload_s, 3),
         "clocks": clk,
         "gpu_launches": int(launches),
-        "e2e": {"value": round(2 * nq * world / (e2e_ms / 1e3), 3), "unit": "queries/s",
+        "e2e": {"value": round(2 * nq / (e2e_ms / 1e3), 3), "unit": "queries/s",
                 "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "profile": prof,
     }
@@ -538,7 +552,160 @@ def run_ours(args, rank, world, local_rank):
     return out
 
 
-def run_e2e(eng, w, args, sp, merger, world, max_total):
+def run_sharded(args, rank, world, local_rank):
+    """N > 1: one shard of the fixed collection per GPU (strong scaling), the
+    same query batch on every rank.  A step = range batch + kNN batch, each
+    answered by every shard and merged on the query owners
+    (paper_2404_00966_b200/sharded.py: kNN probe radii all-reduced with MIN,
+    answers all-to-all'd to their owner, k_merge_rank on the owner's GPU).
+    value = the batch's queries / max-over-ranks device time."""
+    import torch
+    import torch.distributed as dist
+    from paper_2404_00966_b200 import _lib
+    from paper_2404_00966_b200.sharded import ShardExchange, ShardSearcher, sharded_step
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    w = make_workload(args.workload, rank, args, world, keep_full=(rank == 0 and not args.no_cpu_baseline))
+    eng = Engine(w, local_rank)
+    stream = torch.cuda.Stream(dev)
+    sp = stream.cuda_stream
+    nq = w["nq"]
+    ss = ShardSearcher(eng.ix, dev, stream=sp)
+    ex = ShardExchange(nq, dev)
+    ks_dev = torch.from_numpy(eng.ks).to(dev)
+
+    def one_step():
+        with torch.cuda.stream(stream):
+            return sharded_step(ss, ex, eng.radii, eng.ks, ks_dev)
+
+    with torch.cuda.stream(stream):
+        ss.upload(eng.qb)
+    clocks = ClockSampler(local_rank, args.clock_ms)
+    gc.collect()
+    gc.disable()
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    ans = one_step()
+    torch.cuda.synchronize()
+    own_answers = [tuple(t.cpu().numpy() for t in a) for a in ans]
+
+    dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    launches0 = _lib.launch_count()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    evs[0].record(stream)
+    for i in range(args.steps):
+        one_step()
+        evs[i + 1].record(stream)
+        evs[i + 1].synchronize()
+    torch.cuda.synchronize()
+    launches = _lib.launch_count() - launches0
+    clk = clocks.stop()
+    step_ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
+    t = torch.tensor([evs[0].elapsed_time(evs[-1]) / args.steps], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    dist.barrier()
+
+    # e2e: H2D of the pinned host batch + search + exchange + D2H of the
+    # owner's answers, every step
+    if eng.edit:
+        pc = torch.from_numpy(w["qcodes"]).pin_memory()
+        po = torch.from_numpy(w["qoff"]).pin_memory()
+        qb = _lib.GtsQueryBatch(0, nq, 0, None, C.cast(pc.data_ptr(), _lib._i32p), C.cast(po.data_ptr(), _lib._i64p))
+        h2d = pc.numel() * 4 + po.numel() * 8
+    else:
+        pv = torch.from_numpy(w["q"]).pin_memory()
+        qb = _lib.GtsQueryBatch(eng.code, nq, w["dim"], C.cast(pv.data_ptr(), _lib._f64p), None, None)
+        h2d = pv.numel() * 8
+    d2h = [0]
+    pinned = {}
+
+    def e2e_step():
+        with torch.cuda.stream(stream):
+            ss.upload(qb)
+            res = sharded_step(ss, ex, eng.radii, eng.ks, ks_dev)
+            b = 0
+            for i, part in enumerate(res):
+                for j, tns in enumerate(part):
+                    host = pinned.get((i, j))
+                    if host is None or host.numel() < tns.numel():
+                        host = pinned[(i, j)] = torch.empty(int(tns.numel() * 1.25) + 1024, dtype=tns.dtype,
+                                                            pin_memory=True)
+                    host[:tns.numel()].copy_(tns, non_blocking=True)
+                    b += tns.numel() * tns.element_size()
+            stream.synchronize()
+            d2h[0] = b
+
+    for _ in range(max(1, args.warmup // 2)):
+        e2e_step()
+    dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    te = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_ms = float(te.item())
+    clocks.close()
+    gc.enable()
+
+    # parity of rank 0's owned queries against brute force over the whole collection
+    parity = None
+    if rank == 0 and "full" in w:
+        parity = sharded_parity(w, ex.own, own_answers)
+    ss.free()
+    if rank != 0:
+        return None
+    return {
+        "metric": "range+kNN queries/sec", "value": round(2 * nq / (ms / 1e3), 3), "unit": "queries/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "step_ms_rank0": [round(x, 3) for x in step_ms], "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "u8 symbols / int32 bit-parallel DP" if eng.edit else "f32 screen + f64 exact recheck",
+        "data": "synthetic", "config": bench_config(args, w, world),
+        "build_s_rank0": round(eng.build_s, 3), "index_upload_s_rank0": round(eng.upload_s, 3),
+        "clocks": clk, "gpu_launches": int(launches),
+        "e2e": {"value": round(2 * nq / (e2e_ms / 1e3), 3), "unit": "queries/s", "ms_per_step": round(e2e_ms, 4),
+                "h2d_bytes_per_step": int(h2d + nq * 16), "d2h_bytes_per_step": int(d2h[0])},
+        "parity": parity,
+    }
+
+
+def sharded_parity(w, own, answers, n_sample=32):
+    """Rank 0's merged answers for a sample of its owned queries vs the
+    oracle's brute force over the whole collection (oracle.py:19-36)."""
+    from oracle import oracle as O
+    f = w["full"]
+    if w["metric"] == "edit":
+        data = O.Payloads(O.EDIT, codes=f["codes"], off=f["off"], ids=f["ids"])
+    else:
+        data = O.Payloads({"l1": O.L1, "l2": O.L2}[w["metric"]], vec=f["mat"], ids=f["ids"])
+    lo, hi = own
+    rng = np.random.default_rng(0)
+    idx = np.sort(rng.choice(np.arange(lo, hi), size=min(n_sample, hi - lo), replace=False))
+    qs = oracle_queries(O, w, idx)
+    thr = os.cpu_count() or 1
+    want = [O.brute(data, qs, O.RANGE, radii=np.full(idx.size, w["radius"]), threads=thr).answers(),
+            O.brute(data, qs, O.KNN, ks=np.full(idx.size, w["k"]), threads=thr).answers()]
+    mism = 0
+    for (off, ids, dis), wa in zip(answers, want):
+        for j, q in enumerate(idx):
+            a, b = off[q - lo], off[q - lo + 1]
+            if not (np.array_equal(ids[a:b], wa[j][0]) and np.array_equal(dis[a:b], wa[j][1])):
+                mism += 1
+    return {"checked": 2 * idx.size, "mismatches": mism, "tolerated": 0,
+            "against": "oracle brute force over the whole collection (range and kNN (distance, id) lists), "
+                       "sample of rank 0's owned queries"}
+
+
+def run_e2e(eng, w, args, sp, max_total):
     import torch
     from paper_2404_00966_b200 import _lib
     nq = w["nq"]
@@ -795,7 +962,7 @@ def run_reference(args, rank, world):
     return {
         "impl": "reference", "metric": "range+kNN queries/sec", "value": round(v, 3), "unit": "queries/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot_t / args.steps * 1e3, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64/int64 (CPU)",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64/int64 (CPU)",
         "data": "synthetic", "config": bench_config(args, w, world),
         "cpu_baseline": {"value": round(v, 3), "unit": "queries/s", "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": round(v, 3), "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -817,6 +984,17 @@ def main():
     ap.add_argument("--clock-ms", type=int, default=200, help="nvidia-smi sampling interval in the timed region")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        # one process per GPU: re-launch this command under torchrun
+        import socket
+        import subprocess
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
@@ -833,7 +1011,12 @@ def main():
             torch.cuda.set_device(local_rank)
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             dist.init_process_group(os.environ.get("GTS_DIST_BACKEND", "nccl"))
-        out = (run_stream if args.workload == "dna_stream" else run_ours)(args, rank, world, local_rank)
+        if args.workload == "dna_stream":
+            out = run_stream(args, rank, world, local_rank)
+        elif world > 1:
+            out = run_sharded(args, rank, world, local_rank)
+        else:
+            out = run_ours(args, rank, world, local_rank)
         if world > 1:
             import torch.distributed as dist
             dist.destroy_process_group()

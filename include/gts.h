@@ -121,6 +121,17 @@ int gts_range_batch(gts_index *ix, const gts_queries *q, const double *radii,
  * the k smallest (distance, id) pairs over live objects (oracle.py:30-36). */
 int gts_knn_batch(gts_index *ix, const gts_queries *q, const int64_t *ks,
                   int64_t memory_units, int pruning, void *stream, gts_result **out);
+/* kNN in two phases, for a collection sharded over several indexes
+ * (SURVEY.md §8(e) collective 2; the reference has one index, search.py:250-296):
+ * gts_knn_probe writes each query's probe radius -- an upper bound of the
+ * k-th distance within this index -- into radius_out[nq] (device float32).
+ * The MIN of those radii over all shards bounds the global k-th distance;
+ * gts_knn_batch_bounded then searches with that radius instead of probing
+ * (radius NULL = probe as gts_knn_batch does).  flags as gts_batch_host. */
+int gts_knn_probe(gts_index *ix, const gts_queries *q, const int64_t *ks, void *stream, float *radius_out);
+int gts_knn_batch_bounded(gts_index *ix, const gts_queries *q, const int64_t *ks, const float *radius,
+                          int64_t memory_units, int flags, void *stream, gts_result **out);
+
 /* One-call host path: upload + search + download (the e2e boundary). */
 int gts_range_batch_host(gts_index *ix, const gts_query_batch *qb, const double *radii,
                          int64_t memory_units, int pruning, void *stream, gts_result **out);
@@ -150,6 +161,35 @@ int gts_result_copy(const gts_result *r, int64_t *offsets, int64_t *ids, double 
 int gts_result_device(const gts_result *r, const int64_t **offsets, const int64_t **ids,
                       const double **dis);
 int gts_result_free(gts_result *r);
+
+/* ---- sharded collections ------------------------------
+ * A collection split into shards, one GTS tree (one gts_index) per shard.
+ * Exact answers over the union are the union of exact per-shard answers
+ * (PAPER.md:213-222); the merge keeps, per query, the k smallest (kNN,
+ * _KnnPool.merge search.py:116-144) or all (range) answers ordered by
+ * (distance, id) (_collect search.py:298-314).
+ *
+ * gts_merge_results: the owner side of an all-to-all exchange.  nsrc sorted
+ * answer lists per query, all device pointers on the current device:
+ * counts[nsrc][nq]; ids / dis: source-major, then query-major (each
+ * (source, query) list sorted by (distance, id)); ks[nq] (kNN) or NULL
+ * (range); verified / pruned [nsrc][nq] or NULL (summed).  The merged CSR is
+ * a result handle (gts_result_copy / gts_result_device / gts_result_free). */
+int gts_merge_results(int nsrc, int64_t nq, const int64_t *counts, const int64_t *ids, const double *dis,
+                      const int64_t *ks, const int64_t *verified, const int64_t *pruned, void *stream,
+                      gts_result **out);
+
+/* One handle over several shard indexes (the SURVEY.md §8(b) multi-device
+ * handle: the shards' devices form its device set).  The shard indexes stay
+ * owned by the caller and must outlive the handle.  gts_multi_batch_host runs
+ * one host thread per shard (upload, search on the shard's device), kNN with
+ * the MIN-radius exchange, gathers the answers to shards[0]'s device over
+ * peer copies and merges them there. */
+typedef struct gts_multi gts_multi;
+int gts_multi_create(int nshards, gts_index *const *shards, gts_multi **out);
+int gts_multi_destroy(gts_multi *m);
+int gts_multi_batch_host(gts_multi *m, const gts_query_batch *qb, int mode, const double *radii,
+                         const int64_t *ks, int64_t memory_units, int flags, gts_result **out);
 
 /* Exact single-pair and row-pair distances on the device (metrics.py:196-223
  * and data.py:245-263 row_to_row), float64 result, for tests and the cache

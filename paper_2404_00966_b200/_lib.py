@@ -87,6 +87,13 @@ def lib():
             "gts_result_free": (C.c_int, [v]),
             "gts_pair_distances": (C.c_int, [C.c_int32, C.c_int64, C.c_int64, _f64p, _f64p, _i32p, _i64p,
                                              _i32p, _i64p, _f64p, v]),
+            "gts_knn_probe": (C.c_int, [v, v, _i64p, v, v]),
+            "gts_knn_batch_bounded": (C.c_int, [v, v, _i64p, v, C.c_int64, C.c_int, v, C.POINTER(v)]),
+            "gts_merge_results": (C.c_int, [C.c_int, C.c_int64, v, v, v, v, v, v, v, C.POINTER(v)]),
+            "gts_multi_create": (C.c_int, [C.c_int, C.POINTER(v), C.POINTER(v)]),
+            "gts_multi_destroy": (C.c_int, [v]),
+            "gts_multi_batch_host": (C.c_int, [v, C.POINTER(GtsQueryBatch), C.c_int, _f64p, _i64p, C.c_int64,
+                                               C.c_int, C.POINTER(v)]),
             "gts_launch_count": (C.c_int64, []),
             "gts_profile_enable": (C.c_int, [C.c_int]),
             "gts_profile_read": (C.c_int, [C.c_char_p, C.c_int64, C.c_int]),
@@ -108,7 +115,8 @@ EXPORTED = (
     "gts_knn_batch", "gts_range_batch_host", "gts_knn_batch_host", "gts_result_info", "gts_result_copy",
     "gts_result_device", "gts_result_free", "gts_pair_distances", "gts_launch_count", "gts_last_error",
     "gts_version", "gts_profile_enable", "gts_profile_read", "gts_bench_int_peak", "gts_batch_host",
-    "gts_index_cache_set",
+    "gts_index_cache_set", "gts_knn_probe", "gts_knn_batch_bounded", "gts_merge_results", "gts_multi_create",
+    "gts_multi_destroy", "gts_multi_batch_host",
 )
 
 

@@ -24,6 +24,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <thread>
 #include <tuple>
 #include <string>
 #include <vector>
@@ -148,6 +149,27 @@ static inline unsigned grid_for(int64_t threads, int block, unsigned cap = 1u <<
     if (g < 1) g = 1;
     if (g > cap) g = cap;
     return (unsigned)g;
+}
+
+// Dynamic shared-memory opt-in.  cudaFuncSetAttribute applies per device
+// context, so the granted size is recorded per (device, kernel); a mutex
+// makes it safe for the per-shard host threads of a multi-device index.
+static void smem_optin(const void *fn, size_t bytes)
+{
+    static std::mutex mu;
+    static std::vector<std::tuple<int, const void *, size_t>> granted;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> g(mu);
+    for (auto &t : granted)
+        if (std::get<0>(t) == dev && std::get<1>(t) == fn) {
+            if (std::get<2>(t) >= bytes) return;
+            CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+            std::get<2>(t) = bytes;
+            return;
+        }
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    granted.emplace_back(dev, fn, bytes);
 }
 
 // ---------------------------------------------------------------------------
@@ -2428,6 +2450,48 @@ __global__ void __launch_bounds__(256) k_probe_select(IndexView ix, int q0, int 
     }
 }
 
+// Largest fp32 distance from the root pivot (query slot 0 of a one-row
+// batch) to any entry.  By the triangle inequality d(q,o) <= d(q,root) +
+// that radius for every object, so it bounds any k-th distance; it is the
+// kNN starting radius when the probe finds no finite estimate (k above the
+// probe's candidate cap, or probed nodes left with fewer than k live
+// entries after deletes), so the histogram shrink still has a finite range.
+template <int MET>
+__global__ void k_root_radius(IndexView ix, QueryView qv, int64_t n, unsigned *out)
+{
+    float m = 0.f;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const float d = dist32<MET>(ix, qv, 0, (int)e);
+        if (d == d) m = fmaxf(m, d);
+    }
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(kFull, m, o));
+    if (lane_id() == 0) atomicMax(out, __float_as_uint(m));
+}
+
+template <int MET>
+__global__ void k_finite_bound(IndexView ix, QueryView qv, int nq, float rroot, float *r32, double *r64)
+{
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq || r32[q] < INFINITY) return;
+    const float d = dist32<MET>(ix, qv, q, ix.node[1].piv);
+    // each fp32 distance is within slack of its float64 value
+    const float t = (d + rroot + slack(ix, d, rroot) + ix.abs_eps) * (1.f + 0x1p-20f);
+    r32[q] = t;
+    r64[q] = (double)t;
+}
+
+// kNN radius supplied by the caller (the MIN over shards of every shard's
+// probe radius, SURVEY.md §8(e) collective 2): each shard's probe radius is
+// an upper bound of its own k-th distance, hence of the global one.
+__global__ void k_set_bound(const float *__restrict__ b, int nq, float *r32, double *r64)
+{
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    const float t = b[q];
+    r32[q] = t;
+    r64[q] = (double)t;
+}
+
 // query preparation --------------------------------------------------------
 
 __global__ void k_map_symbols(const int32_t *codes, int64_t n, const int32_t *alpha, int A, uint8_t *out)
@@ -2736,6 +2800,11 @@ struct gts_index {
     DBuf<int32_t> live_leaves;
     int n_live_leaves = 0;
     std::vector<int32_t> h_alpha;
+    // vectors: fp32 radius of the whole collection around the root pivot
+    // (k_root_radius) and of the pending cache (host, float64), and the root
+    // pivot's payload for the latter
+    float root_radius = INFINITY, cache_radius = 0.f;
+    std::vector<double> root_payload;
 };
 
 struct gts_queries {
@@ -2890,6 +2959,8 @@ struct Search {
     bool prof = false;
     std::vector<std::tuple<const char *, cudaEvent_t, cudaEvent_t>> events;
     DBuf<unsigned long long> work;
+    const float *ext_bound = nullptr;   // kNN: caller-supplied radius per query (device), replaces the probe
+    float *probe_out = nullptr;         // kNN probe-only call: the probe radius per query goes here
 
     // time one launch with events when profiling is on
     template <class F>
@@ -3045,11 +3116,7 @@ struct Search {
         group_rows(rows, m, G, kLgItemRows);
         if (G.nitems == 0) return;
         HitBuf hb{hq.p, he.p, hd.p, (unsigned long long)hq.n, counter.p + 1};
-        static int attr = 0;
-        if (attr < L.total) {
-            CK(cudaFuncSetAttribute(k_leafgroup_edit, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
-            attr = 100 * 1024;
-        }
+        smem_optin((const void *)k_leafgroup_edit, 100 * 1024);
         int sms = 148, per = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_leafgroup_edit, 32 * kLgWarps, L.total));
@@ -3073,11 +3140,7 @@ struct Search {
         while ((int)cols < nmax) cols <<= 1;
         const size_t nkb = (size_t)ix->Dk / 64;
         const size_t smb = 2 * (nkb * 16384 + nkb * (size_t)nmax * 128) + 1024;
-        static size_t attr = 0;
-        if (attr < smb) {
-            CK(cudaFuncSetAttribute(k_leafgroup_mma2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
-            attr = smb;
-        }
+        smem_optin((const void *)k_leafgroup_mma2, smb);
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
         const unsigned grid = (unsigned)std::min<int>(nitems, sms);   // items i, i + grid, ... per CTA
@@ -3155,11 +3218,7 @@ struct Search {
         if (MET == kMetricL2 && ix->vcent.p && pruning) {
             const int nmax = std::max(16, (ix->max_leaf + 15) & ~15);
             const size_t smb = (size_t)(ix->Dk / 64) * (128 * 128 + (size_t)nmax * 128) + 1024;
-            static bool mma_attr = false;
-            if (!mma_attr) {
-                CK(cudaFuncSetAttribute(k_leafgroup_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-                mma_attr = true;
-            }
+            smem_optin((const void *)k_leafgroup_mma, 220 * 1024);
             int sms = 148;
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
             uint32_t cols = 32;
@@ -3179,12 +3238,7 @@ struct Search {
             const size_t tsm = ((size_t)ix->max_leaf * (ix->Dp + 4) + (size_t)128 * (ix->Dp + 4) + ix->max_leaf +
                                 6 * 128) * sizeof(float);
             if (tsm <= 200 * 1024 && std::getenv("GTS_VEC_ROWWARP") == nullptr) {
-                static bool tattr[3] = {false, false, false};
-                if (!tattr[MET]) {
-                    CK(cudaFuncSetAttribute(k_leafgroup_tile<MET>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            200 * 1024));
-                    tattr[MET] = true;
-                }
+                smem_optin((const void *)k_leafgroup_tile<MET>, 200 * 1024);
                 int per = 0;
                 CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_leafgroup_tile<MET>, 256, tsm));
                 const unsigned tgrid = (unsigned)std::min<int64_t>(nitems, (int64_t)148 * std::max(per, 1));
@@ -3201,11 +3255,7 @@ struct Search {
                 return;
             }
         }
-        static bool attr_set[3] = {false, false, false};
-        if (!attr_set[MET]) {
-            CK(cudaFuncSetAttribute(k_leafgroup_vec<MET>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-            attr_set[MET] = true;
-        }
+        smem_optin((const void *)k_leafgroup_vec<MET>, 200 * 1024);
         unsigned grid = (unsigned)std::min<int>(nitems, 148 * 8);
         timed("k_leafgroup_vec", [&] {
             k_leafgroup_vec<MET><<<grid, 256, sm, st>>>(iv, qv, srows.p, items.p, nitems, pruning, r32.p, r64.p, hb,
@@ -3294,12 +3344,8 @@ struct Search {
             int tstride = 0;
             if (ix->max_len <= 64 && env_tx && env_tx[0] == '1') tstride = (((ix->max_len + 3) >> 2) | 1);
             const size_t dyn = (size_t)tstride * kWarp * kLeafWarps * sizeof(uint32_t);
-            static bool le_attr = false;
-            if (!le_attr) {
-                // static 38.9 KB + up to 17 KB of staged texts
-                CK(cudaFuncSetAttribute(k_leaf_edit, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-                le_attr = true;
-            }
+            // static 38.9 KB + up to 17 KB of staged texts
+            smem_optin((const void *)k_leaf_edit, 64 * 1024);
             CK(cudaMemsetAsync(counter.p, 0, sizeof(unsigned long long), st));
             timed("k_leaf_edit", [&] {
                 k_leaf_edit<<<grid, 32 * kLeafWarps, dyn, st>>>(iv, qv, rows, m, pruning, r32.p, hb, verified.p,
@@ -3329,11 +3375,7 @@ struct Search {
             CK(cudaMemsetAsync(counter.p, 0, sizeof(unsigned long long), st));
             if (G.nitems == 0) return 0;
             const size_t smb = (size_t)ix->nc * (ix->Dp + 4) * sizeof(float) + (size_t)ix->nc * sizeof(NodeRec);
-            static size_t attr[3] = {0, 0, 0};
-            if (attr[MET] < smb) {
-                CK(cudaFuncSetAttribute(k_expand_grouped<MET>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
-                attr[MET] = smb;
-            }
+            smem_optin((const void *)k_expand_grouped<MET>, smb);
             const unsigned grid = (unsigned)std::min<int>(G.nitems, 148 * 8);
             timed("k_expand", [&] {
                 k_expand_grouped<MET><<<grid, 256, smb, st>>>(iv, qv, G.srows.p, G.items.p, G.nitems, own, pruning,
@@ -3401,16 +3443,21 @@ struct Search {
     }
 
     template <int MET>
+    void launch_finite_bound()
+    {
+        const float rr = std::max(ix->root_radius, ix->cache_radius);
+        if (!(rr < INFINITY)) return;
+        k_finite_bound<MET><<<grid_for(nq, 256), 256, 0, st>>>(iv, qv, (int)nq, rr, r32.p, r64.p);
+        LAUNCH_CHECK();
+    }
+
+    template <int MET>
     void launch_probe_grouped()
     {
         const int64_t qchunk = std::min<int64_t>(nq, 1 << 17);   // <= 4 GiB of candidate distances
         const size_t pd_smem = (size_t)2 * kPT * (kPD + 4) * sizeof(float);
-        static bool attr = false;
-        if (!attr) {
-            CK(cudaFuncSetAttribute(k_probe_dist<kMetricL1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pd_smem));
-            CK(cudaFuncSetAttribute(k_probe_dist<kMetricL2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pd_smem));
-            attr = true;
-        }
+        smem_optin((const void *)k_probe_dist<kMetricL1>, pd_smem);
+        smem_optin((const void *)k_probe_dist<kMetricL2>, pd_smem);
         DBuf<uint32_t> keys((size_t)kProbeRows * qchunk, st), skeys((size_t)kProbeRows * qchunk, st);
         DBuf<int32_t> vals((size_t)kProbeRows * qchunk, st), svals((size_t)kProbeRows * qchunk, st);
         DBuf<float> dist((size_t)qchunk * kProbeCand, st);
@@ -3442,11 +3489,20 @@ struct Search {
             CK(cudaMemsetAsync(hist.p, 0, sizeof(unsigned) * (size_t)nq * kHistBins, st));
         }
         if (mode == 1 && pruning) {
-            switch (ix->metric) {
-            case GTS_EDIT: launch_probe<kMetricEdit>(); break;
-            case GTS_L1: launch_probe<kMetricL1>(); break;
-            case GTS_ANGULAR: launch_probe<kMetricAngular>(); break;
-            default: launch_probe<kMetricL2>(); break;
+            if (ext_bound) {
+                k_set_bound<<<grid_for(nq, 256), 256, 0, st>>>(ext_bound, (int)nq, r32.p, r64.p);
+                LAUNCH_CHECK();
+            } else {
+                switch (ix->metric) {
+                case GTS_EDIT: launch_probe<kMetricEdit>(); break;
+                case GTS_L1: launch_probe<kMetricL1>(); launch_finite_bound<kMetricL1>(); break;
+                case GTS_ANGULAR: launch_probe<kMetricAngular>(); launch_finite_bound<kMetricAngular>(); break;
+                default: launch_probe<kMetricL2>(); launch_finite_bound<kMetricL2>(); break;
+                }
+            }
+            if (probe_out) {
+                CK(cudaMemcpyAsync(probe_out, r32.p, sizeof(float) * nq, cudaMemcpyDeviceToDevice, st));
+                return;
             }
             if (ix->metric != GTS_EDIT) {
                 fhist.alloc((size_t)nq * kFHist, st);
@@ -3542,6 +3598,9 @@ struct Search {
     void collect_impl(gts_result *res)
     {
         const int64_t n = (int64_t)hits;
+        // the CUB sorts index with int: fail loudly instead of truncating
+        if (n > (int64_t)INT32_MAX)
+            fail(GTS_EBUDGET, "%lld answers in one batch exceed 2^31-1; split the query batch", (long long)n);
         res->nq = nq;
         res->peak = peak;
         std::memcpy(res->limits, limits, sizeof(limits));
@@ -3746,7 +3805,8 @@ static double now_ms()
 }
 
 gts_result *run_search(gts_index *ix, const gts_queries *q, int mode, const double *radii, const int64_t *ks,
-                       int64_t memory_units, int pruning, cudaStream_t st, bool use_cache = false)
+                       int64_t memory_units, int pruning, cudaStream_t st, bool use_cache = false,
+                       const float *ext_bound = nullptr, float *probe_out = nullptr)
 {
     static const bool trace = std::getenv("GTS_TRACE") != nullptr;
     const double t0 = trace ? now_ms() : 0.0;
@@ -3790,7 +3850,17 @@ gts_result *run_search(gts_index *ix, const gts_queries *q, int mode, const doub
     }
     const double t1 = trace ? now_ms() : 0.0;
     s.use_cache = use_cache;
+    s.ext_bound = mode == 1 ? ext_bound : nullptr;
+    s.probe_out = mode == 1 ? probe_out : nullptr;
     s.run();
+    if (s.probe_out) {
+        if (!pruning || ix->levels == 0 || ix->n == 0) {
+            std::vector<float> inf32((size_t)nq, INFINITY);
+            h2d(probe_out, inf32.data(), (size_t)nq, st);
+        }
+        CK(cudaStreamSynchronize(st));
+        return nullptr;
+    }
     s.scan_cache();
     const double t2 = trace ? now_ms() : 0.0;
     {
@@ -3828,6 +3898,53 @@ gts_result *run_search(gts_index *ix, const gts_queries *q, int mode, const doub
 }
 
 }  // namespace
+
+// fp32 radius of the collection around the root pivot (k_root_radius):
+// the root pivot's payload is uploaded as a one-row query batch.
+void compute_root_radius(gts_index *ix, const gts_dataset *ds, const gts_tree *t, cudaStream_t st)
+{
+    const int64_t prow = t->pivot_row[1];
+    if (prow < 0 || prow >= ds->n) return;
+    ix->root_payload.assign(ds->vectors + prow * ix->D, ds->vectors + (prow + 1) * ix->D);
+    gts_query_batch qb{ds->metric, 1, ix->D, ix->root_payload.data(), nullptr, nullptr};
+    gts_queries *q = upload_queries(ix, &qb, st);
+    DBuf<unsigned> m(1, st);
+    CK(cudaMemsetAsync(m.p, 0, sizeof(unsigned), st));
+    const IndexView iv = make_view(ix, q);
+    const QueryView qv = make_qview(ix, q);
+    const unsigned grid = grid_for(ix->n, 256, 148u * 8u);
+    switch (ix->metric) {
+    case GTS_L1: k_root_radius<kMetricL1><<<grid, 256, 0, st>>>(iv, qv, ix->n, m.p); break;
+    case GTS_ANGULAR: k_root_radius<kMetricAngular><<<grid, 256, 0, st>>>(iv, qv, ix->n, m.p); break;
+    default: k_root_radius<kMetricL2><<<grid, 256, 0, st>>>(iv, qv, ix->n, m.p); break;
+    }
+    LAUNCH_CHECK();
+    unsigned h = 0;
+    CK(cudaMemcpyAsync(&h, m.p, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    delete q;
+    float r;
+    std::memcpy(&r, &h, sizeof(r));
+    ix->root_radius = r;
+}
+
+// float64 radius of the pending cache around the root pivot, rounded up
+double host_metric(int metric, const double *a, const double *b, int64_t D)
+{
+    double acc = 0.0;
+    if (metric == GTS_L1) {
+        for (int64_t i = 0; i < D; i++) acc += std::fabs(a[i] - b[i]);
+        return acc;
+    }
+    if (metric == GTS_L2) {
+        for (int64_t i = 0; i < D; i++) acc += (a[i] - b[i]) * (a[i] - b[i]);
+        return std::sqrt(acc);
+    }
+    double na = 0.0, nb = 0.0;
+    for (int64_t i = 0; i < D; i++) { acc += a[i] * b[i]; na += a[i] * a[i]; nb += b[i] * b[i]; }
+    if (na == 0.0 || nb == 0.0) return M_PI;
+    return std::acos(std::max(-1.0, std::min(1.0, acc / std::sqrt(na * nb))));
+}
 
 // ===========================================================================
 // C ABI
@@ -4235,6 +4352,7 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
             }
         }
         CK(cudaStreamSynchronize(st));
+        if (ds->metric != GTS_EDIT && n > 0 && ix->levels > 0) compute_root_radius(ix, ds, t, st);
         *out = ix;
         return GTS_OK;
     } catch (...) {
@@ -4313,6 +4431,26 @@ extern "C" int gts_knn_batch(gts_index *ix, const gts_queries *q, const int64_t 
     ABI_END
 }
 
+extern "C" int gts_knn_probe(gts_index *ix, const gts_queries *q, const int64_t *ks, void *stream, float *radius_out)
+{
+    ABI_BEGIN
+    if (!ix || !q || !radius_out || (!ks && q->nq)) fail(GTS_EINVAL, "null argument");
+    run_search(ix, q, 1, nullptr, ks, 0, 1, (cudaStream_t)stream, false, nullptr, radius_out);
+    return GTS_OK;
+    ABI_END
+}
+
+extern "C" int gts_knn_batch_bounded(gts_index *ix, const gts_queries *q, const int64_t *ks, const float *radius,
+                                     int64_t memory_units, int flags, void *stream, gts_result **out)
+{
+    ABI_BEGIN
+    if (!out || (!ks && q && q->nq)) fail(GTS_EINVAL, "null argument");
+    *out = run_search(ix, q, 1, nullptr, ks, memory_units, (flags & GTS_FLAG_PRUNING) ? 1 : 0, (cudaStream_t)stream,
+                      (flags & GTS_FLAG_CACHE) != 0, radius, nullptr);
+    return GTS_OK;
+    ABI_END
+}
+
 extern "C" int gts_range_batch_host(gts_index *ix, const gts_query_batch *qb, const double *radii,
                                     int64_t memory_units, int pruning, void *stream, gts_result **out)
 {
@@ -4374,6 +4512,7 @@ extern "C" int gts_index_cache_set(gts_index *ix, const gts_dataset *items, void
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t n = items->n;
     ix->cache_n = 0;
+    ix->cache_radius = 0.f;
     if (n == 0) return GTS_OK;
     if (n > (1 << 30)) fail(GTS_EINVAL, "cache too large");
     if (items->metric != ix->metric) fail(GTS_EMETRIC, "cache metric %d != index metric %d", items->metric, ix->metric);
@@ -4400,6 +4539,13 @@ extern "C" int gts_index_cache_set(gts_index *ix, const gts_dataset *items, void
         if (items->dim != ix->D) fail(GTS_EMETRIC, "cache dimensionality %lld != %d", (long long)items->dim, ix->D);
         ix->cache_vec64.alloc((size_t)(n * ix->D), st);
         h2d(ix->cache_vec64.p, items->vectors, (size_t)(n * ix->D), st);
+        double cr = 0.0;
+        if ((int64_t)ix->root_payload.size() == ix->D)
+            for (int64_t i = 0; i < n; i++)
+                cr = std::max(cr, host_metric(ix->metric, items->vectors + i * ix->D, ix->root_payload.data(), ix->D));
+        else
+            cr = INFINITY;
+        ix->cache_radius = (float)(cr * (1.0 + 1e-6) + 1e-6);
     }
     CK(cudaStreamSynchronize(st));
     ix->cache_n = (int)n;
@@ -4532,3 +4678,6 @@ extern "C" int gts_pair_distances(int32_t metric, int64_t np, int64_t dim, const
     return GTS_OK;
     ABI_END
 }
+
+// multi-shard exchange + merge
+#include "sharded.cuh"

@@ -157,19 +157,23 @@ class FlatPivotTree:
             p(self.rows, _lib._i64p), p(self.dis, _lib._f64p), p(self.tombstone, _lib._u8p))
 
     def device_index(self, device=0):
-        """The device-resident list tables of this tree (created once)."""
+        """The device-resident list tables of this tree on `device` (created
+        once per device; tombstones re-synced when they changed)."""
         if self._dev is None:
+            self._dev, self._dev_tomb = {}, {}
+        dev = self._dev.get(int(device))
+        if dev is None:
             ds, keep = _c_dataset(self.dataset)
             h = C.c_void_p()
             t = self._c_tree()
             _lib.check(_lib.lib().gts_index_create(C.byref(ds), C.byref(t), int(device), C.byref(h)))
-            self._dev = _DeviceIndex(h)
-            self._dev_tomb = self.tombstone.copy()
-        elif not np.array_equal(self._dev_tomb, self.tombstone):
+            dev = self._dev[int(device)] = _DeviceIndex(h)
+            self._dev_tomb[int(device)] = self.tombstone.copy()
+        elif not np.array_equal(self._dev_tomb[int(device)], self.tombstone):
             tomb = np.ascontiguousarray(self.tombstone, dtype=np.uint8)
-            _lib.check(_lib.lib().gts_index_set_tombstones(self._dev.h, _lib.ptr(tomb, _lib._u8p), None))
-            self._dev_tomb = tomb.copy()
-        return self._dev
+            _lib.check(_lib.lib().gts_index_set_tombstones(dev.h, _lib.ptr(tomb, _lib._u8p), None))
+            self._dev_tomb[int(device)] = tomb.copy()
+        return dev
 
 
 class _DeviceIndex:
