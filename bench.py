@@ -291,7 +291,13 @@ class Engine:
                                  p(a["dis"], _lib._f64p), p(a["tomb"], _lib._u8p))
         root_row = int(np.random.default_rng(0).integers(0, n))
         t0 = time.perf_counter()
-        _lib.check(self.L.gts_build_tree(C.byref(self.ds), root_row, 0, C.byref(self.tree)))
+        # device bulk build (csrc/devbuild.cuh; bit-identical to the host
+        # builder); GTS_HOST_BUILD=1 uses the host C++/OpenMP builder
+        self.build_where = "host" if os.environ.get("GTS_HOST_BUILD") == "1" else "device"
+        if self.build_where == "host":
+            _lib.check(self.L.gts_build_tree(C.byref(self.ds), root_row, 0, C.byref(self.tree)))
+        else:
+            _lib.check(self.L.gts_build_tree_device(C.byref(self.ds), root_row, device, C.byref(self.tree)))
         self.build_s = time.perf_counter() - t0
         self.levels = levels
         h = C.c_void_p()
@@ -539,6 +545,7 @@ def run_ours(args, rank, world, local_rank):
         "knn_answers_per_step": totals[1],
         "distance_evals_per_s": round(work["pairs"] / (step_ms_prof / 1e3), 1) if step_ms_prof else None,
         "build_s": round(eng.build_s, 3),
+        "build_where": eng.build_where,
         "index_upload_s": round(eng.upload_s, 3),
         "clocks": clk,
         "gpu_launches": int(launches),

@@ -84,6 +84,18 @@ int64_t gts_node_count(int64_t levels, int64_t nc);
  * (tree.py:263, 288-291), made by the caller.  nthreads <= 0: all cores. */
 int gts_build_tree(const gts_dataset *ds, int64_t root_row, int nthreads, gts_tree *tree);
 
+/* The same build on the device: per level a segmented
+ * reduction picks the pivots, one thread per entry maps its float64 (numpy
+ * pairwise order) or exact edit distance, two stable radix sorts order the
+ * level by (dis / (max + 1) + ordinal, id).  Bit-identical to gts_build_tree
+ * and to the reference (tree.py:241-385).  Metrics edit, l1, l2 (angular
+ * stays on gts_build_tree: numpy's arccos is not the device's). */
+int gts_build_tree_device(const gts_dataset *ds, int64_t root_row, int device, gts_tree *tree);
+/* Device build over device-resident float32 vectors x[n][dim] on `device`
+ * (e.g. gts_generate_clustered output); ids: host [n]; metric l1 or l2. */
+int gts_build_tree_device_f32(int32_t metric, int64_t n, int64_t dim, const float *x, const int64_t *ids,
+                              int64_t root_row, int device, gts_tree *tree);
+
 /* Device index: uploads the flattened list tables (node table, pivot ids
  * and ranges, object table with pivot distances, payloads in table order).
  * Replaces the state BatchSearcher.__init__ binds (search.py:225-234). */

@@ -94,6 +94,9 @@ def lib():
             "gts_multi_destroy": (C.c_int, [v]),
             "gts_multi_batch_host": (C.c_int, [v, C.POINTER(GtsQueryBatch), C.c_int, _f64p, _i64p, C.c_int64,
                                                C.c_int, C.POINTER(v)]),
+            "gts_build_tree_device": (C.c_int, [C.POINTER(GtsDataset), C.c_int64, C.c_int, C.POINTER(GtsTree)]),
+            "gts_build_tree_device_f32": (C.c_int, [C.c_int32, C.c_int64, C.c_int64, v, _i64p, C.c_int64, C.c_int,
+                                                    C.POINTER(GtsTree)]),
             "gts_launch_count": (C.c_int64, []),
             "gts_profile_enable": (C.c_int, [C.c_int]),
             "gts_profile_read": (C.c_int, [C.c_char_p, C.c_int64, C.c_int]),
@@ -116,7 +119,7 @@ EXPORTED = (
     "gts_result_device", "gts_result_free", "gts_pair_distances", "gts_launch_count", "gts_last_error",
     "gts_version", "gts_profile_enable", "gts_profile_read", "gts_bench_int_peak", "gts_batch_host",
     "gts_index_cache_set", "gts_knn_probe", "gts_knn_batch_bounded", "gts_merge_results", "gts_multi_create",
-    "gts_multi_destroy", "gts_multi_batch_host",
+    "gts_multi_destroy", "gts_multi_batch_host", "gts_build_tree_device", "gts_build_tree_device_f32",
 )
 
 

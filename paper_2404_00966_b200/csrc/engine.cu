@@ -19,6 +19,7 @@
 #include <chrono>
 #include <cstdlib>
 #include <cfloat>
+#include <climits>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -4681,3 +4682,5 @@ extern "C" int gts_pair_distances(int32_t metric, int64_t np, int64_t dim, const
 
 // multi-shard exchange + merge
 #include "sharded.cuh"
+// device bulk build
+#include "devbuild.cuh"

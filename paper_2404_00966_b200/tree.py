@@ -203,8 +203,10 @@ def _c_dataset(ds):
     return s, (mat, ids)
 
 
-def build(dataset, config=None, runtime=None, threads=0):
-    """Build a FlatPivotTree (tree.py:370-385) with the native builder."""
+def build(dataset, config=None, runtime=None, threads=0, device=None):
+    """Build a FlatPivotTree (tree.py:370-385) with the native builder:
+    host C++/OpenMP by default, or on GPU `device` (gts_build_tree_device;
+    edit / l1 / l2, the same tree bit for bit)."""
     config = config or TreeConfig()
     tree = FlatPivotTree(config, dataset)
     n = dataset.n
@@ -218,5 +220,8 @@ def build(dataset, config=None, runtime=None, threads=0):
     root_row = int(np.random.default_rng(config.seed).integers(0, n))
     ds, keep = _c_dataset(dataset)
     t = tree._c_tree()
-    _lib.check(_lib.lib().gts_build_tree(C.byref(ds), root_row, int(threads), C.byref(t)))
+    if device is None:
+        _lib.check(_lib.lib().gts_build_tree(C.byref(ds), root_row, int(threads), C.byref(t)))
+    else:
+        _lib.check(_lib.lib().gts_build_tree_device(C.byref(ds), root_row, int(device), C.byref(t)))
     return tree
