@@ -36,6 +36,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 ALPHA_WORDS = "abcdefghijklmnopqrstuvwxyz"
+GEN_SEED, QUERY_SEED = 12, 13   # device generator (gts_generate_clustered) seeds
 
 WORKLOADS = {
     # configs[1] -- the headline
@@ -55,6 +56,11 @@ WORKLOADS = {
     # configs[4] single shard: 32-d L1, 12.5M per GPU at 8 GPUs, kNN k=100
     "l1shard": dict(metric="l1", n=12_500_000, nq=100_000, dim=32, clusters=10_000, spread=0.05, noise=0.01,
                     radius=0.5, k=100, config_index=4),
+    # configs[4] whole: 32-d L1 n=100M, kNN k=100, 1M-query batch; the
+    # collection and the queries are generated on the device (Philox,
+    # gts_generate_clustered), one shard per GPU, built on the device
+    "l1_100m": dict(metric="l1", n=100_000_000, nq=1_000_000, dim=32, clusters=100_000, spread=0.05, noise=0.01,
+                    radius=0.5, k=100, config_index=4, device_gen=True, modes=(1,)),
 }
 
 
@@ -111,6 +117,11 @@ def make_workload(name, rank, args, world=1, keep_full=False):
     lo, hi = n_total * rank // world, n_total * (rank + 1) // world
     seed = 12
     full = {}
+    if w.get("device_gen"):
+        # generated on the device by Engine (no host copy of the collection)
+        w["ids"] = np.arange(lo, hi, dtype=np.int64)
+        w["n"], w["n_total"], w["shard"] = hi - lo, n_total, (lo, hi)
+        return w
     if w["metric"] == "edit":
         codes, off = gen_strings(n_total, seed, w["min_len"], w["max_len"], w["alphabet"])
         qcodes, qoff = string_queries(codes, off, w["nq"], 13, w["alphabet"])
@@ -269,6 +280,10 @@ class Engine:
         code = {"edit": 0, "l1": 1, "l2": 2}[w["metric"]]
         p = _lib.ptr
         n = w["n"]
+        self.modes = w.get("modes", (0, 1))
+        if w.get("device_gen"):
+            self._init_device_gen(w, device)
+            return
         if self.edit:
             self.ds = _lib.GtsDataset(code, n, 0, None, p(w["codes"], _lib._i32p), p(w["off"], _lib._i64p),
                                       p(w["ids"], _lib._i64p))
@@ -314,15 +329,74 @@ class Engine:
             self.qb = _lib.GtsQueryBatch(code, nq, w["dim"], p(w["q"], _lib._f64p), None, None)
         self.code = code
 
+    def _init_device_gen(self, w, device):
+        """Collection shard and query batch generated on the device
+        (gts_generate_clustered), tree built on the device from the float32
+        payloads (gts_build_tree_device_f32), index over them
+        (gts_index_create_f32dev): nothing of the collection touches the host."""
+        import torch
+        _lib, L, p = self._lib, self.L, self._lib.ptr
+        n, D, nq = w["n"], w["dim"], w["nq"]
+        code = {"l1": 1, "l2": 2}[w["metric"]]
+        dev = torch.device("cuda", device)
+        t0 = time.perf_counter()
+        x = torch.empty((max(n, 1), D), dtype=torch.float32, device=dev)
+        qd = torch.empty((max(nq, 1), D), dtype=torch.float32, device=dev)
+        st = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+        lo = w["shard"][0]
+        _lib.check(L.gts_generate_clustered(GEN_SEED, w["n_total"], D, w["clusters"], w["spread"], lo, n, 0, 0.0,
+                                            C.c_void_p(x.data_ptr()), st))
+        _lib.check(L.gts_generate_clustered(GEN_SEED, w["n_total"], D, w["clusters"], w["spread"], 0, nq, QUERY_SEED,
+                                            w["noise"], C.c_void_p(qd.data_ptr()), st))
+        torch.cuda.synchronize(dev)
+        self.gen_s = time.perf_counter() - t0
+        w["q"] = qd[:nq].double().cpu().numpy()
+        del qd
+        nc = 20
+        mh, sp = C.c_int64(), C.c_int64()
+        _lib.check(L.gts_tree_height(n, nc, C.byref(mh), C.byref(sp)))
+        levels = sp.value + 1
+        nodes = L.gts_node_count(levels, nc)
+        self.arrs = dict(
+            pivot_id=np.zeros(nodes + 1, np.int64), pivot_row=np.zeros(nodes + 1, np.int64),
+            pos=np.zeros(nodes + 1, np.int64), size=np.zeros(nodes + 1, np.int64),
+            min_dis=np.zeros(nodes + 1), max_dis=np.zeros(nodes + 1), rows=np.zeros(n, np.int64),
+            dis=np.zeros(n), tomb=np.zeros(n, np.uint8))
+        a = self.arrs
+        self.tree = _lib.GtsTree(nc, levels, sp.value, nodes, n, p(a["pivot_id"], _lib._i64p),
+                                 p(a["pivot_row"], _lib._i64p), p(a["pos"], _lib._i64p), p(a["size"], _lib._i64p),
+                                 p(a["min_dis"], _lib._f64p), p(a["max_dis"], _lib._f64p), p(a["rows"], _lib._i64p),
+                                 p(a["dis"], _lib._f64p), p(a["tomb"], _lib._u8p))
+        root_row = int(np.random.default_rng(0).integers(0, n))
+        t0 = time.perf_counter()
+        _lib.check(L.gts_build_tree_device_f32(code, n, D, C.c_void_p(x.data_ptr()), p(w["ids"], _lib._i64p),
+                                               root_row, device, C.byref(self.tree)))
+        self.build_s = time.perf_counter() - t0
+        self.build_where = "device (float32 payloads generated on the device)"
+        self.levels = levels
+        h = C.c_void_p()
+        t0 = time.perf_counter()
+        _lib.check(L.gts_index_create_f32dev(C.byref(self.tree), code, D, C.c_void_p(x.data_ptr()),
+                                             p(w["ids"], _lib._i64p), device, C.byref(h)))
+        self.upload_s = time.perf_counter() - t0
+        del x
+        torch.cuda.empty_cache()
+        self.ix = h
+        self.radii = np.full(nq, w["radius"], dtype=np.float64)
+        self.ks = np.full(nq, w["k"], dtype=np.int64)
+        self.qb = _lib.GtsQueryBatch(code, nq, D, p(w["q"], _lib._f64p), None, None)
+        self.code = code
+
     def upload(self, stream):
         q = C.c_void_p()
         self._lib.check(self.L.gts_queries_upload(self.ix, C.byref(self.qb), C.c_void_p(stream), C.byref(q)))
         self.q = q
 
     def step_device(self, stream):
-        """Range + kNN batch on device-resident queries; results stay in HBM."""
+        """Range + kNN batch (or the workload's modes) on device-resident
+        queries; results stay in HBM."""
         res = []
-        for mode in (0, 1):
+        for mode in self.modes:
             h = C.c_void_p()
             if mode == 0:
                 rc = self.L.gts_range_batch(self.ix, self.q, self._lib.ptr(self.radii, self._lib._f64p), 0, 1,
@@ -469,9 +543,10 @@ def run_ours(args, rank, world, local_rank):
     hs = eng.step_device(sp)
     torch.cuda.synchronize()
     totals = [eng.info(h)[1] for h in hs]
-    # the answers of the timed batch (range, kNN), kept for the parity check
-    gpu_answers = [eng.fetch(h, sp) for h in hs]
+    # the answers of the timed batch per mode (0 range, 1 kNN), kept for the parity check
+    gpu_answers = {m: eng.fetch(h, sp) for m, h in zip(eng.modes, hs)}
     eng.free(hs)
+    tot_of = dict(zip(eng.modes, totals))
 
     # timed region (value): inputs resident in HBM.  Each step ends with a
     # device sync (the step's answers are complete), as a serving loop would.
@@ -518,7 +593,8 @@ def run_ours(args, rank, world, local_rank):
 
     if rank != 0:
         return None
-    qps = 2 * nq / (ms / 1e3)
+    nmodes = len(eng.modes)
+    qps = nmodes * nq / (ms / 1e3)
     # the dominant leaf-verification kernel of this workload (whichever ran)
     cands = ("k_leafgroup_edit", "k_leaf_edit") if eng.edit else ("k_leafgroup_mma2", "k_leafgroup_mma", "k_leafgroup_tile", "k_leafgroup_vec", "k_verify")
     kname = max(cands, key=lambda k: prof["kernels"].get(k, {"ms": 0.0})["ms"])
@@ -526,7 +602,7 @@ def run_ours(args, rank, world, local_rank):
     work = prof["work"]
     step_ms_prof = sum(v["ms"] for v in prof["kernels"].values())
     out = {
-        "metric": "range+kNN queries/sec",
+        "metric": "range+kNN queries/sec" if nmodes == 2 else "kNN queries/sec",
         "value": round(qps, 3),
         "unit": "queries/s",
         "n_gpus": world,
@@ -541,21 +617,24 @@ def run_ours(args, rank, world, local_rank):
         "dtype": "u8 symbols / int32 bit-parallel DP" if eng.edit else "f32 screen + f64 exact recheck",
         "data": "synthetic",
         "config": bench_config(args, w, world),
-        "range_answers_per_step": totals[0],
-        "knn_answers_per_step": totals[1],
+        "range_answers_per_step": tot_of.get(0),
+        "knn_answers_per_step": tot_of.get(1),
         "distance_evals_per_s": round(work["pairs"] / (step_ms_prof / 1e3), 1) if step_ms_prof else None,
         "build_s": round(eng.build_s, 3),
         "build_where": eng.build_where,
         "index_upload_s": round(eng.upload_s, 3),
         "clocks": clk,
         "gpu_launches": int(launches),
-        "e2e": {"value": round(2 * nq / (e2e_ms / 1e3), 3), "unit": "queries/s",
+        "e2e": {"value": round(nmodes * nq / (e2e_ms / 1e3), 3), "unit": "queries/s",
                 "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "profile": prof,
     }
     out["roofline"] = roofline(eng, prof, kver, step_ms_prof)
     if world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"], out["parity"] = cpu_baseline(w, args, gpu_answers)
+        if w.get("device_gen"):
+            out["cpu_baseline"], out["parity"] = scan_baseline(w, gpu_answers, eng.modes)
+        else:
+            out["cpu_baseline"], out["parity"] = cpu_baseline(w, args, gpu_answers)
     return out
 
 
@@ -574,6 +653,7 @@ def run_sharded(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     w = make_workload(args.workload, rank, args, world, keep_full=(rank == 0 and not args.no_cpu_baseline))
+    want_parity = rank == 0 and not args.no_cpu_baseline
     eng = Engine(w, local_rank)
     stream = torch.cuda.Stream(dev)
     sp = stream.cuda_stream
@@ -581,10 +661,11 @@ def run_sharded(args, rank, world, local_rank):
     ss = ShardSearcher(eng.ix, dev, stream=sp)
     ex = ShardExchange(nq, dev)
     ks_dev = torch.from_numpy(eng.ks).to(dev)
+    nmodes = len(eng.modes)
 
     def one_step():
         with torch.cuda.stream(stream):
-            return sharded_step(ss, ex, eng.radii, eng.ks, ks_dev)
+            return sharded_step(ss, ex, eng.radii, eng.ks, ks_dev, eng.modes)
 
     with torch.cuda.stream(stream):
         ss.upload(eng.qb)
@@ -634,7 +715,7 @@ def run_sharded(args, rank, world, local_rank):
     def e2e_step():
         with torch.cuda.stream(stream):
             ss.upload(qb)
-            res = sharded_step(ss, ex, eng.radii, eng.ks, ks_dev)
+            res = sharded_step(ss, ex, eng.radii, eng.ks, ks_dev, eng.modes)
             b = 0
             for i, part in enumerate(res):
                 for j, tns in enumerate(part):
@@ -665,13 +746,14 @@ def run_sharded(args, rank, world, local_rank):
 
     # parity of rank 0's owned queries against brute force over the whole collection
     parity = None
-    if rank == 0 and "full" in w:
+    if want_parity:
         parity = sharded_parity(w, ex.own, own_answers)
     ss.free()
     if rank != 0:
         return None
     return {
-        "metric": "range+kNN queries/sec", "value": round(2 * nq / (ms / 1e3), 3), "unit": "queries/s",
+        "metric": "range+kNN queries/sec" if nmodes == 2 else "kNN queries/sec",
+        "value": round(nmodes * nq / (ms / 1e3), 3), "unit": "queries/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
         "step_ms_rank0": [round(x, 3) for x in step_ms], "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None,
@@ -679,8 +761,8 @@ def run_sharded(args, rank, world, local_rank):
         "data": "synthetic", "config": bench_config(args, w, world),
         "build_s_rank0": round(eng.build_s, 3), "index_upload_s_rank0": round(eng.upload_s, 3),
         "clocks": clk, "gpu_launches": int(launches),
-        "e2e": {"value": round(2 * nq / (e2e_ms / 1e3), 3), "unit": "queries/s", "ms_per_step": round(e2e_ms, 4),
-                "h2d_bytes_per_step": int(h2d + nq * 16), "d2h_bytes_per_step": int(d2h[0])},
+        "e2e": {"value": round(nmodes * nq / (e2e_ms / 1e3), 3), "unit": "queries/s", "ms_per_step": round(e2e_ms, 4),
+                "h2d_bytes_per_step": int(h2d + nq * 8 * nmodes), "d2h_bytes_per_step": int(d2h[0])},
         "parity": parity,
     }
 
@@ -689,12 +771,25 @@ def sharded_parity(w, own, answers, n_sample=32):
     """Rank 0's merged answers for a sample of its owned queries vs the
     oracle's brute force over the whole collection (oracle.py:19-36)."""
     from oracle import oracle as O
+    lo, hi = own
+    if w.get("device_gen"):
+        idx = np.sort(np.random.default_rng(0).choice(np.arange(lo, hi), size=min(n_sample, hi - lo), replace=False))
+        modes = w.get("modes", (0, 1))
+        want, _ = chunked_brute(w, idx, modes, os.cpu_count() or 1)
+        mism = 0
+        for m, (off, ids, dis) in zip(modes, answers):
+            for j, q in enumerate(idx):
+                a, b = off[q - lo], off[q - lo + 1]
+                if not (np.array_equal(ids[a:b], want[m][j][0]) and np.array_equal(dis[a:b], want[m][j][1])):
+                    mism += 1
+        return {"checked": len(modes) * idx.size, "mismatches": mism, "tolerated": 0,
+                "against": "oracle brute force over the whole (device-regenerated) collection, sample of rank 0's "
+                           "owned queries"}
     f = w["full"]
     if w["metric"] == "edit":
         data = O.Payloads(O.EDIT, codes=f["codes"], off=f["off"], ids=f["ids"])
     else:
         data = O.Payloads({"l1": O.L1, "l2": O.L2}[w["metric"]], vec=f["mat"], ids=f["ids"])
-    lo, hi = own
     rng = np.random.default_rng(0)
     idx = np.sort(rng.choice(np.arange(lo, hi), size=min(n_sample, hi - lo), replace=False))
     qs = oracle_queries(O, w, idx)
@@ -739,7 +834,7 @@ def run_e2e(eng, w, args, sp, max_total):
 
     def step():
         b = 0
-        for mode in (0, 1):
+        for mode in eng.modes:
             h = C.c_void_p()
             if mode == 0:
                 rc = L.gts_range_batch_host(eng.ix, C.byref(qb), C.cast(prad.data_ptr(), _lib._f64p), 0, 1,
@@ -766,7 +861,7 @@ def run_e2e(eng, w, args, sp, max_total):
         step()
     torch.cuda.synchronize()
     ms = (time.perf_counter() - t0) * 1e3 / args.steps
-    h2d = 2 * h2d_in + nq * 8 * 2
+    h2d = len(eng.modes) * (h2d_in + nq * 8)
     return ms, h2d, bytes_out[0]
 
 
@@ -931,6 +1026,71 @@ def parity_check(O, data, w, t, gpu_answers, threads):
     return out
 
 
+def chunked_brute(w, idx, modes, threads, chunk=1 << 23):
+    """Oracle brute force (oracle.py:19-47) over a device-generated
+    collection: chunks are regenerated on the device (the same Philox
+    stream), copied to the host as float64 and scanned; per-query answers
+    are merged by (distance, id) (k smallest for kNN).  Returns
+    ({mode: [(ids, dis)] per query}, scan seconds)."""
+    import torch
+    from oracle import oracle as O
+    from paper_2404_00966_b200 import _lib
+    met = {"l1": O.L1, "l2": O.L2}[w["metric"]]
+    qs = O.Payloads(met, vec=w["q"][idx])
+    parts = {m: [[] for _ in idx] for m in modes}
+    secs = 0.0
+    dev = torch.device("cuda", torch.cuda.current_device())
+    buf = torch.empty((chunk, w["dim"]), dtype=torch.float32, device=dev)
+    for a in range(0, w["n_total"], chunk):
+        b = min(w["n_total"], a + chunk)
+        _lib.check(_lib.lib().gts_generate_clustered(GEN_SEED, w["n_total"], w["dim"], w["clusters"], w["spread"],
+                                                     a, b - a, 0, 0.0, C.c_void_p(buf.data_ptr()), None))
+        torch.cuda.synchronize()
+        data = O.Payloads(met, vec=buf[:b - a].double().cpu().numpy(), ids=np.arange(a, b, dtype=np.int64))
+        t0 = time.perf_counter()
+        for m in modes:
+            r = O.brute(data, qs, m, radii=np.full(len(idx), w["radius"]), ks=np.full(len(idx), w["k"]),
+                        threads=threads)
+            for j, (ii, dd) in enumerate(r.answers()):
+                parts[m][j].append((ii, dd))
+        secs += time.perf_counter() - t0
+    out = {}
+    for m in modes:
+        lst = []
+        for j in range(len(idx)):
+            ii = np.concatenate([p[0] for p in parts[m][j]])
+            dd = np.concatenate([p[1] for p in parts[m][j]])
+            o = np.lexsort((ii, dd))
+            if m == 1:
+                o = o[: w["k"]]
+            lst.append((ii[o], dd[o]))
+        out[m] = lst
+    return out, secs
+
+
+def scan_baseline(w, gpu_answers, modes, n_sample=32):
+    """CPU baseline + parity for a device-generated collection: the oracle's
+    brute-force scan -- the reference's pruning-off mode (_scan_all,
+    search.py:338-355) -- on a sample of the batch, all host threads."""
+    thr = os.cpu_count() or 1
+    idx = np.sort(np.random.default_rng(0).choice(w["nq"], size=min(n_sample, w["nq"]), replace=False))
+    want, secs = chunked_brute(w, idx, modes, thr)
+    mism = 0
+    for m in modes:
+        off, ids, dis = gpu_answers[m]
+        for j, q in enumerate(idx):
+            if not (np.array_equal(ids[off[q]:off[q + 1]], want[m][j][0])
+                    and np.array_equal(dis[off[q]:off[q + 1]], want[m][j][1])):
+                mism += 1
+    cb = {"value": round(len(modes) * len(idx) / secs, 4), "unit": "queries/s", "cores": thr, "kind": "port",
+          "sample": f"{len(idx)} queries x {len(modes)} mode(s) of the batch, oracle brute-force scan over all "
+                    f"{w['n_total']} objects (the reference's pruning-off mode, search.py:338-355), {thr} threads; "
+                    "the collection regenerated in chunks (device Philox) and scanned in float64"}
+    par = {"checked": len(idx) * len(modes), "mismatches": mism, "tolerated": 0,
+           "against": "oracle brute force over the whole collection, (distance, id) lists"}
+    return cb, par
+
+
 def cpu_baseline(w, args, gpu_answers=None):
     O, data, tree, build_s = oracle_setup(w)
     threads = os.cpu_count() or 1
@@ -949,10 +1109,42 @@ def cpu_baseline(w, args, gpu_answers=None):
     return cb, par
 
 
+def run_reference_scan(args, w, world):
+    """Reference arm for a device-generated collection (configs[4] whole):
+    the oracle's brute-force scan (the reference's pruning-off mode,
+    search.py:338-355) over the collection, regenerated in chunks; one scan
+    serves every step's sample (4 queries per step)."""
+    import torch
+    from paper_2404_00966_b200 import _lib
+    torch.cuda.set_device(0)
+    nq = w["nq"]
+    qd = torch.empty((nq, w["dim"]), dtype=torch.float32, device="cuda")
+    _lib.check(_lib.lib().gts_generate_clustered(GEN_SEED, w["n_total"], w["dim"], w["clusters"], w["spread"], 0, nq,
+                                                 QUERY_SEED, w["noise"], C.c_void_p(qd.data_ptr()), None))
+    w["q"] = qd.double().cpu().numpy()
+    modes = w.get("modes", (0, 1))
+    idx = np.sort(np.random.default_rng(1).choice(nq, size=min(nq, 4 * args.steps), replace=False))
+    _, secs = chunked_brute(w, idx, modes, os.cpu_count() or 1)
+    v = len(modes) * len(idx) / secs
+    thr = os.cpu_count() or 1
+    return {
+        "impl": "reference", "metric": "range+kNN queries/sec" if len(modes) == 2 else "kNN queries/sec",
+        "value": round(v, 4), "unit": "queries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(secs / args.steps * 1e3, 3), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64 (CPU)", "data": "synthetic", "config": bench_config(args, w, world),
+        "cpu_baseline": {"value": round(v, 4), "unit": "queries/s", "cores": thr, "kind": "port",
+                         "sample": f"4 queries per step, oracle brute-force scan over all {w['n_total']} objects "
+                                   f"(pruning-off mode), {thr} threads"},
+        "e2e": {"value": round(v, 4), "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return None
     w = make_workload(args.workload, 0, args)
+    if w.get("device_gen"):
+        return run_reference_scan(args, w, world)
     O, data, tree, build_s = oracle_setup(w)
     threads = os.cpu_count() or 1
     n_r, n_k = (32, 32) if w["metric"] == "edit" else ((500, 500) if w["n"] <= 100_000 else (16, 16))

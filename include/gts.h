@@ -102,6 +102,21 @@ int gts_build_tree_device_f32(int32_t metric, int64_t n, int64_t dim, const floa
 typedef struct gts_index gts_index;
 int gts_index_create(const gts_dataset *ds, const gts_tree *tree, int device, gts_index **out);
 int gts_index_destroy(gts_index *ix);
+/* Index over device-resident float32 vectors x[n][dim] (dataset row order,
+ * on `device`): the same tables as gts_index_create, with the payload
+ * gathers done on the device.  Metrics l1, l2. */
+int gts_index_create_f32dev(const gts_tree *tree, int32_t metric, int64_t dim, const float *x,
+                            const int64_t *ids, int device, gts_index **out);
+/* Synthetic clustered float32 vectors on the device (SURVEY.md §8(d) C5,
+ * a generate_clustered-equivalent, data.py:403-412): object i of an n_total
+ * collection = centre[c] + N(0, spread), c uniform in [0, clusters), centres
+ * U(0,1]^dim, all from a counter-based Philox4x32-10 stream, so any range
+ * [first, first + count) is generated independently (one shard per GPU).
+ * query_seed != 0: query i = a uniformly drawn object + N(0, noise). */
+int gts_generate_clustered(uint64_t seed, int64_t n_total, int64_t dim, int64_t clusters, float spread,
+                           int64_t first, int64_t count, uint64_t query_seed, float noise, float *out,
+                           void *stream);
+
 /* tombstone marks in table order (tree.tombstone, updates.py:124-135) */
 int gts_index_set_tombstones(gts_index *ix, const uint8_t *tombstone, void *stream);
 

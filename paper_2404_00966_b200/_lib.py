@@ -97,6 +97,10 @@ def lib():
             "gts_build_tree_device": (C.c_int, [C.POINTER(GtsDataset), C.c_int64, C.c_int, C.POINTER(GtsTree)]),
             "gts_build_tree_device_f32": (C.c_int, [C.c_int32, C.c_int64, C.c_int64, v, _i64p, C.c_int64, C.c_int,
                                                     C.POINTER(GtsTree)]),
+            "gts_index_create_f32dev": (C.c_int, [C.POINTER(GtsTree), C.c_int32, C.c_int64, v, _i64p, C.c_int,
+                                                  C.POINTER(v)]),
+            "gts_generate_clustered": (C.c_int, [C.c_uint64, C.c_int64, C.c_int64, C.c_int64, C.c_float, C.c_int64,
+                                                 C.c_int64, C.c_uint64, C.c_float, v, v]),
             "gts_launch_count": (C.c_int64, []),
             "gts_profile_enable": (C.c_int, [C.c_int]),
             "gts_profile_read": (C.c_int, [C.c_char_p, C.c_int64, C.c_int]),
@@ -120,6 +124,7 @@ EXPORTED = (
     "gts_version", "gts_profile_enable", "gts_profile_read", "gts_bench_int_peak", "gts_batch_host",
     "gts_index_cache_set", "gts_knn_probe", "gts_knn_batch_bounded", "gts_merge_results", "gts_multi_create",
     "gts_multi_destroy", "gts_multi_batch_host", "gts_build_tree_device", "gts_build_tree_device_f32",
+    "gts_index_create_f32dev", "gts_generate_clustered",
 )
 
 

@@ -479,3 +479,199 @@ extern "C" int gts_build_tree_device_f32(int32_t metric, int64_t n, int64_t dim,
     return GTS_OK;
     ABI_END
 }
+
+// ---------------------------------------------------------------------------
+// Device-side synthetic data (a generate_clustered-
+// equivalent collection produced on the device with a counter-based RNG, so
+// a 100M x 32 collection never exists as a host array) and an index over
+// device-resident float32 vectors.
+// ---------------------------------------------------------------------------
+namespace {
+
+// Philox4x32-10 (Salmon, Moraes, Dror, Shaw, SC'11): counter-based, so any
+// object of the collection is generated independently from its index.
+__device__ __forceinline__ uint4 philox4x32(uint4 c, uint2 k)
+{
+#pragma unroll
+    for (int r = 0; r < 10; r++) {
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+        c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+        k.x += 0x9E3779B9u;
+        k.y += 0xBB67AE85u;
+    }
+    return c;
+}
+
+__device__ __forceinline__ float u01(uint32_t x) { return (float)((x >> 8) + 1u) * 0x1p-24f; }   // (0, 1]
+
+__device__ __forceinline__ void normals4(uint4 r, float *z)
+{
+    const float a = sqrtf(-2.f * logf(u01(r.x))), b = sqrtf(-2.f * logf(u01(r.z)));
+    float s0, c0, s1, c1;
+    sincospif(2.f * u01(r.y), &s0, &c0);
+    sincospif(2.f * u01(r.w), &s1, &c1);
+    z[0] = a * c0;
+    z[1] = a * s0;
+    z[2] = b * c1;
+    z[3] = b * s1;
+}
+
+// out[i] = object first+i (query_seed == 0): cluster c uniform in
+// [0, clusters), centre U(0,1]^D, member = centre + N(0, spread);
+// or query first+i (query_seed != 0): a uniformly drawn object + N(0, noise).
+__global__ void k_gen_clustered(uint2 key, int64_t n_total, int D, int64_t clusters, float spread, int64_t first,
+                                int64_t count, uint2 qkey, int query, float noise, float *out)
+{
+    const int g4 = (D + 3) >> 2;
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= count * g4) return;
+    const int64_t i = t / g4;
+    const int d4 = (int)(t - i * g4);
+    const uint64_t j = (uint64_t)(first + i);
+    uint64_t row = j;
+    if (query) {
+        const uint4 r = philox4x32(make_uint4((uint32_t)j, (uint32_t)(j >> 32), 0xA5A5A5A5u, 0u), qkey);
+        row = (((uint64_t)r.x << 32) | r.y) % (uint64_t)n_total;
+    }
+    const uint4 a = philox4x32(make_uint4((uint32_t)row, (uint32_t)(row >> 32), 0xC1u, 0u), key);
+    const uint64_t c = (((uint64_t)a.x << 32) | a.y) % (uint64_t)clusters;
+    const uint4 cu = philox4x32(make_uint4((uint32_t)c, (uint32_t)(c >> 32), (uint32_t)d4, 0xCEu), key);
+    float z[4], w[4] = {0.f, 0.f, 0.f, 0.f};
+    normals4(philox4x32(make_uint4((uint32_t)row, (uint32_t)(row >> 32), (uint32_t)d4, 0x4Eu), key), z);
+    if (query) normals4(philox4x32(make_uint4((uint32_t)j, (uint32_t)(j >> 32), (uint32_t)d4, 0x51u), qkey), w);
+    const float cen[4] = {u01(cu.x), u01(cu.y), u01(cu.z), u01(cu.w)};
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const int d = d4 * 4 + k;
+        if (d < D) {
+            float v = __fadd_rn(cen[k], __fmul_rn(spread, z[k]));
+            if (query) v = __fadd_rn(v, __fmul_rn(noise, w[k]));
+            out[i * D + d] = v;
+        }
+    }
+}
+
+__global__ void k_gather_rows_f32(const float *__restrict__ x, int D, int Dp, const int32_t *__restrict__ drow,
+                                  int64_t n, float *v32)
+{
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n * Dp) return;
+    const int64_t e = t / Dp;
+    const int d = (int)(t - e * Dp);
+    v32[t] = d < D ? x[(int64_t)drow[e] * D + d] : 0.f;
+}
+
+// tensor-core copy (k_leafgroup_mma2): bf16(o - leaf pivot), K padded to Dk
+__global__ void k_vcent(const float *__restrict__ v32, int D, int Dp, int Dk, const int32_t *__restrict__ epiv,
+                        int64_t n, __nv_bfloat16 *vc)
+{
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n * Dk) return;
+    const int64_t e = t / Dk;
+    const int d = (int)(t - e * Dk);
+    const int p = epiv[e];
+    vc[t] = __float2bfloat16(d < D && p >= 0 ? v32[e * Dp + d] - v32[(int64_t)p * Dp + d] : 0.f);
+}
+
+// se_e = c . bf16(o_e - c) accumulated in float64 in index order (the
+// host's loop, gts_index_create)
+__global__ void k_vse(const float *__restrict__ v32, int D, int Dp, int Dk, const int32_t *__restrict__ epiv,
+                      const __nv_bfloat16 *__restrict__ vc, int64_t n, float *se)
+{
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= n) return;
+    const int p = epiv[e];
+    double acc = 0.0;
+    if (p >= 0)
+        for (int d = 0; d < D; d++)
+            acc = __dadd_rn(acc, __dmul_rn((double)v32[(int64_t)p * Dp + d], (double)__bfloat162float(vc[e * Dk + d])));
+    se[e] = (float)acc;
+}
+
+}  // namespace
+
+extern "C" int gts_generate_clustered(uint64_t seed, int64_t n_total, int64_t dim, int64_t clusters, float spread,
+                                      int64_t first, int64_t count, uint64_t query_seed, float noise, float *out,
+                                      void *stream)
+{
+    ABI_BEGIN
+    if (!out || dim < 1 || clusters < 1 || n_total < 1 || first < 0 || count < 0) fail(GTS_EINVAL, "invalid arguments");
+    if (count == 0) return GTS_OK;
+    const int64_t work = count * ((dim + 3) / 4);
+    k_gen_clustered<<<grid_for(work, 256), 256, 0, (cudaStream_t)stream>>>(
+        make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)), n_total, (int)dim, clusters, spread, first, count,
+        make_uint2((uint32_t)query_seed, (uint32_t)(query_seed >> 32)), query_seed != 0, noise, out);
+    LAUNCH_CHECK();
+    return GTS_OK;
+    ABI_END
+}
+
+// Index over device-resident float32 vectors x[n][dim] (dataset row order,
+// on `device`); tree: host arrays of the collection's tree; ids: host [n].
+extern "C" int gts_index_create_f32dev(const gts_tree *t, int32_t metric, int64_t dim, const float *x,
+                                       const int64_t *ids, int device, gts_index **out)
+{
+    ABI_BEGIN
+    if (!t || !x || !ids || !out) fail(GTS_EINVAL, "null argument");
+    if (metric != GTS_L1 && metric != GTS_L2) fail(GTS_EMETRIC, "device-resident vectors: l1 or l2");
+    if (t->n > (1ll << 31) - 64) fail(GTS_EINVAL, "index larger than 2^31 entries; shard it");
+    prime_pool(device);
+    CK(cudaSetDevice(device));
+    auto *ix = new gts_index();
+    try {
+        cudaStream_t st = 0;
+        ix->device = device;
+        ix->metric = metric;
+        ix->n = t->n;
+        ix->nc = (int)t->nc;
+        ix->levels = (int)t->levels;
+        ix->split_rounds = (int)t->split_rounds;
+        ix->nodes = t->nodes;
+        ix->D = (int)dim;
+        ix->Dp = (ix->D + 3) & ~3;
+        const int64_t n = t->n;
+        if (n == 0 || t->levels == 0) { *out = ix; return GTS_OK; }
+        std::vector<int64_t> ord((size_t)n), drow;
+        for (int64_t e = 0; e < n; e++) ord[(size_t)e] = e;
+        std::vector<NodeRec> nodes;
+        upload_tables(ix, t, ord, ids, st, drow, nodes);
+        ix->data_exact = true;   // float32 payloads: the fp32 copy is exact
+        ix->vec32.alloc((size_t)(n * ix->Dp), st);
+        k_gather_rows_f32<<<grid_for(n * ix->Dp, 256), 256, 0, st>>>(x, ix->D, ix->Dp, ix->row.p, n, ix->vec32.p);
+        LAUNCH_CHECK();
+        if (metric == GTS_L2 && ix->D >= 32 && ix->D <= 128 && ix->max_leaf <= 256 &&
+            std::getenv("GTS_NO_MMA") == nullptr) {
+            ix->Dk = (ix->D + 63) & ~63;
+            std::vector<int32_t> epiv((size_t)n, -1);
+            for (int64_t i = ix->leaf_first; i < (int64_t)ix->leaf_first + ix->leaf_count; i++)
+                for (int64_t e = t->pos[i]; e < t->pos[i] + t->size[i]; e++) epiv[(size_t)e] = nodes[(size_t)i].piv;
+            DBuf<int32_t> dep;
+            h2d_vec(dep, epiv, st);
+            const size_t tail = (size_t)16 * ix->Dk / 8;
+            ix->vcent.alloc((size_t)n * ix->Dk / 8 + tail, st);
+            CK(cudaMemsetAsync(ix->vcent.p, 0, ((size_t)n * ix->Dk / 8 + tail) * sizeof(uint4), st));
+            auto *vc = reinterpret_cast<__nv_bfloat16 *>(ix->vcent.p);
+            k_vcent<<<grid_for(n * ix->Dk, 256), 256, 0, st>>>(ix->vec32.p, ix->D, ix->Dp, ix->Dk, dep.p, n, vc);
+            LAUNCH_CHECK();
+            ix->vse.alloc((size_t)n, st);
+            k_vse<<<grid_for(n, 256), 256, 0, st>>>(ix->vec32.p, ix->D, ix->Dp, ix->Dk, dep.p, vc, n, ix->vse.p);
+            LAUNCH_CHECK();
+        }
+        CK(cudaStreamSynchronize(st));
+        // max |x| (used only by inexact data's slack; kept for completeness)
+        ix->data_maxabs = 0.f;
+        const int64_t prow = t->pivot_row[1];
+        if (prow >= 0 && prow < n) {
+            std::vector<float> r32((size_t)ix->D);
+            CK(cudaMemcpy(r32.data(), x + prow * ix->D, sizeof(float) * ix->D, cudaMemcpyDeviceToHost));
+            root_radius_of(ix, std::vector<double>(r32.begin(), r32.end()), st);
+        }
+        *out = ix;
+        return GTS_OK;
+    } catch (...) {
+        delete ix;
+        throw;
+    }
+    ABI_END
+}

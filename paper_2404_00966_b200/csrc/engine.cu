@@ -3900,14 +3900,124 @@ gts_result *run_search(gts_index *ix, const gts_queries *q, int mode, const doub
 
 }  // namespace
 
+// The tables every index has, from the host tree arrays (reference
+// tree.py:155-175): node records with fp32 ranges rounded outward, node
+// positions, live leaves, entry rows / pivot distances / ids / alive bits
+// in device table order (ord[e] = reference table position of entry e).
+void upload_tables(gts_index *ix, const gts_tree *t, const std::vector<int64_t> &ord, const int64_t *row_ids,
+                   cudaStream_t st, std::vector<int64_t> &drow, std::vector<NodeRec> &nodes)
+{
+    const int64_t n = t->n;
+    drow.assign((size_t)n, 0);
+    std::vector<int32_t> tpos((size_t)n);
+    #pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < n; e++) drow[(size_t)e] = t->rows[ord[(size_t)e]];
+    ix->ord = ord;
+    #pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < n; e++) tpos[(size_t)drow[(size_t)e]] = (int32_t)e;
+    nodes.assign((size_t)t->nodes + 1, NodeRec{});
+    std::vector<int32_t> npos((size_t)t->nodes + 1);
+    for (int64_t i = 0; i <= t->nodes; i++) {
+        NodeRec r;
+        float mn = (float)t->min_dis[i], mx = (float)t->max_dis[i];
+        if ((double)mn > t->min_dis[i]) mn = std::nextafter(mn, -INFINITY);
+        if ((double)mx < t->max_dis[i]) mx = std::nextafter(mx, INFINITY);
+        r.mn = mn;
+        r.mx = mx;
+        r.size = (int32_t)t->size[i];
+        r.piv = t->pivot_row[i] >= 0 ? tpos[(size_t)t->pivot_row[i]] : -1;
+        nodes[(size_t)i] = r;
+        npos[(size_t)i] = (int32_t)t->pos[i];
+    }
+    ix->node.alloc(nodes.size(), st);
+    h2d(ix->node.p, nodes.data(), nodes.size(), st);
+    ix->npos.alloc(npos.size(), st);
+    h2d(ix->npos.p, npos.data(), npos.size(), st);
+    // live leaves (for pruning-disabled scans)
+    {
+        __int128 c = 1;
+        for (int l = 1; l < ix->levels; l++) c *= ix->nc;
+        const int64_t first = (int64_t)((c - 1) / (ix->nc - 1) + 1), count = (int64_t)c;
+        std::vector<int32_t> lv;
+        for (int64_t i = first; i < first + count; i++) if (t->size[i] > 0) lv.push_back((int32_t)i);
+        ix->n_live_leaves = (int)lv.size();
+        ix->live_leaves.alloc(std::max<size_t>(lv.size(), 1), st);
+        h2d(ix->live_leaves.p, lv.data(), lv.size(), st);
+        for (int64_t i = first; i < first + count; i++) ix->max_leaf = std::max<int>(ix->max_leaf, (int)t->size[i]);
+        ix->leaf_first = (int)first;
+        ix->leaf_count = (int)count;
+    }
+    {
+        std::vector<int32_t> row((size_t)n);
+        #pragma omp parallel for schedule(static)
+        for (int64_t e = 0; e < n; e++) row[(size_t)e] = (int32_t)drow[(size_t)e];
+        ix->row.alloc((size_t)n, st);
+        h2d(ix->row.p, row.data(), (size_t)n, st);
+    }
+    std::vector<float> dis((size_t)n);
+    std::vector<int64_t> ids((size_t)n);
+    std::vector<uint32_t> alive((size_t)((n + 31) / 32), 0u);
+    #pragma omp parallel for schedule(static)
+    for (int64_t w = 0; w < (n + 31) / 32; w++) {
+        uint32_t bits = 0;
+        for (int64_t e = w * 32; e < std::min<int64_t>(n, w * 32 + 32); e++) {
+            const int64_t o = ord[(size_t)e];
+            dis[(size_t)e] = (float)t->dis[o];
+            ids[(size_t)e] = row_ids[drow[(size_t)e]];
+            if (!t->tombstone || t->tombstone[o] == 0) bits |= 1u << (e & 31);
+        }
+        alive[(size_t)w] = bits;
+    }
+    ix->dis.alloc((size_t)n, st);
+    h2d(ix->dis.p, dis.data(), (size_t)n, st);
+    ix->ids.alloc((size_t)n, st);
+    h2d(ix->ids.p, ids.data(), (size_t)n, st);
+    ix->alive.alloc(alive.size(), st);
+    h2d(ix->alive.p, alive.data(), alive.size(), st);
+}
+
+// Device memory pool of an index's device: keep freed blocks mapped and
+// map a large block once (see below).
+void prime_pool(int device)
+{
+    // search scratch comes from the device's default stream-ordered pool;
+    // keep freed blocks mapped between calls instead of unmapping them at
+    // every synchronisation (release threshold 0 is the CUDA default)
+    CK(cudaSetDevice(device));
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        // Prime the pool once: map a large block up front so batch-sized
+        // scratch (frontier tables, hit / candidate buffers, sort space:
+        // GBs for 100k-query kNN) is carved from mapped memory instead of
+        // growing the pool -- mapping new physical memory mid-call costs
+        // 100s of ms.  GTS_POOL_PRIME_GB overrides (0 = off).
+        const char *env = std::getenv("GTS_POOL_PRIME_GB");
+        size_t free_b = 0, total_b = 0;
+        cudaMemGetInfo(&free_b, &total_b);
+        size_t want = env ? (size_t)std::atoll(env) << 30 : std::min<size_t>((size_t)24 << 30, total_b / 6);
+        uint64_t reserved = 0;
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+        if (want > reserved && want < free_b / 2) {
+            void *p = nullptr;
+            if (cudaMallocAsync(&p, want, 0) == cudaSuccess) {
+                cudaFreeAsync(p, 0);
+                cudaStreamSynchronize(0);
+            }
+            cudaGetLastError();
+        }
+    }
+}
+
 // fp32 radius of the collection around the root pivot (k_root_radius):
 // the root pivot's payload is uploaded as a one-row query batch.
-void compute_root_radius(gts_index *ix, const gts_dataset *ds, const gts_tree *t, cudaStream_t st)
+void compute_root_radius(gts_index *ix, const gts_dataset *ds, const gts_tree *t, cudaStream_t st);
+
+void root_radius_of(gts_index *ix, std::vector<double> payload, cudaStream_t st)
 {
-    const int64_t prow = t->pivot_row[1];
-    if (prow < 0 || prow >= ds->n) return;
-    ix->root_payload.assign(ds->vectors + prow * ix->D, ds->vectors + (prow + 1) * ix->D);
-    gts_query_batch qb{ds->metric, 1, ix->D, ix->root_payload.data(), nullptr, nullptr};
+    ix->root_payload = std::move(payload);
+    gts_query_batch qb{ix->metric, 1, ix->D, ix->root_payload.data(), nullptr, nullptr};
     gts_queries *q = upload_queries(ix, &qb, st);
     DBuf<unsigned> m(1, st);
     CK(cudaMemsetAsync(m.p, 0, sizeof(unsigned), st));
@@ -3927,6 +4037,13 @@ void compute_root_radius(gts_index *ix, const gts_dataset *ds, const gts_tree *t
     float r;
     std::memcpy(&r, &h, sizeof(r));
     ix->root_radius = r;
+}
+
+void compute_root_radius(gts_index *ix, const gts_dataset *ds, const gts_tree *t, cudaStream_t st)
+{
+    const int64_t prow = t->pivot_row[1];
+    if (prow < 0 || prow >= ds->n) return;
+    root_radius_of(ix, std::vector<double>(ds->vectors + prow * ix->D, ds->vectors + (prow + 1) * ix->D), st);
 }
 
 // float64 radius of the pending cache around the root pivot, rounded up
@@ -4073,36 +4190,10 @@ extern "C" int gts_bench_int_peak(double *ops_per_s, void *stream)
 extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int device, gts_index **out)
 {
     ABI_BEGIN
-    {
-        // search scratch comes from the device's default stream-ordered pool;
-        // keep freed blocks mapped between calls instead of unmapping them at
-        // every synchronisation (release threshold 0 is the CUDA default)
-        CK(cudaSetDevice(device));
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-            uint64_t thr = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-            // Prime the pool once: map a large block up front so batch-sized
-            // scratch (frontier tables, hit / candidate buffers, sort space:
-            // GBs for 100k-query kNN) is carved from mapped memory instead of
-            // growing the pool -- mapping new physical memory mid-call costs
-            // 100s of ms.  GTS_POOL_PRIME_GB overrides (0 = off).
-            const char *env = std::getenv("GTS_POOL_PRIME_GB");
-            size_t free_b = 0, total_b = 0;
-            cudaMemGetInfo(&free_b, &total_b);
-            size_t want = env ? (size_t)std::atoll(env) << 30 : std::min<size_t>((size_t)24 << 30, total_b / 6);
-            uint64_t reserved = 0;
-            cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
-            if (want > reserved && want < free_b / 2) {
-                void *p = nullptr;
-                if (cudaMallocAsync(&p, want, 0) == cudaSuccess) {
-                    cudaFreeAsync(p, 0);
-                    cudaStreamSynchronize(0);
-                }
-                cudaGetLastError();
-            }
-        }
-    }
+    static const bool trace = std::getenv("GTS_TRACE") != nullptr;
+    const double c0 = trace ? now_ms() : 0.0;
+    prime_pool(device);
+    const double c1 = trace ? now_ms() : 0.0;
     if (!ds || !t || !out) fail(GTS_EINVAL, "null argument");
     if (ds->metric != GTS_EDIT && ds->metric != GTS_L1 && ds->metric != GTS_L2 && ds->metric != GTS_ANGULAR)
         fail(GTS_EMETRIC, "metric %d not supported on the device path (edit, l1, l2, angular)", ds->metric);
@@ -4130,8 +4221,6 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
         ix->nodes = t->nodes;
         const int64_t n = ds->n;
         if (n == 0 || t->levels == 0) { *out = ix; return GTS_OK; }
-        // inverse permutation: table position of each dataset row
-        std::vector<int32_t> tpos((size_t)n);
         // Device table order: the reference table order, except that string
         // entries are stably sorted by length inside each leaf (leaves are
         // scanned, never ordered, search.py:518-524), so DP lanes of a warp
@@ -4155,63 +4244,10 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
                     });
             }
         }
-        std::vector<int64_t> drow((size_t)n);
-        for (int64_t e = 0; e < n; e++) drow[(size_t)e] = t->rows[ord[(size_t)e]];
-        ix->ord = ord;
-        for (int64_t e = 0; e < n; e++) tpos[(size_t)drow[(size_t)e]] = (int32_t)e;
-        std::vector<NodeRec> nodes((size_t)t->nodes + 1);
-        std::vector<int32_t> npos((size_t)t->nodes + 1);
-        for (int64_t i = 0; i <= t->nodes; i++) {
-            NodeRec r;
-            float mn = (float)t->min_dis[i], mx = (float)t->max_dis[i];
-            if ((double)mn > t->min_dis[i]) mn = std::nextafter(mn, -INFINITY);
-            if ((double)mx < t->max_dis[i]) mx = std::nextafter(mx, INFINITY);
-            r.mn = mn;
-            r.mx = mx;
-            r.size = (int32_t)t->size[i];
-            r.piv = t->pivot_row[i] >= 0 ? tpos[(size_t)t->pivot_row[i]] : -1;
-            nodes[(size_t)i] = r;
-            npos[(size_t)i] = (int32_t)t->pos[i];
-        }
-        ix->node.alloc(nodes.size(), st);
-        h2d(ix->node.p, nodes.data(), nodes.size(), st);
-        ix->npos.alloc(npos.size(), st);
-        h2d(ix->npos.p, npos.data(), npos.size(), st);
-        // live leaves (for pruning-disabled scans)
-        {
-            __int128 c = 1;
-            for (int l = 1; l < ix->levels; l++) c *= ix->nc;
-            const int64_t first = (int64_t)((c - 1) / (ix->nc - 1) + 1), count = (int64_t)c;
-            std::vector<int32_t> lv;
-            for (int64_t i = first; i < first + count; i++) if (t->size[i] > 0) lv.push_back((int32_t)i);
-            ix->n_live_leaves = (int)lv.size();
-            ix->live_leaves.alloc(std::max<size_t>(lv.size(), 1), st);
-            h2d(ix->live_leaves.p, lv.data(), lv.size(), st);
-            for (int64_t i = first; i < first + count; i++) ix->max_leaf = std::max<int>(ix->max_leaf, (int)t->size[i]);
-            ix->leaf_first = (int)first;
-            ix->leaf_count = (int)count;
-        }
-        {
-            std::vector<int32_t> row((size_t)n);
-            for (int64_t e = 0; e < n; e++) row[(size_t)e] = (int32_t)drow[(size_t)e];
-            ix->row.alloc((size_t)n, st);
-            h2d(ix->row.p, row.data(), (size_t)n, st);
-        }
-        std::vector<float> dis((size_t)n);
-        std::vector<int64_t> ids((size_t)n);
-        std::vector<uint32_t> alive((size_t)((n + 31) / 32), 0u);
-        for (int64_t e = 0; e < n; e++) {
-            const int64_t o = ord[(size_t)e];
-            dis[(size_t)e] = (float)t->dis[o];
-            ids[(size_t)e] = ds->ids[drow[(size_t)e]];
-            if (!t->tombstone || t->tombstone[o] == 0) alive[(size_t)(e >> 5)] |= 1u << (e & 31);
-        }
-        ix->dis.alloc((size_t)n, st);
-        h2d(ix->dis.p, dis.data(), (size_t)n, st);
-        ix->ids.alloc((size_t)n, st);
-        h2d(ix->ids.p, ids.data(), (size_t)n, st);
-        ix->alive.alloc(alive.size(), st);
-        h2d(ix->alive.p, alive.data(), alive.size(), st);
+        std::vector<int64_t> drow;
+        std::vector<NodeRec> nodes;
+        upload_tables(ix, t, ord, ds->ids, st, drow, nodes);
+        const double c2 = trace ? now_ms() : 0.0;
         if (ds->metric == GTS_EDIT) {
             const int64_t ncodes = ds->offsets[n];
             std::vector<int32_t> alpha;
@@ -4235,6 +4271,7 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
             ix->slen.alloc(lens.size(), st);
             h2d(ix->slen.p, lens.data(), lens.size(), st);
             std::vector<uint4> rec((size_t)n);
+            #pragma omp parallel for schedule(static)
             for (int64_t e = 0; e < n; e++) {
                 float d = (float)t->dis[ord[(size_t)e]];
                 uint32_t db;
@@ -4257,6 +4294,7 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
             if (ix->A > kHistMinAlphabet) {
                 // 32 byte-buckets of symbol counts per entry (saturating)
                 std::vector<uint8_t> hb((size_t)n * 32, 0);
+                #pragma omp parallel for schedule(static, 4096)
                 for (int64_t e = 0; e < n; e++) {
                     const int64_t r = drow[(size_t)e];
                     uint8_t *h = hb.data() + e * 32;
@@ -4276,6 +4314,7 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
             std::vector<float> v32((size_t)(n * ix->Dp), 0.f);
             bool exact = true;
             float mx = 0.f;
+            #pragma omp parallel for schedule(static, 4096) reduction(&& : exact) reduction(max : mx)
             for (int64_t e = 0; e < n; e++) {
                 const double *src = ds->vectors + drow[(size_t)e] * ix->D;
                 for (int d = 0; d < ix->D; d++) {
@@ -4295,6 +4334,7 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
                 __int128 c = 1;
                 for (int l = 1; l < ix->levels; l++) c *= ix->nc;
                 const int64_t lfirst = (int64_t)((c - 1) / (ix->nc - 1) + 1), lcount = (int64_t)c;
+                #pragma omp parallel for schedule(dynamic, 64)
                 for (int64_t i = lfirst; i < lfirst + lcount; i++) {
                     const int64_t p0 = t->pos[i], sz = t->size[i];
                     if (sz <= 0) continue;
@@ -4307,6 +4347,7 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
                 // se_e = c . bf16(o_e - c): the pivot term of the uncentred
                 // query product (k_leafgroup_mma2), from the same rounded values
                 std::vector<float> se((size_t)n, 0.f);
+                #pragma omp parallel for schedule(dynamic, 64)
                 for (int64_t i = lfirst; i < lfirst + lcount; i++) {
                     const int64_t p0 = t->pos[i], sz = t->size[i];
                     if (sz <= 0) continue;
@@ -4346,6 +4387,7 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
             h2d(ix->vec32.p, v32.data(), v32.size(), st);
             if (!exact) {
                 std::vector<double> v64((size_t)(n * ix->D));
+                #pragma omp parallel for schedule(static, 4096)
                 for (int64_t e = 0; e < n; e++)
                     std::memcpy(v64.data() + e * ix->D, ds->vectors + drow[(size_t)e] * ix->D, sizeof(double) * ix->D);
                 ix->vec64.alloc(v64.size(), st);
@@ -4353,7 +4395,11 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
             }
         }
         CK(cudaStreamSynchronize(st));
+        const double c3 = trace ? now_ms() : 0.0;
         if (ds->metric != GTS_EDIT && n > 0 && ix->levels > 0) compute_root_radius(ix, ds, t, st);
+        if (trace)
+            fprintf(stderr, "[gts] index_create n=%lld pool=%.1fms tables=%.1fms payload=%.1fms root=%.1fms\n",
+                    (long long)n, c1 - c0, c2 - c1, c3 - c2, now_ms() - c3);
         *out = ix;
         return GTS_OK;
     } catch (...) {

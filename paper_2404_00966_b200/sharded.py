@@ -227,15 +227,19 @@ class ShardSearcher:
         return result_tensors(h, self.device, self.stream)
 
 
-def sharded_step(searcher, exchange, radii, ks, ks_dev):
-    """One replicated batch over a sharded collection: range answers and kNN
-    answers (probe -> MIN bound -> bounded search), each merged on its
-    owner.  Returns ((offsets, ids, dis) range, (offsets, ids, dis) kNN) for
-    this rank's query slice."""
-    rng = exchange.merge_range(*searcher.range(radii))
-    r = exchange.knn_bound(searcher.probe(ks))
-    knn = exchange.merge_knn(*searcher.knn(ks, r), ks_dev)
-    return rng, knn
+def sharded_step(searcher, exchange, radii, ks, ks_dev, modes=(0, 1)):
+    """One replicated batch over a sharded collection: range answers (mode 0)
+    and kNN answers (mode 1: probe -> MIN bound -> bounded search), each
+    merged on its owner.  Returns one (offsets, ids, dis) per mode for this
+    rank's query slice."""
+    out = []
+    for m in modes:
+        if m == 0:
+            out.append(exchange.merge_range(*searcher.range(radii)))
+        else:
+            r = exchange.knn_bound(searcher.probe(ks))
+            out.append(exchange.merge_knn(*searcher.knn(ks, r), ks_dev))
+    return tuple(out)
 
 
 # ---------------------------------------------------------------------------
