@@ -630,6 +630,8 @@ def run_ours(args, rank, world, local_rank):
         "profile": prof,
     }
     out["roofline"] = roofline(eng, prof, kver, step_ms_prof)
+    out["roofline"]["traversal"] = traversal_roofline(prof, args.workload)
+    out["roofline"]["traffic"] = ncu_traffic(args.workload, kname)
     if world == 1 and not args.no_cpu_baseline:
         if w.get("device_gen"):
             out["cpu_baseline"], out["parity"] = scan_baseline(w, gpu_answers, eng.modes)
@@ -906,13 +908,16 @@ def roofline(eng, prof, kver, step_ms_prof):
         # register-tiled fp32 distances for every (query, entry) pair of an item:
         # 2 fp32 ops per dimension (L1: sub, |.|-add; L2: sub, fma counted once)
         ops = work["entries"] * 2 * D
-        pk = 148 * 128 * 1.965e9 / 1e12
+        fp = C.c_double()
+        _lib.check(_lib.lib().gts_bench_fp32_peak(C.byref(fp), None))
+        pk = fp.value / 1e12
         achieved = ops / t / 1e12 if t else None
         return dict(common, **{
             "bound": "fp32", "achieved": round(achieved, 3) if achieved else None, "peak": round(pk, 2),
             "unit": "Tops/s", "frac": round(achieved / pk, 4) if achieved else None, "traffic": None,
             "work_unit": f"2*D = {2 * D} fp32 lane-ops per (query, entry) pair of an item",
-            "peak_source": "B200 nominal fp32 issue: 148 SMs x 128 lanes x 1.965 GHz (one op per lane per clock)"})
+            "peak_source": "gts_bench_fp32_peak: best of FADD-only / FFMA-only 16-chain loops on all SMs, measured "
+                           "in this run (MEASURED_PEAKS.json has no fp32 peak)"})
     hbm = peaks.get("hbm_gbs", 6650.0)
     bytes_alg = work["entries"] * 8 + work["pairs"] * 4 * D
     achieved = bytes_alg / t / 1e9 if t else None
@@ -921,6 +926,38 @@ def roofline(eng, prof, kver, step_ms_prof):
         "frac": round(achieved / hbm, 4) if achieved else None, "traffic": None,
         "work_unit": "8 B per (query, entry) scanned + 4*D B per lemma-1-passing pair",
         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s (B200_PROFILING.md)"})
+
+
+def traversal_roofline(prof, workload):
+    """HBM roofline of the list-table traversal (k_expand / k_expand_grouped,
+    search.py:405-477): algorithmic bytes per SURVEY.md §8(d) (parent row,
+    N_c 16-byte child records, the evaluated children's pivot payloads, the
+    emitted 16-byte rows) / the launches' device time."""
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peaks = json.load(open(peaks_path)) if os.path.exists(peaks_path) else {}
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    k = prof["kernels"].get("k_expand")
+    ex = prof.get("expand", {})
+    if not k or not k["ms"]:
+        return None
+    gbs = ex.get("bytes", 0) / (k["ms"] / 1e3) / 1e9
+    out = {"kernel": "k_expand", "launches_per_step": k["count"], "ms_per_step": round(k["ms"], 4),
+           "bytes_per_step": int(ex.get("bytes", 0)), "rows_in": int(ex.get("rows_in", 0)),
+           "rows_out": int(ex.get("rows_out", 0)), "bound": "hbm", "achieved": round(gbs, 2), "peak": hbm,
+           "unit": "GB/s", "frac": round(gbs / hbm, 4),
+           "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s (B200_PROFILING.md)"}
+    out["traffic"] = ncu_traffic(workload, "k_expand")
+    return out
+
+
+def ncu_traffic(workload, kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`
+    from the committed ncu --set full capture summary (profiles/), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(path):
+        return None
+    tab = json.load(open(path))
+    return tab.get(f"{workload}:{kernel}")
 
 
 # Algorithmic integer ops per word-step: the 10-op Hyyro recurrence (DESIGN.md).

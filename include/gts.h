@@ -227,6 +227,8 @@ int gts_pair_distances(int32_t metric, int64_t npairs, int64_t dim,
                        const int32_t *b_codes, const int64_t *b_off,
                        double *out, void *stream);
 
+/* Number of visible CUDA devices (0 when none). */
+int gts_device_count(void);
 /* Count of this library's kernel launches since load (bench evidence). */
 int64_t gts_launch_count(void);
 /* Per-kernel CUDA-event timing + algorithmic work counters (bench.py's
@@ -235,6 +237,8 @@ int gts_profile_enable(int on);
 int gts_profile_read(char *buf, int64_t cap, int reset);
 /* Integer-pipe throughput microbenchmark (LOP3 + IMAD chains), ops/s. */
 int gts_bench_int_peak(double *ops_per_s, void *stream);
+/* FP32-pipe throughput microbenchmark (FADD / FFMA chains), lane-ops/s. */
+int gts_bench_fp32_peak(double *ops_per_s, void *stream);
 const char *gts_last_error(void);
 const char *gts_version(void);
 

@@ -102,9 +102,11 @@ def lib():
             "gts_generate_clustered": (C.c_int, [C.c_uint64, C.c_int64, C.c_int64, C.c_int64, C.c_float, C.c_int64,
                                                  C.c_int64, C.c_uint64, C.c_float, v, v]),
             "gts_launch_count": (C.c_int64, []),
+            "gts_device_count": (C.c_int, []),
             "gts_profile_enable": (C.c_int, [C.c_int]),
             "gts_profile_read": (C.c_int, [C.c_char_p, C.c_int64, C.c_int]),
             "gts_bench_int_peak": (C.c_int, [_f64p, v]),
+            "gts_bench_fp32_peak": (C.c_int, [_f64p, v]),
             "gts_last_error": (C.c_char_p, []),
             "gts_version": (C.c_char_p, []),
         }
@@ -124,7 +126,8 @@ EXPORTED = (
     "gts_version", "gts_profile_enable", "gts_profile_read", "gts_bench_int_peak", "gts_batch_host",
     "gts_index_cache_set", "gts_knn_probe", "gts_knn_batch_bounded", "gts_merge_results", "gts_multi_create",
     "gts_multi_destroy", "gts_multi_batch_host", "gts_build_tree_device", "gts_build_tree_device_f32",
-    "gts_index_create_f32dev", "gts_generate_clustered",
+    "gts_index_create_f32dev", "gts_generate_clustered", "gts_bench_fp32_peak",
+    "gts_device_count",
 )
 
 

@@ -91,6 +91,7 @@ static std::vector<std::pair<std::string, ProfRec>> g_prof;
 static unsigned long long g_work[4] = {0, 0, 0, 0};   // pairs, word-steps, entries, rows
 static unsigned long long *g_phase_dev = nullptr;       // GTS_PHASES: per-phase clocks of k_leafgroup_mma
 enum { kWorkPairs = 0, kWorkSteps = 1, kWorkEntries = 2, kWorkRows = 3 };
+static double g_expand[3] = {0, 0, 0};   // traversal: algorithmic bytes, parent rows in, child rows out
 
 static void prof_add(const char *name, double ms)
 {
@@ -2805,6 +2806,7 @@ struct gts_index {
     // (k_root_radius) and of the pending cache (host, float64), and the root
     // pivot's payload for the latter
     float root_radius = INFINITY, cache_radius = 0.f;
+    double avg_text_bytes = 0.0;   // strings: mean stored bytes per entry (traversal byte counts)
     std::vector<double> root_payload;
 };
 
@@ -3397,12 +3399,27 @@ struct Search {
     int64_t expand(const Row *in, int64_t m, int layer, Row *out)
     {
         const int own = (layer + 1) == ix->levels;
+        int64_t cnt;
         switch (ix->metric) {
-        case GTS_EDIT: return launch_expand<kMetricEdit>(in, m, own, out, layer);
-        case GTS_L1: return launch_expand<kMetricL1>(in, m, own, out, layer);
-        case GTS_ANGULAR: return launch_expand<kMetricAngular>(in, m, own, out, layer);
-        default: return launch_expand<kMetricL2>(in, m, own, out, layer);
+        case GTS_EDIT: cnt = launch_expand<kMetricEdit>(in, m, own, out, layer); break;
+        case GTS_L1: cnt = launch_expand<kMetricL1>(in, m, own, out, layer); break;
+        case GTS_ANGULAR: cnt = launch_expand<kMetricAngular>(in, m, own, out, layer); break;
+        default: cnt = launch_expand<kMetricL2>(in, m, own, out, layer); break;
         }
+        if (prof) {
+            // algorithmic traversal bytes: the parent row,
+            // N_c 16-byte child records, the pivot payload of every child
+            // whose distance is evaluated (internal levels: the survivors of
+            // the parent-range pre-screen = the emitted rows; the leaf level:
+            // every child) and the emitted 16-byte rows
+            const int64_t evaluated = own ? m * ix->nc : cnt;
+            const double pay = ix->metric == GTS_EDIT ? ix->avg_text_bytes : 4.0 * ix->Dp;
+            std::lock_guard<std::mutex> g(g_prof_mu);
+            g_expand[0] += (double)m * 16.0 * (1 + ix->nc) + (double)evaluated * pay + (double)cnt * 16.0;
+            g_expand[1] += (double)m;
+            g_expand[2] += (double)cnt;
+        }
+        return cnt;
     }
 
     // depth-first over layers in chunks of level_size_limit parent rows
@@ -4077,6 +4094,15 @@ double host_metric(int metric, const double *a, const double *b, int64_t D)
 extern "C" const char *gts_last_error(void) { return g_err; }
 extern "C" const char *gts_version(void) { return "gts-b200 0.1 sm_100a"; }
 extern "C" int64_t gts_launch_count(void) { return g_launches.load(); }
+extern "C" int gts_device_count(void)
+{
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return c;
+}
 
 extern "C" int gts_profile_enable(int on)
 {
@@ -4097,12 +4123,16 @@ extern "C" int gts_profile_read(char *buf, int64_t cap, int reset)
         first = false;
     }
     char tmp[256];
-    snprintf(tmp, sizeof(tmp), "}, \"work\": {\"pairs\": %llu, \"word_steps\": %llu, \"entries\": %llu, \"rows\": %llu}}",
+    snprintf(tmp, sizeof(tmp), "}, \"work\": {\"pairs\": %llu, \"word_steps\": %llu, \"entries\": %llu, \"rows\": %llu}",
              g_work[0], g_work[1], g_work[2], g_work[3]);
+    js += tmp;
+    snprintf(tmp, sizeof(tmp), ", \"expand\": {\"bytes\": %.0f, \"rows_in\": %.0f, \"rows_out\": %.0f}}", g_expand[0],
+             g_expand[1], g_expand[2]);
     js += tmp;
     if (reset) {
         g_prof.clear();
         for (auto &w : g_work) w = 0;
+        for (auto &w : g_expand) w = 0;
     }
     if (!buf || cap <= (int64_t)js.size()) return set_error(GTS_EINVAL, "profile buffer too small (%zu)", js.size());
     std::memcpy(buf, js.c_str(), js.size() + 1);
@@ -4168,6 +4198,64 @@ static double int_peak_variant(cudaStream_t st, int blocks, uint32_t *sink)
     cudaEventDestroy(a);
     cudaEventDestroy(b);
     return (double)blocks * block * iters * 16 / (ms * 1e-3);
+}
+
+// FP32 pipe: 16 independent FADD (VAR 0) or FFMA (VAR 1) chains per thread
+template <int VAR>
+__global__ void k_fp32_peak(float seed, int iters, float *sink)
+{
+    float a[16];
+#pragma unroll
+    for (int i = 0; i < 16; i++) a[i] = seed + (float)(threadIdx.x * 16 + i) * 1e-7f;
+    const float c = seed * 0.5f;
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int i = 0; i < 16; i++) {
+            if (VAR == 0) a[i] = __fadd_rn(a[i], a[(i + 1) & 15]);
+            else a[i] = __fmaf_rn(a[i], c, a[(i + 1) & 15]);
+        }
+    }
+    float r = 0.f;
+#pragma unroll
+    for (int i = 0; i < 16; i++) r += a[i];
+    if (r == 1.2345f) sink[0] = r;
+}
+
+template <int VAR>
+static double fp32_peak_variant(cudaStream_t st, int blocks, float *sink)
+{
+    const int iters = 2048, block = 256;
+    k_fp32_peak<VAR><<<blocks, block, 0, st>>>(1e-9f, 32, sink);   // warm-up
+    LAUNCH_CHECK();
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    CK(cudaEventRecord(a, st));
+    k_fp32_peak<VAR><<<blocks, block, 0, st>>>(1e-9f, iters, sink);
+    LAUNCH_CHECK();
+    CK(cudaEventRecord(b, st));
+    CK(cudaEventSynchronize(b));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return (double)blocks * block * iters * 16 / (ms * 1e-3);
+}
+
+// FP32 lane-operation throughput (FADD / FFMA instructions x 32 lanes per
+// second), the denominator of the CUDA-core distance kernels' rooflines
+extern "C" int gts_bench_fp32_peak(double *ops_per_s, void *stream)
+{
+    ABI_BEGIN
+    cudaStream_t st = (cudaStream_t)stream;
+    int dev = 0, sms = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    DBuf<float> sink(1, st);
+    const int blocks = sms * 8;
+    ops_per_s[0] = std::max(fp32_peak_variant<0>(st, blocks, sink.p), fp32_peak_variant<1>(st, blocks, sink.p));
+    return GTS_OK;
+    ABI_END
 }
 
 extern "C" int gts_bench_int_peak(double *ops_per_s, void *stream)
@@ -4266,6 +4354,7 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
             h2d(ix->alpha.p, alpha.data(), alpha.size(), st);
             ix->str.alloc(words.size(), st);
             h2d(ix->str.p, words.data(), words.size(), st);
+            ix->avg_text_bytes = 4.0 * (double)words.size() / (double)std::max<int64_t>(n, 1);
             ix->sword.alloc(wstart.size(), st);
             h2d(ix->sword.p, wstart.data(), wstart.size(), st);
             ix->slen.alloc(lens.size(), st);
