@@ -117,6 +117,21 @@ int gts_generate_clustered(uint64_t seed, int64_t n_total, int64_t dim, int64_t 
                            int64_t first, int64_t count, uint64_t query_seed, float noise, float *out,
                            void *stream);
 
+/* In-place insert into leaf slack (the reference buffers
+ * inserts in a pending list and rebuilds on overflow, updates.py:109-158,
+ * PAPER.md:436-448).  Every leaf of the device layout is followed by free
+ * slots; each item descends the tree (the ring holding its distance to each
+ * pivot, else the nearest; at the last split the nearest leaf with room),
+ * takes that leaf's next free slot, and widens the leaf's own-pivot range and
+ * every chosen node's parent-pivot range to its distances, so pruning stays
+ * exact.  slots[i] = the slot of item i, or -1 if it cannot be placed (leaf
+ * full, string longer than a slot or with a symbol outside the index
+ * alphabet, payload not float32-exact over float32-exact data, angular):
+ * the caller keeps those in the pending cache (gts_index_cache_set). */
+int gts_index_insert(gts_index *ix, const gts_dataset *items, int32_t *slots, void *stream);
+/* Delete inserted objects by slot (a delete of a pending id, updates.py:124-135). */
+int gts_index_erase(gts_index *ix, const int32_t *slots, int64_t n, void *stream);
+
 /* tombstone marks in table order (tree.tombstone, updates.py:124-135) */
 int gts_index_set_tombstones(gts_index *ix, const uint8_t *tombstone, void *stream);
 

@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgts.so")
 SOURCES = ["engine.cu", "builder.cpp"]
-HEADERS = ["kernels.cuh", "tcgen05.cuh", "sharded.cuh", "devbuild.cuh", "common.h", os.path.join("..", "..", "include", "gts.h")]
+HEADERS = ["kernels.cuh", "tcgen05.cuh", "sharded.cuh", "devbuild.cuh", "updates.cuh", "common.h", os.path.join("..", "..", "include", "gts.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

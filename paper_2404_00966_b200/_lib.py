@@ -101,6 +101,8 @@ def lib():
                                                   C.POINTER(v)]),
             "gts_generate_clustered": (C.c_int, [C.c_uint64, C.c_int64, C.c_int64, C.c_int64, C.c_float, C.c_int64,
                                                  C.c_int64, C.c_uint64, C.c_float, v, v]),
+            "gts_index_insert": (C.c_int, [v, C.POINTER(GtsDataset), _i32p, v]),
+            "gts_index_erase": (C.c_int, [v, _i32p, C.c_int64, v]),
             "gts_launch_count": (C.c_int64, []),
             "gts_device_count": (C.c_int, []),
             "gts_profile_enable": (C.c_int, [C.c_int]),
@@ -127,7 +129,7 @@ EXPORTED = (
     "gts_index_cache_set", "gts_knn_probe", "gts_knn_batch_bounded", "gts_merge_results", "gts_multi_create",
     "gts_multi_destroy", "gts_multi_batch_host", "gts_build_tree_device", "gts_build_tree_device_f32",
     "gts_index_create_f32dev", "gts_generate_clustered", "gts_bench_fp32_peak",
-    "gts_device_count",
+    "gts_device_count", "gts_index_insert", "gts_index_erase",
 )
 
 

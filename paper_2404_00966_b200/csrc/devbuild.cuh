@@ -559,7 +559,7 @@ __global__ void k_gather_rows_f32(const float *__restrict__ x, int D, int Dp, co
     if (t >= n * Dp) return;
     const int64_t e = t / Dp;
     const int d = (int)(t - e * Dp);
-    v32[t] = d < D ? x[(int64_t)drow[e] * D + d] : 0.f;
+    v32[t] = (d < D && drow[e] >= 0) ? x[(int64_t)drow[e] * D + d] : 0.f;
 }
 
 // tensor-core copy (k_leafgroup_mma2): bf16(o - leaf pivot), K padded to Dk
@@ -634,28 +634,32 @@ extern "C" int gts_index_create_f32dev(const gts_tree *t, int32_t metric, int64_
         if (n == 0 || t->levels == 0) { *out = ix; return GTS_OK; }
         std::vector<int64_t> ord((size_t)n), drow;
         for (int64_t e = 0; e < n; e++) ord[(size_t)e] = e;
+        const SlotLayout lay = slot_layout(t);
+        ord = slot_order(t, lay, ord);
         std::vector<NodeRec> nodes;
-        upload_tables(ix, t, ord, ids, st, drow, nodes);
+        upload_tables(ix, t, ord, ids, st, drow, nodes, lay);
+        const int64_t ns = lay.n_slots;
         ix->data_exact = true;   // float32 payloads: the fp32 copy is exact
-        ix->vec32.alloc((size_t)(n * ix->Dp), st);
-        k_gather_rows_f32<<<grid_for(n * ix->Dp, 256), 256, 0, st>>>(x, ix->D, ix->Dp, ix->row.p, n, ix->vec32.p);
+        ix->vec32.alloc((size_t)(ns * ix->Dp), st);
+        k_gather_rows_f32<<<grid_for(ns * ix->Dp, 256), 256, 0, st>>>(x, ix->D, ix->Dp, ix->row.p, ns, ix->vec32.p);
         LAUNCH_CHECK();
         if (metric == GTS_L2 && ix->D >= 32 && ix->D <= 128 && ix->max_leaf <= 256 &&
             std::getenv("GTS_NO_MMA") == nullptr) {
             ix->Dk = (ix->D + 63) & ~63;
-            std::vector<int32_t> epiv((size_t)n, -1);
+            std::vector<int32_t> epiv((size_t)ns, -1);
             for (int64_t i = ix->leaf_first; i < (int64_t)ix->leaf_first + ix->leaf_count; i++)
-                for (int64_t e = t->pos[i]; e < t->pos[i] + t->size[i]; e++) epiv[(size_t)e] = nodes[(size_t)i].piv;
+                for (int64_t e = lay.dpos[(size_t)i]; e < lay.dpos[(size_t)i] + t->size[i]; e++)
+                    epiv[(size_t)e] = nodes[(size_t)i].piv;
             DBuf<int32_t> dep;
             h2d_vec(dep, epiv, st);
             const size_t tail = (size_t)16 * ix->Dk / 8;
-            ix->vcent.alloc((size_t)n * ix->Dk / 8 + tail, st);
-            CK(cudaMemsetAsync(ix->vcent.p, 0, ((size_t)n * ix->Dk / 8 + tail) * sizeof(uint4), st));
+            ix->vcent.alloc((size_t)ns * ix->Dk / 8 + tail, st);
+            CK(cudaMemsetAsync(ix->vcent.p, 0, ((size_t)ns * ix->Dk / 8 + tail) * sizeof(uint4), st));
             auto *vc = reinterpret_cast<__nv_bfloat16 *>(ix->vcent.p);
-            k_vcent<<<grid_for(n * ix->Dk, 256), 256, 0, st>>>(ix->vec32.p, ix->D, ix->Dp, ix->Dk, dep.p, n, vc);
+            k_vcent<<<grid_for(ns * ix->Dk, 256), 256, 0, st>>>(ix->vec32.p, ix->D, ix->Dp, ix->Dk, dep.p, ns, vc);
             LAUNCH_CHECK();
-            ix->vse.alloc((size_t)n, st);
-            k_vse<<<grid_for(n, 256), 256, 0, st>>>(ix->vec32.p, ix->D, ix->Dp, ix->Dk, dep.p, vc, n, ix->vse.p);
+            ix->vse.alloc((size_t)ns, st);
+            k_vse<<<grid_for(ns, 256), 256, 0, st>>>(ix->vec32.p, ix->D, ix->Dp, ix->Dk, dep.p, vc, ns, ix->vse.p);
             LAUNCH_CHECK();
         }
         CK(cudaStreamSynchronize(st));

@@ -2463,6 +2463,7 @@ __global__ void k_root_radius(IndexView ix, QueryView qv, int64_t n, unsigned *o
 {
     float m = 0.f;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        if (!is_alive(ix.alive, (int)e)) continue;   // free slots and tombstones hold no answer
         const float d = dist32<MET>(ix, qv, 0, (int)e);
         if (d == d) m = fmaxf(m, d);
     }
@@ -2715,17 +2716,19 @@ static double host_norm(const double *x, int64_t D, std::vector<double> &tmp)
 // `sym`) 4 per 32-bit word, each string starting on a 16-byte boundary.
 template <class SymOf>
 static void pack_words(int64_t n, const int64_t *off, SymOf sym, std::vector<uint32_t> &words,
-                       std::vector<uint32_t> &wstart, std::vector<int32_t> &len, const int64_t *order = nullptr)
+                       std::vector<uint32_t> &wstart, std::vector<int32_t> &len, const int64_t *order = nullptr,
+                       int64_t reserve = 0)
 {
+    // order[e] < 0: a free slot (leaf slack), `reserve` words of room
     wstart.resize((size_t)n);
     len.resize((size_t)n);
     uint64_t w = 0;
     for (int64_t e = 0; e < n; e++) {
         const int64_t r = order ? order[e] : e;
-        const int64_t l = off[r + 1] - off[r];
+        const int64_t l = r >= 0 ? off[r + 1] - off[r] : 0;
         wstart[(size_t)e] = (uint32_t)w;
         len[(size_t)e] = (int32_t)l;
-        w += (uint64_t)((l + 15) / 16) * 4;    // 16-byte aligned objects
+        w += r >= 0 ? (uint64_t)((l + 15) / 16) * 4 : (uint64_t)reserve;    // 16-byte aligned objects
     }
     w += 8;                                    // the DP prefetches one uint4 past an object
     if (w >= (1ull << 32)) fail(GTS_EINVAL, "string payload exceeds 16 GiB per index; shard it");
@@ -2733,6 +2736,7 @@ static void pack_words(int64_t n, const int64_t *off, SymOf sym, std::vector<uin
     #pragma omp parallel for schedule(static, 4096)
     for (int64_t e = 0; e < n; e++) {
         const int64_t r = order ? order[e] : e;
+        if (r < 0) continue;
         uint32_t *dst = words.data() + wstart[(size_t)e];
         for (int64_t k = off[r], j = 0; k < off[r + 1]; k++, j++)
             dst[j >> 2] |= (uint32_t)sym(k) << (8 * (j & 3));
@@ -2807,6 +2811,16 @@ struct gts_index {
     // pivot's payload for the latter
     float root_radius = INFINITY, cache_radius = 0.f;
     double avg_text_bytes = 0.0;   // strings: mean stored bytes per entry (traversal byte counts)
+    // leaf slack (in-place inserts): device slot layout and
+    // host mirrors of what the insert path changes
+    int64_t n_ref = 0;                 // entries of the reference tree
+    std::vector<int64_t> leaf_dpos, leaf_cap, leaf_size;   // per leaf (index = node - leaf_first)
+    std::vector<uint32_t> h_alive;     // host copy of the alive bitmask
+    std::vector<uint32_t> h_sword;     // strings: first text word of every slot
+    std::vector<int32_t> h_slen;       // strings: length of every slot's string
+    std::vector<NodeRec> h_nodes;      // host copy of the node records (ranges widen on insert)
+    int slot_words = 0;                // strings: text words reserved per free slot
+    int64_t n_inserted = 0;            // slots filled by gts_index_insert
     std::vector<double> root_payload;
 };
 
@@ -3637,7 +3651,10 @@ struct Search {
         while ((1ll << dbits) <= (long long)std::max(ix->max_len, max_qlen)) dbits++;
         int rbits = 1;
         while ((1ll << rbits) < ix->n) rbits++;
-        const bool packed = ix->metric == GTS_EDIT && qbits + dbits + rbits <= 64 && !cache_hits;
+        // ids in slot order no longer follow row order once a slot was filled
+        // by an insert: sort by the 64-bit id then
+        const bool by_id = cache_hits || ix->n_inserted > 0;
+        const bool packed = ix->metric == GTS_EDIT && qbits + dbits + rbits <= 64 && !by_id;
         if (n > 0 && packed) {
             DBuf<unsigned long long> ka((size_t)n, st), kb((size_t)n, st);
             perm_a.alloc((size_t)n, st);
@@ -3659,7 +3676,7 @@ struct Search {
             perm_a.alloc((size_t)n, st);
             perm_b.alloc((size_t)n, st);
             const unsigned g = grid_for(n, 256);
-            if (cache_hits) {
+            if (by_id) {
                 k_gather_id<<<g, 256, 0, st>>>(he.p, n, ix->ids.p, ix->cache_ids.p, ka.p, perm_a.p);
                 LAUNCH_CHECK();
             }
@@ -3669,8 +3686,8 @@ struct Search {
                                             perm_b.p, (int)n, 0, 32, st);
             tmp_bytes = std::max(tmp_bytes, t2);
             DBuf<uint8_t> tmp(tmp_bytes, st);
-            // 1) by id (by dataset row, rbits wide, when no cache entry is among the hits)
-            if (!cache_hits) {
+            // 1) by id (by dataset row, rbits wide, when no cache or inserted entry is among the hits)
+            if (!by_id) {
                 DBuf<uint32_t> ra((size_t)n, st), rb((size_t)n, st);
                 k_gather_row<<<g, 256, 0, st>>>(he.p, n, ix->row.p, ra.p, perm_a.p);
                 LAUNCH_CHECK();
@@ -3917,21 +3934,85 @@ gts_result *run_search(gts_index *ix, const gts_queries *q, int mode, const doub
 
 }  // namespace
 
+// Device slot layout: every leaf keeps its reference entries in order,
+// followed by free slots for in-place inserts (leaf slack: size/8, at least
+// 4, none for empty leaves; GTS_LEAF_SLACK=<d> sets size/d, 0 = none).
+// Internal nodes span their leaves' slots.
+struct SlotLayout {
+    std::vector<int64_t> dpos, span;   // per node: first slot, slot count (leaves: capacity)
+    int64_t n_slots = 0;
+};
+
+SlotLayout slot_layout(const gts_tree *t)
+{
+    SlotLayout L;
+    L.dpos.assign((size_t)t->nodes + 1, 0);
+    L.span.assign((size_t)t->nodes + 1, 0);
+    static const int den = std::getenv("GTS_LEAF_SLACK") ? std::atoi(std::getenv("GTS_LEAF_SLACK")) : 8;
+    __int128 c = 1;
+    for (int64_t l = 1; l < t->levels; l++) c *= t->nc;
+    const int64_t lfirst = (int64_t)((c - 1) / (t->nc - 1) + 1), lcount = (int64_t)c;
+    int64_t p = 0;
+    for (int64_t i = lfirst; i < lfirst + lcount; i++) {
+        const int64_t sz = t->size[i];
+        const int64_t cap = (sz > 0 && den > 0) ? sz + std::max<int64_t>(4, sz / den) : sz;
+        L.dpos[(size_t)i] = p;
+        L.span[(size_t)i] = cap;
+        p += cap;
+    }
+    L.n_slots = p;
+    for (int64_t level = t->levels - 1; level >= 1; level--) {
+        __int128 cc = 1;
+        for (int64_t l = 1; l < level; l++) cc *= t->nc;
+        const int64_t first = (int64_t)((cc - 1) / (t->nc - 1) + 1), count = (int64_t)cc;
+        for (int64_t v = first; v < first + count; v++) {
+            const int64_t c0 = (v - 1) * t->nc + 2;
+            L.dpos[(size_t)v] = L.dpos[(size_t)c0];
+            int64_t sp = 0;
+            for (int64_t j = 0; j < t->nc; j++) sp += L.span[(size_t)(c0 + j)];
+            L.span[(size_t)v] = sp;
+        }
+    }
+    return L;
+}
+
+// reference-position order (ord[k] for reference slot k) -> slot order
+// (ord_s[e] = reference position of slot e, -1 for a free slot)
+std::vector<int64_t> slot_order(const gts_tree *t, const SlotLayout &L, const std::vector<int64_t> &ord)
+{
+    std::vector<int64_t> os((size_t)L.n_slots, -1);
+    __int128 c = 1;
+    for (int64_t l = 1; l < t->levels; l++) c *= t->nc;
+    const int64_t lfirst = (int64_t)((c - 1) / (t->nc - 1) + 1), lcount = (int64_t)c;
+    #pragma omp parallel for schedule(dynamic, 256)
+    for (int64_t i = lfirst; i < lfirst + lcount; i++)
+        for (int64_t k = 0; k < t->size[i]; k++) os[(size_t)(L.dpos[(size_t)i] + k)] = ord[(size_t)(t->pos[i] + k)];
+    return os;
+}
+
 // The tables every index has, from the host tree arrays (reference
 // tree.py:155-175): node records with fp32 ranges rounded outward, node
 // positions, live leaves, entry rows / pivot distances / ids / alive bits
-// in device table order (ord[e] = reference table position of entry e).
+// in device slot order (ord[e] = reference table position of slot e, -1 =
+// free slot).  Leaf records carry their entry count, internal ones their
+// slot span (> 0 iff the node holds entries).
 void upload_tables(gts_index *ix, const gts_tree *t, const std::vector<int64_t> &ord, const int64_t *row_ids,
-                   cudaStream_t st, std::vector<int64_t> &drow, std::vector<NodeRec> &nodes)
+                   cudaStream_t st, std::vector<int64_t> &drow, std::vector<NodeRec> &nodes, const SlotLayout &lay)
 {
-    const int64_t n = t->n;
-    drow.assign((size_t)n, 0);
-    std::vector<int32_t> tpos((size_t)n);
+    const int64_t n = (int64_t)ord.size();
+    ix->n = n;
+    ix->n_ref = t->n;
+    drow.assign((size_t)n, -1);
+    std::vector<int32_t> tpos((size_t)t->n, -1);
     #pragma omp parallel for schedule(static)
-    for (int64_t e = 0; e < n; e++) drow[(size_t)e] = t->rows[ord[(size_t)e]];
+    for (int64_t e = 0; e < n; e++) drow[(size_t)e] = ord[(size_t)e] >= 0 ? t->rows[ord[(size_t)e]] : -1;
     ix->ord = ord;
     #pragma omp parallel for schedule(static)
-    for (int64_t e = 0; e < n; e++) tpos[(size_t)drow[(size_t)e]] = (int32_t)e;
+    for (int64_t e = 0; e < n; e++)
+        if (drow[(size_t)e] >= 0) tpos[(size_t)drow[(size_t)e]] = (int32_t)e;
+    __int128 c = 1;
+    for (int l = 1; l < ix->levels; l++) c *= ix->nc;
+    const int64_t lfirst = (int64_t)((c - 1) / (ix->nc - 1) + 1), lcount = (int64_t)c;
     nodes.assign((size_t)t->nodes + 1, NodeRec{});
     std::vector<int32_t> npos((size_t)t->nodes + 1);
     for (int64_t i = 0; i <= t->nodes; i++) {
@@ -3941,28 +4022,35 @@ void upload_tables(gts_index *ix, const gts_tree *t, const std::vector<int64_t> 
         if ((double)mx < t->max_dis[i]) mx = std::nextafter(mx, INFINITY);
         r.mn = mn;
         r.mx = mx;
-        r.size = (int32_t)t->size[i];
+        const bool leaf = i >= lfirst && i < lfirst + lcount;
+        r.size = (int32_t)(leaf ? t->size[i] : lay.span[(size_t)i]);
         r.piv = t->pivot_row[i] >= 0 ? tpos[(size_t)t->pivot_row[i]] : -1;
         nodes[(size_t)i] = r;
-        npos[(size_t)i] = (int32_t)t->pos[i];
+        npos[(size_t)i] = (int32_t)lay.dpos[(size_t)i];
     }
+    ix->h_nodes = nodes;
     ix->node.alloc(nodes.size(), st);
     h2d(ix->node.p, nodes.data(), nodes.size(), st);
     ix->npos.alloc(npos.size(), st);
     h2d(ix->npos.p, npos.data(), npos.size(), st);
-    // live leaves (for pruning-disabled scans)
+    // live leaves (for pruning-disabled scans); the largest leaf capacity
     {
-        __int128 c = 1;
-        for (int l = 1; l < ix->levels; l++) c *= ix->nc;
-        const int64_t first = (int64_t)((c - 1) / (ix->nc - 1) + 1), count = (int64_t)c;
         std::vector<int32_t> lv;
-        for (int64_t i = first; i < first + count; i++) if (t->size[i] > 0) lv.push_back((int32_t)i);
+        ix->leaf_dpos.assign((size_t)lcount, 0);
+        ix->leaf_cap.assign((size_t)lcount, 0);
+        ix->leaf_size.assign((size_t)lcount, 0);
+        for (int64_t i = lfirst; i < lfirst + lcount; i++) {
+            if (t->size[i] > 0) lv.push_back((int32_t)i);
+            ix->max_leaf = std::max<int>(ix->max_leaf, (int)lay.span[(size_t)i]);
+            ix->leaf_dpos[(size_t)(i - lfirst)] = lay.dpos[(size_t)i];
+            ix->leaf_cap[(size_t)(i - lfirst)] = lay.span[(size_t)i];
+            ix->leaf_size[(size_t)(i - lfirst)] = t->size[i];
+        }
         ix->n_live_leaves = (int)lv.size();
         ix->live_leaves.alloc(std::max<size_t>(lv.size(), 1), st);
         h2d(ix->live_leaves.p, lv.data(), lv.size(), st);
-        for (int64_t i = first; i < first + count; i++) ix->max_leaf = std::max<int>(ix->max_leaf, (int)t->size[i]);
-        ix->leaf_first = (int)first;
-        ix->leaf_count = (int)count;
+        ix->leaf_first = (int)lfirst;
+        ix->leaf_count = (int)lcount;
     }
     {
         std::vector<int32_t> row((size_t)n);
@@ -3979,12 +4067,18 @@ void upload_tables(gts_index *ix, const gts_tree *t, const std::vector<int64_t> 
         uint32_t bits = 0;
         for (int64_t e = w * 32; e < std::min<int64_t>(n, w * 32 + 32); e++) {
             const int64_t o = ord[(size_t)e];
+            if (o < 0) {
+                dis[(size_t)e] = NAN;
+                ids[(size_t)e] = -1;
+                continue;
+            }
             dis[(size_t)e] = (float)t->dis[o];
             ids[(size_t)e] = row_ids[drow[(size_t)e]];
             if (!t->tombstone || t->tombstone[o] == 0) bits |= 1u << (e & 31);
         }
         alive[(size_t)w] = bits;
     }
+    ix->h_alive = alive;
     ix->dis.alloc((size_t)n, st);
     h2d(ix->dis.p, dis.data(), (size_t)n, st);
     ix->ids.alloc((size_t)n, st);
@@ -4332,9 +4426,13 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
                     });
             }
         }
+        // every leaf is followed by free slots (leaf slack) for in-place inserts
+        const SlotLayout lay = slot_layout(t);
+        ord = slot_order(t, lay, ord);
+        const int64_t ns = lay.n_slots;
         std::vector<int64_t> drow;
         std::vector<NodeRec> nodes;
-        upload_tables(ix, t, ord, ds->ids, st, drow, nodes);
+        upload_tables(ix, t, ord, ds->ids, st, drow, nodes, lay);
         const double c2 = trace ? now_ms() : 0.0;
         if (ds->metric == GTS_EDIT) {
             const int64_t ncodes = ds->offsets[n];
@@ -4344,25 +4442,31 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
                 fail(GTS_EMETRIC, "string alphabet of %zu symbols exceeds the device's 254", alpha.size());
             ix->A = (int)alpha.size();
             ix->h_alpha = alpha;
+            int64_t maxlen = 0;
+            for (int64_t r = 0; r < n; r++) maxlen = std::max<int64_t>(maxlen, ds->offsets[r + 1] - ds->offsets[r]);
+            // a free slot reserves room for a string as long as the longest stored one
+            ix->slot_words = (int)(((maxlen + 15) / 16) * 4);
             std::vector<uint32_t> words, wstart;
             std::vector<int32_t> lens;
             const SymMap smap(alpha);
             auto symof = [&](int64_t k) { return smap(ds->codes[k]); };
-            pack_words(n, ds->offsets, symof, words, wstart, lens, drow.data());
+            pack_words(ns, ds->offsets, symof, words, wstart, lens, drow.data(), ix->slot_words);
             for (auto l : lens) ix->max_len = std::max<int>(ix->max_len, l);
             ix->alpha.alloc(std::max<size_t>(alpha.size(), 1), st);
             h2d(ix->alpha.p, alpha.data(), alpha.size(), st);
             ix->str.alloc(words.size(), st);
             h2d(ix->str.p, words.data(), words.size(), st);
             ix->avg_text_bytes = 4.0 * (double)words.size() / (double)std::max<int64_t>(n, 1);
+            ix->h_sword = wstart;
             ix->sword.alloc(wstart.size(), st);
             h2d(ix->sword.p, wstart.data(), wstart.size(), st);
             ix->slen.alloc(lens.size(), st);
             h2d(ix->slen.p, lens.data(), lens.size(), st);
-            std::vector<uint4> rec((size_t)n);
+            ix->h_slen = lens;
+            std::vector<uint4> rec((size_t)ns);
             #pragma omp parallel for schedule(static)
-            for (int64_t e = 0; e < n; e++) {
-                float d = (float)t->dis[ord[(size_t)e]];
+            for (int64_t e = 0; e < ns; e++) {
+                const float d = ord[(size_t)e] >= 0 ? (float)t->dis[ord[(size_t)e]] : NAN;
                 uint32_t db;
                 std::memcpy(&db, &d, 4);
                 const float lf = (float)lens[(size_t)e];
@@ -4371,21 +4475,23 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
                 rec[(size_t)e] = make_uint4(db, (uint32_t)lens[(size_t)e], wstart[(size_t)e], lb);
             }
             for (int64_t i = ix->leaf_first; i < (int64_t)ix->leaf_first + ix->leaf_count; i++) {
-                if (t->size[i] <= 0) continue;
-                const int64_t a = t->pos[i], b = t->pos[i] + t->size[i] - 1;
-                const int64_t wend = (int64_t)wstart[(size_t)b] + ((lens[(size_t)b] + 15) / 16) * 4;
+                if (lay.span[(size_t)i] <= 0) continue;
+                const int64_t a = lay.dpos[(size_t)i], b = a + lay.span[(size_t)i] - 1;
+                const int64_t wend = (int64_t)wstart[(size_t)b] + std::max<int64_t>(((lens[(size_t)b] + 15) / 16) * 4,
+                                                                                  ord[(size_t)b] < 0 ? ix->slot_words : 0);
                 ix->max_leaf_words = std::max<int>(ix->max_leaf_words, (int)std::min<int64_t>(wend - wstart[(size_t)a], 1 << 30));
             }
             ix->erec.alloc(rec.size(), st);
             h2d(ix->erec.p, rec.data(), rec.size(), st);
-            k_erec_alive<<<grid_for(n, 256), 256, 0, st>>>(ix->erec.p, ix->dis.p, ix->alive.p, n);
+            k_erec_alive<<<grid_for(ns, 256), 256, 0, st>>>(ix->erec.p, ix->dis.p, ix->alive.p, ns);
             LAUNCH_CHECK();
             if (ix->A > kHistMinAlphabet) {
                 // 32 byte-buckets of symbol counts per entry (saturating)
-                std::vector<uint8_t> hb((size_t)n * 32, 0);
+                std::vector<uint8_t> hb((size_t)ns * 32, 0);
                 #pragma omp parallel for schedule(static, 4096)
-                for (int64_t e = 0; e < n; e++) {
+                for (int64_t e = 0; e < ns; e++) {
                     const int64_t r = drow[(size_t)e];
+                    if (r < 0) continue;
                     uint8_t *h = hb.data() + e * 32;
                     for (int64_t k = ds->offsets[r]; k < ds->offsets[r + 1]; k++) {
                         const int sym = (int)(std::lower_bound(alpha.begin(), alpha.end(), ds->codes[k]) - alpha.begin());
@@ -4393,18 +4499,19 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
                         if (c < 255) c++;
                     }
                 }
-                ix->ehist.alloc((size_t)n * 2, st);
+                ix->ehist.alloc((size_t)ns * 2, st);
                 CK(cudaMemcpyAsync(ix->ehist.p, hb.data(), hb.size(), cudaMemcpyHostToDevice, st));
                 CK(cudaStreamSynchronize(st));
             }
         } else {
             ix->D = (int)ds->dim;
             ix->Dp = (ix->D + 3) & ~3;
-            std::vector<float> v32((size_t)(n * ix->Dp), 0.f);
+            std::vector<float> v32((size_t)(ns * ix->Dp), 0.f);
             bool exact = true;
             float mx = 0.f;
             #pragma omp parallel for schedule(static, 4096) reduction(&& : exact) reduction(max : mx)
-            for (int64_t e = 0; e < n; e++) {
+            for (int64_t e = 0; e < ns; e++) {
+                if (drow[(size_t)e] < 0) continue;
                 const double *src = ds->vectors + drow[(size_t)e] * ix->D;
                 for (int d = 0; d < ix->D; d++) {
                     float f = (float)src[d];
@@ -4419,13 +4526,11 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
             if (ds->metric == GTS_L2 && ix->D >= 32 && ix->D <= 128 && ix->max_leaf <= 256 &&
                 std::getenv("GTS_NO_MMA") == nullptr) {
                 ix->Dk = (ix->D + 63) & ~63;
-                std::vector<__nv_bfloat16> vc((size_t)n * ix->Dk, __float2bfloat16(0.f));
-                __int128 c = 1;
-                for (int l = 1; l < ix->levels; l++) c *= ix->nc;
-                const int64_t lfirst = (int64_t)((c - 1) / (ix->nc - 1) + 1), lcount = (int64_t)c;
+                std::vector<__nv_bfloat16> vc((size_t)ns * ix->Dk, __float2bfloat16(0.f));
+                const int64_t lfirst = ix->leaf_first, lcount = ix->leaf_count;
                 #pragma omp parallel for schedule(dynamic, 64)
                 for (int64_t i = lfirst; i < lfirst + lcount; i++) {
-                    const int64_t p0 = t->pos[i], sz = t->size[i];
+                    const int64_t p0 = lay.dpos[(size_t)i], sz = t->size[i];
                     if (sz <= 0) continue;
                     const int pvp = nodes[(size_t)i].piv;
                     for (int64_t e = p0; e < p0 + sz; e++)
@@ -4435,10 +4540,10 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
                 }
                 // se_e = c . bf16(o_e - c): the pivot term of the uncentred
                 // query product (k_leafgroup_mma2), from the same rounded values
-                std::vector<float> se((size_t)n, 0.f);
+                std::vector<float> se((size_t)ns, 0.f);
                 #pragma omp parallel for schedule(dynamic, 64)
                 for (int64_t i = lfirst; i < lfirst + lcount; i++) {
-                    const int64_t p0 = t->pos[i], sz = t->size[i];
+                    const int64_t p0 = lay.dpos[(size_t)i], sz = t->size[i];
                     if (sz <= 0) continue;
                     const int pvp = nodes[(size_t)i].piv;
                     for (int64_t e = p0; e < p0 + sz; e++) {
@@ -4455,30 +4560,32 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
                 ix->vcent.alloc(vc.size() / 8 + tail, st);
                 CK(cudaMemcpyAsync(ix->vcent.p, vc.data(), vc.size() * sizeof(__nv_bfloat16), cudaMemcpyHostToDevice, st));
                 CK(cudaMemsetAsync(ix->vcent.p + vc.size() / 8, 0, tail * sizeof(uint4), st));
-                ix->vse.alloc((size_t)n, st);
-                h2d(ix->vse.p, se.data(), (size_t)n, st);
+                ix->vse.alloc((size_t)ns, st);
+                h2d(ix->vse.p, se.data(), (size_t)ns, st);
                 CK(cudaStreamSynchronize(st));
             }
             if (ds->metric == GTS_ANGULAR) {
-                std::vector<double> nrm((size_t)n), tmp;
-                std::vector<float> nrm32((size_t)n);
-                for (int64_t e = 0; e < n; e++) {
+                std::vector<double> nrm((size_t)ns, 0.0), tmp;
+                std::vector<float> nrm32((size_t)ns, 0.f);
+                for (int64_t e = 0; e < ns; e++) {
+                    if (drow[(size_t)e] < 0) continue;
                     nrm[(size_t)e] = host_norm(ds->vectors + drow[(size_t)e] * ix->D, ix->D, tmp);
                     nrm32[(size_t)e] = (float)nrm[(size_t)e];
                 }
-                ix->vnorm64.alloc((size_t)n, st);
-                h2d(ix->vnorm64.p, nrm.data(), (size_t)n, st);
-                ix->vnorm32.alloc((size_t)n, st);
-                h2d(ix->vnorm32.p, nrm32.data(), (size_t)n, st);
+                ix->vnorm64.alloc((size_t)ns, st);
+                h2d(ix->vnorm64.p, nrm.data(), (size_t)ns, st);
+                ix->vnorm32.alloc((size_t)ns, st);
+                h2d(ix->vnorm32.p, nrm32.data(), (size_t)ns, st);
                 CK(cudaStreamSynchronize(st));
             }
             ix->vec32.alloc(v32.size(), st);
             h2d(ix->vec32.p, v32.data(), v32.size(), st);
             if (!exact) {
-                std::vector<double> v64((size_t)(n * ix->D));
+                std::vector<double> v64((size_t)(ns * ix->D), 0.0);
                 #pragma omp parallel for schedule(static, 4096)
-                for (int64_t e = 0; e < n; e++)
-                    std::memcpy(v64.data() + e * ix->D, ds->vectors + drow[(size_t)e] * ix->D, sizeof(double) * ix->D);
+                for (int64_t e = 0; e < ns; e++)
+                    if (drow[(size_t)e] >= 0)
+                        std::memcpy(v64.data() + e * ix->D, ds->vectors + drow[(size_t)e] * ix->D, sizeof(double) * ix->D);
                 ix->vec64.alloc(v64.size(), st);
                 h2d(ix->vec64.p, v64.data(), v64.size(), st);
             }
@@ -4487,8 +4594,8 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
         const double c3 = trace ? now_ms() : 0.0;
         if (ds->metric != GTS_EDIT && n > 0 && ix->levels > 0) compute_root_radius(ix, ds, t, st);
         if (trace)
-            fprintf(stderr, "[gts] index_create n=%lld pool=%.1fms tables=%.1fms payload=%.1fms root=%.1fms\n",
-                    (long long)n, c1 - c0, c2 - c1, c3 - c2, now_ms() - c3);
+            fprintf(stderr, "[gts] index_create n=%lld slots=%lld pool=%.1fms tables=%.1fms payload=%.1fms root=%.1fms\n",
+                    (long long)n, (long long)ns, c1 - c0, c2 - c1, c3 - c2, now_ms() - c3);
         *out = ix;
         return GTS_OK;
     } catch (...) {
@@ -4516,9 +4623,20 @@ extern "C" int gts_index_set_tombstones(gts_index *ix, const uint8_t *tomb, void
     if (!ix || !tomb) fail(GTS_EINVAL, "null argument");
     if (ix->n == 0) return GTS_OK;
     CK(cudaSetDevice(ix->device));
-    std::vector<uint32_t> alive((size_t)((ix->n + 31) / 32), 0u);
-    for (int64_t e = 0; e < ix->n; e++)
-        if (tomb[ix->ord[(size_t)e]] == 0) alive[(size_t)(e >> 5)] |= 1u << (e & 31);
+    // reference entries follow `tomb`; slots filled by gts_index_insert keep
+    // their own state (gts_index_erase)
+    std::vector<uint32_t> &alive = ix->h_alive;
+    #pragma omp parallel for schedule(static)
+    for (int64_t w = 0; w < (ix->n + 31) / 32; w++) {
+        uint32_t bits = alive[(size_t)w];
+        for (int64_t e = w * 32; e < std::min<int64_t>(ix->n, w * 32 + 32); e++) {
+            const int64_t o = ix->ord[(size_t)e];
+            if (o < 0) continue;
+            const uint32_t b = 1u << (e & 31);
+            bits = tomb[o] == 0 ? (bits | b) : (bits & ~b);
+        }
+        alive[(size_t)w] = bits;
+    }
     cudaStream_t st = (cudaStream_t)stream;
     h2d(ix->alive.p, alive.data(), alive.size(), st);
     if (ix->erec.p) {
@@ -4819,3 +4937,5 @@ extern "C" int gts_pair_distances(int32_t metric, int64_t np, int64_t dim, const
 #include "sharded.cuh"
 // device bulk build
 #include "devbuild.cuh"
+// in-place inserts into leaf slack
+#include "updates.cuh"
