@@ -170,7 +170,8 @@ def bench_config(args, w, world):
     return {
         "workload": f"{args.workload} (BASELINE.json configs[{w['config_index']}])",
         "n": n_total, "n_per_gpu": n_total // world, "nq": w["nq"], "radius": w["radius"], "k": w["k"],
-        "node_capacity": 20, "levels_per_shard": split + 1, "memory_units": 1 << 24,
+        "node_capacity": 20, "levels_per_shard": split + 1,
+        "memory_units": "device default: per-layer child tables of min(2^26, free HBM / (64 B x levels)) rows",
         "l2_policy": "index payload+tables exceed nothing: words (~25 MB) stay L2-resident by design; "
                      "no flush between steps (device-resident index is the operating point)",
         "parallelism": (f"{world} shards (contiguous id ranges, one GTS tree per GPU), replicated query batch; "
@@ -440,6 +441,7 @@ def run_stream(args, rank, world, local_rank):
     import torch
     import paper_2404_00966_b200 as P
     from paper_2404_00966_b200 import _lib
+    from paper_2404_00966_b200.search import HBM_SIZED
     torch.cuda.set_device(local_rank)
     w = make_workload("dna_stream", rank, args)
     codes, off = w["codes"], w["off"]
@@ -448,7 +450,7 @@ def run_stream(args, rank, world, local_rank):
     q = ["".join(map(chr, w["qcodes"][w["qoff"][i]:w["qoff"][i + 1]])) for i in range(w["nq"])]
     t0 = time.perf_counter()
     si = P.StreamingIndex(P.Dataset.from_strings(strs, P.EDIT, ids=w["ids"]), P.TreeConfig(20, 0),
-                          cache_capacity=w["cache_capacity"])
+                          cache_capacity=w["cache_capacity"], memory_units=HBM_SIZED)
     build_s = time.perf_counter() - t0
     rng = np.random.default_rng(5)
     # deleted ids are re-inserted in the same step, so the live id set never

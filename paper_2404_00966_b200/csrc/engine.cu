@@ -3839,6 +3839,19 @@ static double now_ms()
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
+int64_t hbm_rows(const gts_index *ix)
+{
+    static const char *env = std::getenv("GTS_DEFAULT_ROWS");
+    if (env) return std::max<int64_t>(std::atoll(env), ix->nc);
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+        cudaGetLastError();
+        return 1ll << 24;
+    }
+    const int64_t rows = (int64_t)(free_b / 4 / (16 * (size_t)std::max(ix->levels, 1)));
+    return std::max<int64_t>(std::min<int64_t>(rows, 1ll << 26), std::max<int64_t>(ix->nc, 1ll << 16));
+}
+
 gts_result *run_search(gts_index *ix, const gts_queries *q, int mode, const double *radii, const int64_t *ks,
                        int64_t memory_units, int pruning, cudaStream_t st, bool use_cache = false,
                        const float *ext_bound = nullptr, float *probe_out = nullptr)
@@ -3847,9 +3860,12 @@ gts_result *run_search(gts_index *ix, const gts_queries *q, int mode, const doub
     const double t0 = trace ? now_ms() : 0.0;
     check_queries(ix, q);
     CK(cudaSetDevice(ix->device));
-    // 0 = device default: 16M frontier rows (256 MiB per child table) -- the
-    // reference's 1<<20 (runtime.py:18) was sized for a CPU; same formula
-    const int64_t cap = memory_units > 0 ? memory_units : (1ll << 24);
+    // 0 = device default, sized to HBM: the depth-first driver keeps at most
+    // one child table per layer alive (16-byte rows), and those tables may
+    // take a quarter of the free device memory, capped at 2^26 rows per
+    // table (1 GiB) -- the reference's 1<<20 (runtime.py:18) was sized for a
+    // CPU; the chunking formula (level_size_limit) is the same
+    const int64_t cap = memory_units > 0 ? memory_units : hbm_rows(ix);
     if (ix->n > 0 && cap < ix->nc) fail(GTS_EBUDGET, "memory_units %lld below fan-out %d", (long long)cap, ix->nc);
     const int64_t nq = q->nq;
     Search s(ix, q, st, mode, cap, pruning);

@@ -17,9 +17,13 @@ import numpy as np
 
 from . import _lib
 from .metrics import METRIC_CODES, STRING_METRICS
-from .runtime import BudgetError
+from .runtime import DEFAULT_MEMORY_UNITS, BudgetError
 
-DEVICE_MEMORY_UNITS = 1 << 24
+# memory_units=HBM_SIZED: the device default, sized to free HBM (csrc/engine.cu
+# hbm_rows); None keeps the reference's DEFAULT_MEMORY_UNITS (runtime.py:18),
+# so a default-constructed searcher logs the reference's size_limits
+HBM_SIZED = -1
+DEVICE_MEMORY_UNITS = HBM_SIZED
 
 RANGE = "range"
 KNN = "knn"
@@ -125,8 +129,8 @@ class BatchSearcher:
 
     Args mirror the reference (search.py:214-234): tree, runtime (accepted,
     unused: the device does the parallel work), memory_units (row budget of
-    the one materialized frontier table; None = the device default of 1<<24
-    rows, the reference's CPU default being 1<<20), pruning.
+    the one materialized frontier table; None = the reference's default of
+    1<<20 rows, HBM_SIZED = the device default sized to free HBM), pruning.
     """
 
     def __init__(self, tree, runtime=None, memory_units=None, pruning=True, device=0, _use_cache=False):
@@ -134,10 +138,10 @@ class BatchSearcher:
         self.tree = tree
         self.ds = tree.dataset
         self.rt = runtime
-        self.capacity = int(memory_units or DEVICE_MEMORY_UNITS)
+        self.capacity = DEFAULT_MEMORY_UNITS if memory_units is None else int(memory_units)
         self.pruning = pruning
         self.device = device
-        if tree.n > 0 and self.capacity < tree.nc:
+        if tree.n > 0 and self.capacity != HBM_SIZED and self.capacity < tree.nc:
             raise BudgetError(f"memory_units {self.capacity} below fan-out {tree.nc}")
 
     # -- public API (search.py:238-260) -------------------------------------
@@ -209,6 +213,6 @@ class BatchSearcher:
         rc = L.gts_batch_host(dev.h, C.byref(qb), 0 if mode == RANGE else 1,
                               _lib.ptr(radii, _lib._f64p) if radii is not None else None,
                               _lib.ptr(ks, _lib._i64p) if ks is not None else None,
-                              self.capacity, flags, None, C.byref(h))
+                              max(self.capacity, 0), flags, None, C.byref(h))
         _lib.check(rc)
         return _fetch(h, nq)

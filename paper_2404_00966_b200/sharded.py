@@ -262,7 +262,7 @@ class ShardedIndex:
             raise ValueError("need at least one shard")
         n = dataset.n
         self.bounds = [n * i // S for i in range(S + 1)]
-        self.capacity = int(memory_units or DEVICE_MEMORY_UNITS)
+        self.capacity = DEVICE_MEMORY_UNITS if memory_units is None else int(memory_units)
         self.pruning = pruning
         self.trees = []
         self._keep = []
@@ -271,7 +271,7 @@ class ShardedIndex:
             rows = np.arange(self.bounds[i], self.bounds[i + 1])
             sub = dataset.subset_rows(rows)
             tree = build_tree(sub, self.config)
-            if tree.n > 0 and self.capacity < tree.nc:
+            if tree.n > 0 and self.capacity != DEVICE_MEMORY_UNITS and self.capacity < tree.nc:
                 raise BudgetError(f"memory_units {self.capacity} below fan-out {tree.nc}")
             self.trees.append(tree)
             if tree.levels == 0:
@@ -333,7 +333,7 @@ class ShardedIndex:
         _lib.check(_lib.lib().gts_multi_batch_host(
             self._m, C.byref(qb), 0 if mode == RANGE else 1,
             _lib.ptr(radii, _lib._f64p) if radii is not None else None,
-            _lib.ptr(ks, _lib._i64p) if ks is not None else None, self.capacity, flags, C.byref(h)))
+            _lib.ptr(ks, _lib._i64p) if ks is not None else None, max(self.capacity, 0), flags, C.byref(h)))
         return _fetch(h, nq)
 
 
