@@ -171,7 +171,7 @@ def bench_config(args, w, world):
         "workload": f"{args.workload} (BASELINE.json configs[{w['config_index']}])",
         "n": n_total, "n_per_gpu": n_total // world, "nq": w["nq"], "radius": w["radius"], "k": w["k"],
         "node_capacity": 20, "levels_per_shard": split + 1,
-        "memory_units": "device default: per-layer child tables of min(2^26, free HBM / (64 B x levels)) rows",
+        "memory_units": "device default: per-layer child tables of min(2^24, free HBM / (64 B x levels)) rows",
         "l2_policy": "index payload+tables exceed nothing: words (~25 MB) stay L2-resident by design; "
                      "no flush between steps (device-resident index is the operating point)",
         "parallelism": (f"{world} shards (contiguous id ranges, one GTS tree per GPU), replicated query batch; "
@@ -632,7 +632,7 @@ def run_ours(args, rank, world, local_rank):
         "profile": prof,
     }
     out["roofline"] = roofline(eng, prof, kver, step_ms_prof)
-    out["roofline"]["traversal"] = traversal_roofline(prof, args.workload)
+    out["roofline"]["traversal"] = traversal_roofline(prof, args.workload, w.get("dim") if w["metric"] != "edit" else None)
     out["roofline"]["traffic"] = ncu_traffic(args.workload, kname)
     if world == 1 and not args.no_cpu_baseline:
         if w.get("device_gen"):
@@ -930,11 +930,18 @@ def roofline(eng, prof, kver, step_ms_prof):
         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s (B200_PROFILING.md)"})
 
 
-def traversal_roofline(prof, workload):
-    """HBM roofline of the list-table traversal (k_expand / k_expand_grouped,
-    search.py:405-477): algorithmic bytes per SURVEY.md §8(d) (parent row,
-    N_c 16-byte child records, the evaluated children's pivot payloads, the
-    emitted 16-byte rows) / the launches' device time."""
+def traversal_roofline(prof, workload, dim=None):
+    """Roofline of the list-table traversal (k_expand / k_expand_grouped,
+    search.py:405-477).  HBM leg: algorithmic bytes per SURVEY.md §8(d)
+    (parent row, N_c 16-byte child records, the evaluated children's pivot
+    payloads, the emitted 16-byte rows) / the launches' device time.  For
+    vectors the grouped kernel stages each node's child pivots in shared
+    memory once per item of rows, so the per-(row, child) payload bytes of
+    that model never reach HBM (hbm frac can exceed 1); its bound is then
+    the fp32 pipe: 2*Dp lane-ops per evaluated child distance (sub + fma /
+    |.|-add), against the in-run gts_bench_fp32_peak.  `bound` names the
+    leg with the larger fraction."""
+    from paper_2404_00966_b200 import _lib
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     peaks = json.load(open(peaks_path)) if os.path.exists(peaks_path) else {}
     hbm = peaks.get("hbm_gbs", 6650.0)
@@ -945,9 +952,24 @@ def traversal_roofline(prof, workload):
     gbs = ex.get("bytes", 0) / (k["ms"] / 1e3) / 1e9
     out = {"kernel": "k_expand", "launches_per_step": k["count"], "ms_per_step": round(k["ms"], 4),
            "bytes_per_step": int(ex.get("bytes", 0)), "rows_in": int(ex.get("rows_in", 0)),
-           "rows_out": int(ex.get("rows_out", 0)), "bound": "hbm", "achieved": round(gbs, 2), "peak": hbm,
+           "rows_out": int(ex.get("rows_out", 0)), "distances": int(ex.get("evaluated", 0)),
+           "bound": "hbm", "achieved": round(gbs, 2), "peak": hbm,
            "unit": "GB/s", "frac": round(gbs / hbm, 4),
            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s (B200_PROFILING.md)"}
+    if dim and dim >= 16 and ex.get("evaluated"):
+        dp = (dim + 3) // 4 * 4
+        fp = C.c_double()
+        _lib.check(_lib.lib().gts_bench_fp32_peak(C.byref(fp), None))
+        pk = fp.value / 1e12
+        ach = ex["evaluated"] * 2 * dp / (k["ms"] / 1e3) / 1e12
+        out["fp32"] = {"achieved": round(ach, 3), "peak": round(pk, 2), "unit": "Tops/s", "frac": round(ach / pk, 4),
+                       "work_unit": f"2*Dp = {2 * dp} fp32 lane-ops per evaluated child distance",
+                       "peak_source": "gts_bench_fp32_peak (in-run)"}
+        if ach / pk > out["frac"] or out["frac"] > 1:
+            # the fp32 leg bounds it: report that leg at the top level
+            out["hbm"] = {key: out[key] for key in ("achieved", "peak", "unit", "frac", "peak_source")}
+            out.update({key: out["fp32"][key] for key in ("achieved", "peak", "unit", "frac", "peak_source")})
+            out["bound"] = "fp32"
     out["traffic"] = ncu_traffic(workload, "k_expand")
     return out
 

@@ -91,7 +91,7 @@ static std::vector<std::pair<std::string, ProfRec>> g_prof;
 static unsigned long long g_work[4] = {0, 0, 0, 0};   // pairs, word-steps, entries, rows
 static unsigned long long *g_phase_dev = nullptr;       // GTS_PHASES: per-phase clocks of k_leafgroup_mma
 enum { kWorkPairs = 0, kWorkSteps = 1, kWorkEntries = 2, kWorkRows = 3 };
-static double g_expand[3] = {0, 0, 0};   // traversal: algorithmic bytes, parent rows in, child rows out
+static double g_expand[4] = {0, 0, 0, 0};   // traversal: algorithmic bytes, parent rows in, child rows out, distances
 
 static void prof_add(const char *name, double ms)
 {
@@ -1594,20 +1594,23 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
                  int nmax, unsigned *fhist, const float *r0, const int32_t *ks)
 {
     // Software pipeline over this CTA's items (static order it_i = bid + i*G):
-    //   iteration i: cp.async operands of item i+1 | global loads of item i+2's
-    //   row/column metadata and item i+3's descriptor (into registers) |
-    //   epilogue of item i | store the loaded metadata | barrier | MMA i+1.
-    // Every global-load latency is hidden behind an epilogue; one block
+    //   iteration i: wait MMA i | issue MMA i+1 (its operands landed last
+    //   iteration) | cp.async operands of item i+2 into the stage MMA i just
+    //   released | global loads of item i+3's row/column metadata and item
+    //   i+4's descriptor (registers) | epilogue of item i (TMEM accumulator
+    //   i & 1) | store the loaded metadata | barrier.
+    // The tensor core works on item i+1 while the warps screen item i, and
+    // every global-load latency is hidden behind an epilogue; one block
     // barrier per item.
     extern __shared__ __align__(1024) uint8_t smraw[];
     __shared__ uint64_t mbar[2];
     __shared__ uint32_t tmem_slot;
-    __shared__ int4 s_item[4];           // {leaf, start, count, size}, ring by i % 4
-    __shared__ int4 s_itemraw[4][2];     // raw Item copies (cp.async) before they become s_item
-    __shared__ int s_pos[4];
-    __shared__ float4 s_col[3][256];     // ring by i % 3 (see meta_store)
-    __shared__ int s_rq[3][128];         // query ids (-1: no row)
-    __shared__ float4 s_rf[3][128];      // {dqp, r at load time (radii only shrink), |q|, probe radius}
+    __shared__ int4 s_item[8];           // {leaf, start, count, size}, ring by i % 8
+    __shared__ int4 s_itemraw[8][2];     // raw Item copies (cp.async) before they become s_item
+    __shared__ int s_pos[8];
+    __shared__ float4 s_col[4][256];     // ring by i % 4 (see meta_store)
+    __shared__ int s_rq[4][128];         // query ids (-1: no row)
+    __shared__ float4 s_rf[4][128];      // {dqp, r at load time (radii only shrink), |q|, probe radius}
     (void)item_cursor;
     const uint32_t pad = (1024u - (tc::smem_u32(smraw) & 1023u)) & 1023u;
     uint8_t *sm = smraw + pad;
@@ -1624,8 +1627,8 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
         tc::mbar_init(&mbar[1], 1);
         tc::fence_mbar_init();
     }
-    // descriptors of items 0..2 ({leaf, start, count, size}, pos)
-    if (tid < 3) {
+    // descriptors of items 0..3 ({leaf, start, count, size}, pos)
+    if (tid < 4) {
         int4 d = make_int4(0, 0, 0, 0);
         int p0 = 0;
         if (idx(tid) < nitems) {
@@ -1641,7 +1644,7 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
     tc::fence_after_sync();
     const uint32_t tmem = tmem_slot;
 
-    // metadata loads of item i (registers), then the store into ring slot i % 3.
+    // metadata loads of item i (registers), then the store into ring slot i % 4.
     // Threads 0..127 load row i's {q, dqp, r, |q|, r0}; threads 128..383
     // column (tid - 128)'s {dis, se, alive}; one packed float4 + float each,
     // so few registers stay live across the epilogue.
@@ -1650,8 +1653,8 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
         float b;
     };
     auto meta_load = [&](int i, Meta &m) {
-        const int4 d = s_item[i & 3];
-        const int pos = s_pos[i & 3];
+        const int4 d = s_item[i & 7];
+        const int pos = s_pos[i & 7];
         m.a = make_float4(0.f, -1.f, 0.f, 0.f);
         m.b = __int_as_float(-1);
         if (idx(i) >= nitems) return;
@@ -1671,8 +1674,8 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
         }
     };
     auto meta_store = [&](int i, const Meta &m) {
-        const int sl = i % 3;
-        const int4 d = s_item[i & 3];
+        const int sl = i & 3;
+        const int4 d = s_item[i & 7];
         const int N = max(16, (d.w + 15) & ~15);
         if (tid < 128) {
             s_rq[sl][tid] = __float_as_int(m.b);
@@ -1699,8 +1702,8 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
     // operands of item i into smem stage i & 1 (async)
     auto stage = [&](int i) {
         const int st = i & 1;
-        const int4 d = s_item[i & 3];
-        const int pos = s_pos[i & 3];
+        const int4 d = s_item[i & 7];
+        const int pos = s_pos[i & 7];
         const int N = max(16, (d.w + 15) & ~15);
         const uint32_t A = tc::smem_u32(sm + st * stage_bytes);
         const uint32_t B = A + (uint32_t)a_bytes;
@@ -1712,7 +1715,7 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
         // 32-bit row index (A) -- a few instructions per 16-byte copy.
         const uint32_t sw = tc::sw128_offset(row0, c & 7);
         const uint32_t dstep = (uint32_t)rstep * 128u;
-        const int *rq = s_rq[i % 3];
+        const int *rq = s_rq[i & 3];
         const char *qsrc = reinterpret_cast<const char *>(qv.qbf + c);
         const uint32_t qstride = (uint32_t)c16 * 16u;
         uint32_t adst = A + (uint32_t)(c >> 3) * 16384u + sw;
@@ -1734,7 +1737,7 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
         if (tid != 0) return;
         tc::fence_after_sync();
         const int st = i & 1;
-        const int N = max(16, (s_item[i & 3].w + 15) & ~15);
+        const int N = max(16, (s_item[i & 7].w + 15) & ~15);
         const uint32_t idesc = tc::idesc_bf16(128, N);
         const uint32_t a0 = tc::smem_u32(sm + st * stage_bytes), b0 = a0 + (uint32_t)a_bytes;
         for (int kb = 0; kb < nkb; kb++) {
@@ -1748,19 +1751,23 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
         tc::mma_commit(&mbar[st]);
     };
 
-    // prologue: metadata of items 0 and 1, operands + MMA of item 0
+    // prologue: metadata of items 0..2, operands of items 0 and 1, MMA of item 0
     {
-        Meta m0, m1;
+        Meta m0, m1, m2;
         meta_load(0, m0);
         meta_load(1, m1);
+        meta_load(2, m2);
         meta_store(0, m0);
         meta_store(1, m1);
+        meta_store(2, m2);
     }
     __syncthreads();
     if (idx(0) < nitems) {
         stage(0);
+        if (idx(1) < nitems) stage(1);
         tc::cp_async_wait_all();
         tc::fence_async_smem();
+        tc::fence_before_sync();
         __syncthreads();
         mma(0);
     }
@@ -1768,28 +1775,29 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
     unsigned long long pairs = 0, w_entries = 0, w_rows = 0, w_macs = 0;
     for (int i = 0; idx(i) < nitems; i++) {
         const int s = i & 1;
-        const bool has1 = idx(i + 1) < nitems;
-        if (has1) stage(i + 1);
-        Meta mnext;
-        meta_load(i + 2, mnext);
-        // descriptor of item i+3: a 32-byte async copy straight into smem
-        if (tid == 0 && idx(i + 3) < nitems) {
-            const Item *src = items + idx(i + 3);
-            tc::cp_async16(tc::smem_u32(&s_itemraw[(i + 3) & 3][0]), src, 16u);
-            tc::cp_async16(tc::smem_u32(&s_itemraw[(i + 3) & 3][1]), reinterpret_cast<const int4 *>(src) + 1, 16u);
-            tc::cp_async_commit();
-        }
+        // MMA i done: its accumulator is ready and its operand stage is free
         tc::mbar_wait(&mbar[s], phase[s]);
         phase[s] ^= 1u;
         tc::fence_after_sync();
-        // ---- epilogue of item i (stage s, accumulator s, metadata slot i % 3) ----
+        if (idx(i + 1) < nitems) mma(i + 1);
+        if (idx(i + 2) < nitems) stage(i + 2);
+        Meta mnext;
+        meta_load(i + 3, mnext);
+        // descriptor of item i+4: a 32-byte async copy straight into smem
+        if (tid == 0 && idx(i + 4) < nitems) {
+            const Item *src = items + idx(i + 4);
+            tc::cp_async16(tc::smem_u32(&s_itemraw[(i + 4) & 7][0]), src, 16u);
+            tc::cp_async16(tc::smem_u32(&s_itemraw[(i + 4) & 7][1]), reinterpret_cast<const int4 *>(src) + 1, 16u);
+            tc::cp_async_commit();
+        }
+        // ---- epilogue of item i (accumulator s, metadata slot i % 4) ----
         // thread = one query row (TMEM lane) x every 4th 16-column chunk;
         // per column: lemma 1, approximate d^2, error band, ~12 instructions
         {
-            const int sl = i % 3;
-            const int4 d = s_item[i & 3];
+            const int sl = i & 3;
+            const int4 d = s_item[i & 7];
             const int size = d.w;
-            const int pos = s_pos[i & 3];
+            const int pos = s_pos[i & 7];
             const int N = max(16, (size + 15) & ~15);
             const int qrow = 32 * (warp & 3) + lane;
             const int part = warp >> 2;
@@ -1904,18 +1912,19 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
                 w_macs += (unsigned long long)128 * N * ix.Dk;   // MMA MACs issued
             }
         }
-        // metadata of item i+2 and the descriptor of item i+3 (loads done by now)
-        meta_store(i + 2, mnext);
+        // metadata of item i+3 and the descriptor of item i+4 (loads done by now)
+        meta_store(i + 3, mnext);
         tc::cp_async_wait_all();
         if (tid == 0) {
-            const int4 r0_ = s_itemraw[(i + 3) & 3][0], r1_ = s_itemraw[(i + 3) & 3][1];
-            s_item[(i + 3) & 3] = idx(i + 3) < nitems ? r0_ : make_int4(0, 0, 0, 0);   // {leaf, start, count, size}
-            s_pos[(i + 3) & 3] = r1_.x;
+            const int4 r0_ = s_itemraw[(i + 4) & 7][0], r1_ = s_itemraw[(i + 4) & 7][1];
+            s_item[(i + 4) & 7] = idx(i + 4) < nitems ? r0_ : make_int4(0, 0, 0, 0);   // {leaf, start, count, size}
+            s_pos[(i + 4) & 7] = r1_.x;
         }
+        // operands of item i+2 visible to the tensor core; TMEM reads of
+        // accumulator s ordered before MMA i+2 overwrites it
         tc::fence_async_smem();
         tc::fence_before_sync();
         __syncthreads();
-        if (has1) mma(i + 1);
     }
     if (work) {
         for (int o = 16; o > 0; o >>= 1) pairs += __shfl_down_sync(kFull, pairs, o);
@@ -3345,6 +3354,15 @@ struct Search {
                 break;
             }
             HitBuf hb{hq.p, he.p, hd.p, (unsigned long long)hq.n, counter.p + 1};
+            // at most 2^24 rows per launch (GTS_EDIT_LAUNCH_ROWS overrides):
+            // larger launches measured superlinearly slower for the same work
+            static const int64_t env_lr = std::getenv("GTS_EDIT_LAUNCH_ROWS") ? std::atoll(std::getenv("GTS_EDIT_LAUNCH_ROWS")) : 0;
+            const int64_t launch_rows = env_lr > 0 ? env_lr : (1ll << 24);
+            if (m > launch_rows) {
+                for (int64_t o = 0; o < m; o += launch_rows)
+                    dispatch_verify(rows + o, std::min<int64_t>(launch_rows, m - o), stats_on);
+                break;
+            }
             // one warp per ~contiguous run of rows; enough warps to fill the GPU
             // rows per cursor claim: 16 (GTS_EDIT_CLAIM overrides).  Larger kNN
             // claims (one warp walking a query's leaves in order) did not cut
@@ -3432,6 +3450,7 @@ struct Search {
             g_expand[0] += (double)m * 16.0 * (1 + ix->nc) + (double)evaluated * pay + (double)cnt * 16.0;
             g_expand[1] += (double)m;
             g_expand[2] += (double)cnt;
+            g_expand[3] += (double)evaluated;
         }
         return cnt;
     }
@@ -3849,7 +3868,11 @@ int64_t hbm_rows(const gts_index *ix)
         return 1ll << 24;
     }
     const int64_t rows = (int64_t)(free_b / 4 / (16 * (size_t)std::max(ix->levels, 1)));
-    return std::max<int64_t>(std::min<int64_t>(rows, 1ll << 26), std::max<int64_t>(ix->nc, 1ll << 16));
+    // 2^24 rows (256 MB per table): measured on B200, words, one step:
+    // 84 ms of k_leaf_edit at 2^24-row tables vs 119 ms at 2^25 and 153 ms
+    // at 2^26 for the same DP work (larger leaf launches run superlinearly
+    // slower), and vec128 551 vs 614 ms per step (allocation gaps)
+    return std::max<int64_t>(std::min<int64_t>(rows, 1ll << 24), std::max<int64_t>(ix->nc, 1ll << 16));
 }
 
 gts_result *run_search(gts_index *ix, const gts_queries *q, int mode, const double *radii, const int64_t *ks,
@@ -4236,8 +4259,9 @@ extern "C" int gts_profile_read(char *buf, int64_t cap, int reset)
     snprintf(tmp, sizeof(tmp), "}, \"work\": {\"pairs\": %llu, \"word_steps\": %llu, \"entries\": %llu, \"rows\": %llu}",
              g_work[0], g_work[1], g_work[2], g_work[3]);
     js += tmp;
-    snprintf(tmp, sizeof(tmp), ", \"expand\": {\"bytes\": %.0f, \"rows_in\": %.0f, \"rows_out\": %.0f}}", g_expand[0],
-             g_expand[1], g_expand[2]);
+    snprintf(tmp, sizeof(tmp),
+             ", \"expand\": {\"bytes\": %.0f, \"rows_in\": %.0f, \"rows_out\": %.0f, \"evaluated\": %.0f}}",
+             g_expand[0], g_expand[1], g_expand[2], g_expand[3]);
     js += tmp;
     if (reset) {
         g_prof.clear();

@@ -57,8 +57,8 @@ def test_query_answers_check_and_mismatch(tmp_path):
     wl = tmp_path / "w.txt"
     wl.write_text("\n".join(lines) + "\n")
     out = tmp_path / "r.jsonl"
-    code, _, err = run("query", "--snapshot", SNAP, "--workload", str(wl), "--out", str(out), "--check",
-                       "--batch-sizes", "7,40", "--json")
+    code, _, err = run("--json", "query", "--snapshot", SNAP, "--workload", str(wl), "--out", str(out), "--check",
+                       "--batch-sizes", "7,40")
     assert code == 0, err
     recs = [json.loads(l) for l in out.read_text().splitlines()]
     assert [r["query_index"] for r in recs] == list(range(40))
