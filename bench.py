@@ -53,13 +53,15 @@ WORKLOADS = {
     # configs[2]: 128-d L2 n=1M, kNN k=10, 100k-query batch (clustered)
     "vec128": dict(metric="l2", n=1_000_000, nq=100_000, dim=128, clusters=1000, spread=0.05, noise=0.01,
                    radius=0.5, k=10, config_index=2),
-    # configs[4] single shard: 32-d L1, 12.5M per GPU at 8 GPUs, kNN k=100
-    "l1shard": dict(metric="l1", n=12_500_000, nq=100_000, dim=32, clusters=10_000, spread=0.05, noise=0.01,
+    # configs[4] single shard: 32-d L1, 12.5M per GPU at 8 GPUs, kNN k=100.
+    # C5 uses the reference generator's default spread (generate_clustered(...,
+    # spread=0.01), data.py:405); C3 (vec128) keeps SURVEY §8(d)'s 0.05
+    "l1shard": dict(metric="l1", n=12_500_000, nq=100_000, dim=32, clusters=12_500, spread=0.01, noise=0.01,
                     radius=0.5, k=100, config_index=4),
     # configs[4] whole: 32-d L1 n=100M, kNN k=100, 1M-query batch; the
     # collection and the queries are generated on the device (Philox,
     # gts_generate_clustered), one shard per GPU, built on the device
-    "l1_100m": dict(metric="l1", n=100_000_000, nq=1_000_000, dim=32, clusters=100_000, spread=0.05, noise=0.01,
+    "l1_100m": dict(metric="l1", n=100_000_000, nq=1_000_000, dim=32, clusters=100_000, spread=0.01, noise=0.01,
                     radius=0.5, k=100, config_index=4, device_gen=True, modes=(1,)),
 }
 
@@ -634,6 +636,10 @@ def run_ours(args, rank, world, local_rank):
     out["roofline"] = roofline(eng, prof, kver, step_ms_prof)
     out["roofline"]["traversal"] = traversal_roofline(prof, args.workload, w.get("dim") if w["metric"] != "edit" else None)
     out["roofline"]["traffic"] = ncu_traffic(args.workload, kname)
+    if out["roofline"]["traffic"] is not None:
+        out["roofline"]["traffic_note"] = ("DRAM bytes (read + write) of one launch of this kernel from the "
+                                           "committed ncu --set full capture (profiles/ncu_traffic.json); "
+                                           "compare with achieved x average launch time")
     if world == 1 and not args.no_cpu_baseline:
         if w.get("device_gen"):
             out["cpu_baseline"], out["parity"] = scan_baseline(w, gpu_answers, eng.modes)
@@ -981,7 +987,8 @@ def ncu_traffic(workload, kernel):
     if not os.path.exists(path):
         return None
     tab = json.load(open(path))
-    return tab.get(f"{workload}:{kernel}")
+    e = tab.get(f"{workload}:{kernel}")
+    return e["dram_bytes_per_launch"] if isinstance(e, dict) else e
 
 
 # Algorithmic integer ops per word-step: the 10-op Hyyro recurrence.

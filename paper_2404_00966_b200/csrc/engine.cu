@@ -689,6 +689,7 @@ constexpr int kLgItemRows = 512;   // rows per item: leaf staging amortised over
 
 struct LgEditLayout {              // shared-memory carve-up in bytes (host-computed)
     int cap_e, cap_w;              // staged entries / text words per leaf
+    int tstride;                   // text words per staged entry (odd; fits the longest stored string)
     int wmax, slot_words;          // pattern words (<= 4); words per staged slot (wmax * A, padded)
     int use_hist;
     int off_meta, off_h0, off_h1, off_text, off_peq, off_queue, off_slot, total;
@@ -738,8 +739,9 @@ k_leafgroup_edit(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
         const int size = ix.node[item.leaf].size;
         const int pos = ix.npos[item.leaf];
         if (size == 0) continue;
-        // entries are length-sorted inside a leaf: the last is the longest
-        const int tstride = ((__ldg(ix.slen + pos + size - 1) + 3) >> 2) | 1;
+        // one stride for every leaf: entries inserted in place (leaf slack)
+        // break the in-leaf length order, so the last entry need not be the longest
+        const int tstride = L.tstride;
         for (int k = threadIdx.x; k < size; k += blockDim.x) {
             const int e = pos + k;
             const uint4 rec = __ldg(ix.erec + e);
@@ -1584,26 +1586,35 @@ __global__ void __launch_bounds__(kMmaThreads, 3) k_leafgroup_mma(IndexView ix, 
 //    per-query histogram (their true distance is at most that bound), so the
 //    radius shrinks as the pass goes, exactly as with exact hits.
 // ---------------------------------------------------------------------------
-constexpr int kM2Threads = 512;   // 16 warps: 4 per TMEM lane quadrant
-
-
-__global__ void __launch_bounds__(kM2Threads, 1)
+// Two shapes (template NT threads, NSTAGE operand stages / accumulators):
+//  * NT = 512, NSTAGE = 2 (default): one CTA per SM; MMA i+1 overlaps the
+//    epilogue of item i inside the CTA;
+//  * NT = 256, NSTAGE = 1 (GTS_MMA_SHAPE=256): two CTAs per SM (91 KB of
+//    shared memory, 128 TMEM columns each), MMA i+1 issued after the item-i
+//    barrier, in the hope that the other CTA covers barrier waits (ncu: the
+//    barrier is the top stall of the one-CTA shape).  Measured slower on
+//    B200 (443 vs 343 ms of this kernel per vec128 step).
+template <int NT, int NSTAGE>
+__global__ void __launch_bounds__(NT, NT == 512 ? 1 : 2)
 k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, const Item *__restrict__ items, int nitems,
                  unsigned long long *item_cursor, float *r32, double *r64, CandBuf cb,
                  unsigned long long *verified_stat, int stats_on, unsigned long long *work, uint32_t acc_cols,
                  int nmax, unsigned *fhist, const float *r0, const int32_t *ks)
 {
-    // Software pipeline over this CTA's items (static order it_i = bid + i*G):
-    //   iteration i: wait MMA i | issue MMA i+1 (its operands landed last
-    //   iteration) | cp.async operands of item i+2 into the stage MMA i just
-    //   released | global loads of item i+3's row/column metadata and item
-    //   i+4's descriptor (registers) | epilogue of item i (TMEM accumulator
-    //   i & 1) | store the loaded metadata | barrier.
-    // The tensor core works on item i+1 while the warps screen item i, and
-    // every global-load latency is hidden behind an epilogue; one block
+    // Software pipeline over this CTA's items (static order it_i = bid + i*G).
+    //   NSTAGE 2, iteration i: wait MMA i | issue MMA i+1 (its operands landed
+    //   last iteration) | cp.async operands of item i+2 into the stage MMA i
+    //   just released | global loads of item i+3's row/column metadata and
+    //   item i+4's descriptor (registers) | epilogue of item i (TMEM
+    //   accumulator i & 1) | store the loaded metadata | barrier.
+    //   NSTAGE 1: wait MMA i | cp.async operands of item i+1 into the stage
+    //   MMA i released | metadata / descriptor loads | epilogue of item i |
+    //   stores | barrier | MMA i+1.
+    // Every global-load latency is hidden behind an epilogue; one block
     // barrier per item.
+    constexpr int LA = NSTAGE == 2 ? 1 : 0;   // extra lookahead of the two-stage order
     extern __shared__ __align__(1024) uint8_t smraw[];
-    __shared__ uint64_t mbar[2];
+    __shared__ uint64_t mbar[NSTAGE];
     __shared__ uint32_t tmem_slot;
     __shared__ int4 s_item[8];           // {leaf, start, count, size}, ring by i % 8
     __shared__ int4 s_itemraw[8][2];     // raw Item copies (cp.async) before they become s_item
@@ -1621,10 +1632,9 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
     const size_t stage_bytes = a_bytes + (size_t)nkb * nmax * 128;
     const int G = gridDim.x;
     auto idx = [&](int i) { return (int)blockIdx.x + i * G; };
-    if (warp == 0) tc::tmem_alloc(&tmem_slot, 2 * acc_cols);
+    if (warp == 0) tc::tmem_alloc(&tmem_slot, NSTAGE * acc_cols);
     if (tid == 0) {
-        tc::mbar_init(&mbar[0], 1);
-        tc::mbar_init(&mbar[1], 1);
+        for (int k = 0; k < NSTAGE; k++) tc::mbar_init(&mbar[k], 1);
         tc::fence_mbar_init();
     }
     // descriptors of items 0..3 ({leaf, start, count, size}, pos)
@@ -1645,18 +1655,21 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
     const uint32_t tmem = tmem_slot;
 
     // metadata loads of item i (registers), then the store into ring slot i % 4.
-    // Threads 0..127 load row i's {q, dqp, r, |q|, r0}; threads 128..383
-    // column (tid - 128)'s {dis, se, alive}; one packed float4 + float each,
-    // so few registers stay live across the epilogue.
+    // Threads 0..127 load row i's {q, dqp, r, |q|, r0}; the others the
+    // columns j = tid - 128 (+ NT - 128) {dis, se, alive}; packed floats, so
+    // few registers stay live across the epilogue.
+    constexpr int CPT = NT == 512 ? 1 : 2;   // columns per thread (<= 256 columns)
     struct Meta {
         float4 a;
         float b;
+        float4 c2;   // second column (CPT 2)
     };
     auto meta_load = [&](int i, Meta &m) {
         const int4 d = s_item[i & 7];
         const int pos = s_pos[i & 7];
         m.a = make_float4(0.f, -1.f, 0.f, 0.f);
         m.b = __int_as_float(-1);
+        m.c2 = make_float4(0.f, 0.f, 0.f, 0.f);
         if (idx(i) >= nitems) return;
         if (tid < 128) {
             if (tid < d.z) {
@@ -1671,25 +1684,27 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
                 m.a.y = __ldg(ix.vse + pos + j);
                 m.a.z = is_alive(ix.alive, pos + j) ? 1.f : 0.f;
             }
+            if (CPT == 2 && j + (NT - 128) < d.w) {
+                const int j2 = j + (NT - 128);
+                m.c2.x = __ldg(ix.dis + pos + j2);
+                m.c2.y = __ldg(ix.vse + pos + j2);
+                m.c2.z = is_alive(ix.alive, pos + j2) ? 1.f : 0.f;
+            }
         }
     };
     auto meta_store = [&](int i, const Meta &m) {
         const int sl = i & 3;
         const int4 d = s_item[i & 7];
         const int N = max(16, (d.w + 15) & ~15);
-        if (tid < 128) {
-            s_rq[sl][tid] = __float_as_int(m.b);
-            s_rf[sl][tid] = m.a;
-        } else if (tid - 128 < N) {
-            const int j = tid - 128;
-            // {dis | NaN, y - z | NaN, y + z, dis}: NaN (tombstone / padding)
-            // fails the lemma-1 window and the screen
+        // {dis | NaN, y - z | NaN, y + z, dis}: NaN (tombstone / padding)
+        // fails the lemma-1 window and the screen
+        auto put = [&](int j, const float4 &mc) {
             const float nan = __int_as_float(0x7fc00000);
             float4 col = make_float4(nan, nan, 0.f, INFINITY);
             if (j < d.w) {
-                const float dis = m.a.x, se = m.a.y;
+                const float dis = mc.x, se = mc.y;
                 const float y = fmaf(dis, dis, 2.f * se), z = 8.f * ix.rel * dis * dis;
-                if (m.a.z != 0.f) {
+                if (mc.z != 0.f) {
                     col.x = dis;
                     col.y = y - z;
                 }
@@ -1697,18 +1712,25 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
                 col.w = dis;
             }
             s_col[sl][j] = col;
+        };
+        if (tid < 128) {
+            s_rq[sl][tid] = __float_as_int(m.b);
+            s_rf[sl][tid] = m.a;
+        } else {
+            if (tid - 128 < N) put(tid - 128, m.a);
+            if (CPT == 2 && tid - 128 + (NT - 128) < N) put(tid - 128 + (NT - 128), m.c2);
         }
     };
-    // operands of item i into smem stage i & 1 (async)
+    // operands of item i into smem stage i % NSTAGE (async)
     auto stage = [&](int i) {
-        const int st = i & 1;
+        const int st = NSTAGE == 2 ? (i & 1) : 0;
         const int4 d = s_item[i & 7];
         const int pos = s_pos[i & 7];
         const int N = max(16, (d.w + 15) & ~15);
         const uint32_t A = tc::smem_u32(sm + st * stage_bytes);
         const uint32_t B = A + (uint32_t)a_bytes;
         const int lc = c16 == 16 ? 4 : 3;
-        const int c = tid & (c16 - 1), row0 = tid >> lc, rstep = kM2Threads >> lc;
+        const int c = tid & (c16 - 1), row0 = tid >> lc, rstep = NT >> lc;
         // rstep is a multiple of 8, so every row this thread copies has the
         // same (row & 7) and the same SW128 chunk permutation: the smem
         // address advances by rstep rows, the source by rstep (B) or by a
@@ -1736,7 +1758,7 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
     auto mma = [&](int i) {
         if (tid != 0) return;
         tc::fence_after_sync();
-        const int st = i & 1;
+        const int st = NSTAGE == 2 ? (i & 1) : 0;
         const int N = max(16, (s_item[i & 7].w + 15) & ~15);
         const uint32_t idesc = tc::idesc_bf16(128, N);
         const uint32_t a0 = tc::smem_u32(sm + st * stage_bytes), b0 = a0 + (uint32_t)a_bytes;
@@ -1751,20 +1773,20 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
         tc::mma_commit(&mbar[st]);
     };
 
-    // prologue: metadata of items 0..2, operands of items 0 and 1, MMA of item 0
+    // prologue: metadata of items 0..1+LA, operands of items 0..LA, MMA of item 0
     {
         Meta m0, m1, m2;
         meta_load(0, m0);
         meta_load(1, m1);
-        meta_load(2, m2);
+        if (LA) meta_load(2, m2);
         meta_store(0, m0);
         meta_store(1, m1);
-        meta_store(2, m2);
+        if (LA) meta_store(2, m2);
     }
     __syncthreads();
     if (idx(0) < nitems) {
         stage(0);
-        if (idx(1) < nitems) stage(1);
+        if (LA && idx(1) < nitems) stage(1);
         tc::cp_async_wait_all();
         tc::fence_async_smem();
         tc::fence_before_sync();
@@ -1774,20 +1796,21 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
     uint32_t phase[2] = {0u, 0u};
     unsigned long long pairs = 0, w_entries = 0, w_rows = 0, w_macs = 0;
     for (int i = 0; idx(i) < nitems; i++) {
-        const int s = i & 1;
+        const int s = NSTAGE == 2 ? (i & 1) : 0;
         // MMA i done: its accumulator is ready and its operand stage is free
         tc::mbar_wait(&mbar[s], phase[s]);
         phase[s] ^= 1u;
         tc::fence_after_sync();
-        if (idx(i + 1) < nitems) mma(i + 1);
-        if (idx(i + 2) < nitems) stage(i + 2);
+        if (LA && idx(i + 1) < nitems) mma(i + 1);
+        if (idx(i + 1 + LA) < nitems) stage(i + 1 + LA);
         Meta mnext;
-        meta_load(i + 3, mnext);
-        // descriptor of item i+4: a 32-byte async copy straight into smem
-        if (tid == 0 && idx(i + 4) < nitems) {
-            const Item *src = items + idx(i + 4);
-            tc::cp_async16(tc::smem_u32(&s_itemraw[(i + 4) & 7][0]), src, 16u);
-            tc::cp_async16(tc::smem_u32(&s_itemraw[(i + 4) & 7][1]), reinterpret_cast<const int4 *>(src) + 1, 16u);
+        meta_load(i + 2 + LA, mnext);
+        // descriptor of item i+3+LA: a 32-byte async copy straight into smem
+        const int nd = i + 3 + LA;
+        if (tid == 0 && idx(nd) < nitems) {
+            const Item *src = items + idx(nd);
+            tc::cp_async16(tc::smem_u32(&s_itemraw[nd & 7][0]), src, 16u);
+            tc::cp_async16(tc::smem_u32(&s_itemraw[nd & 7][1]), reinterpret_cast<const int4 *>(src) + 1, 16u);
             tc::cp_async_commit();
         }
         // ---- epilogue of item i (accumulator s, metadata slot i % 4) ----
@@ -1800,7 +1823,7 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
             const int pos = s_pos[i & 7];
             const int N = max(16, (size + 15) & ~15);
             const int qrow = 32 * (warp & 3) + lane;
-            const int part = warp >> 2;
+            const int part = warp >> 2;   // NT / 128 parts of the columns
             const int q = s_rq[sl][qrow];
             const bool valid = q >= 0;
             const float4 rf = s_rf[sl][qrow];
@@ -1834,7 +1857,7 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
             unsigned ver = 0;
             const uint32_t lane_base = tmem + s * acc_cols + ((uint32_t)((warp & 3) * 32) << 16);
             const float4 *cols = s_col[sl];
-            for (int c0 = 16 * part; c0 < N; c0 += 64) {
+            for (int c0 = 16 * part; c0 < N; c0 += 16 * (NT / 128)) {
                 float acc[16];
                 tc::tmem_ld16(lane_base + (uint32_t)c0, acc);   // warp-collective
                 uint32_t win = 0, cm = 0;
@@ -1912,19 +1935,20 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
                 w_macs += (unsigned long long)128 * N * ix.Dk;   // MMA MACs issued
             }
         }
-        // metadata of item i+3 and the descriptor of item i+4 (loads done by now)
-        meta_store(i + 3, mnext);
+        // metadata of item i+2+LA and the descriptor of item i+3+LA (loads done by now)
+        meta_store(i + 2 + LA, mnext);
         tc::cp_async_wait_all();
         if (tid == 0) {
-            const int4 r0_ = s_itemraw[(i + 4) & 7][0], r1_ = s_itemraw[(i + 4) & 7][1];
-            s_item[(i + 4) & 7] = idx(i + 4) < nitems ? r0_ : make_int4(0, 0, 0, 0);   // {leaf, start, count, size}
-            s_pos[(i + 4) & 7] = r1_.x;
+            const int4 r0_ = s_itemraw[nd & 7][0], r1_ = s_itemraw[nd & 7][1];
+            s_item[nd & 7] = idx(nd) < nitems ? r0_ : make_int4(0, 0, 0, 0);   // {leaf, start, count, size}
+            s_pos[nd & 7] = r1_.x;
         }
-        // operands of item i+2 visible to the tensor core; TMEM reads of
-        // accumulator s ordered before MMA i+2 overwrites it
+        // operands of the next staged item visible to the tensor core; TMEM
+        // reads of accumulator s ordered before the MMA that overwrites it
         tc::fence_async_smem();
         tc::fence_before_sync();
         __syncthreads();
+        if (!LA && idx(i + 1) < nitems) mma(i + 1);
     }
     if (work) {
         for (int o = 16; o > 0; o >>= 1) pairs += __shfl_down_sync(kFull, pairs, o);
@@ -1938,7 +1962,7 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
-    if (warp == 0) tc::tmem_dealloc(tmem, 2 * acc_cols);
+    if (warp == 0) tc::tmem_dealloc(tmem, NSTAGE * acc_cols);
 }
 
 // Exact float64 recheck of screened candidates against the final radius
@@ -2807,6 +2831,7 @@ struct gts_index {
     std::atomic<unsigned long long> cand_hint{0};                // tensor-core candidates of the last launch
     // pending-insert cache (device copy of the caller's pending set)
     int cache_n = 0;
+    int cache_max_len = 0;   // strings: longest pending-cache string
     DBuf<int64_t> cache_ids;
     DBuf<float> cache_vec32;
     DBuf<double> cache_vec64;
@@ -3110,7 +3135,8 @@ struct Search {
         const int wmax = std::max(1, (qs->max_len + 31) >> 5);
         if (wmax > 4 || ix->max_len > 65535) return L;
         L.cap_e = std::max(ix->max_leaf, 1);
-        L.cap_w = L.cap_e * ((((ix->max_len + 3) >> 2)) | 1);
+        L.tstride = (((ix->max_len + 3) >> 2)) | 1;
+        L.cap_w = L.cap_e * L.tstride;
         L.wmax = wmax;
         L.slot_words = ((wmax * ix->A + 7) & ~7) | 8;   // odd multiple of 8: slots land on different banks
         L.use_hist = ix->ehist.p != nullptr;
@@ -3161,23 +3187,37 @@ struct Search {
     // candidate pairs (k_recheck)
     void launch_mma2(const Row *srows, const Item *items, int nitems, int stats_on)
     {
+        // default: one 512-thread CTA per SM, two stages (343 ms per vec128
+        // step); GTS_MMA_SHAPE=256 runs two 256-thread one-stage CTAs per SM
+        // (measured 443 ms: the shorter epilogues do not cover the exposed
+        // MMA and copy latency)
+        static const bool two_cta = std::getenv("GTS_MMA_SHAPE") && std::atoi(std::getenv("GTS_MMA_SHAPE")) == 256;
+        if (two_cta) launch_mma2_shape<256, 1>(srows, items, nitems, stats_on, 2);
+        else launch_mma2_shape<512, 2>(srows, items, nitems, stats_on, 1);
+    }
+
+    template <int NT, int NSTAGE>
+    void launch_mma2_shape(const Row *srows, const Item *items, int nitems, int stats_on, int per_sm)
+    {
         const int nmax = std::max(16, (ix->max_leaf + 15) & ~15);
         uint32_t cols = 32;
         while ((int)cols < nmax) cols <<= 1;
         const size_t nkb = (size_t)ix->Dk / 64;
-        const size_t smb = 2 * (nkb * 16384 + nkb * (size_t)nmax * 128) + 1024;
-        smem_optin((const void *)k_leafgroup_mma2, smb);
-        int sms = 148;
+        const size_t smb = NSTAGE * (nkb * 16384 + nkb * (size_t)nmax * 128) + 1024;
+        smem_optin((const void *)k_leafgroup_mma2<NT, NSTAGE>, smb);
+        int sms = 148, fit = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
-        const unsigned grid = (unsigned)std::min<int>(nitems, sms);   // items i, i + grid, ... per CTA
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, k_leafgroup_mma2<NT, NSTAGE>, NT, smb));
+        per_sm = std::max(1, std::min(per_sm, fit));
+        const unsigned grid = (unsigned)std::min<int>(nitems, sms * per_sm);   // items i, i + grid, ... per CTA
         DBuf<unsigned long long> cur(1, st);
         with_candidates<kMetricL2>([&](const CandBuf &cb, int first) {
             CK(cudaMemsetAsync(cur.p, 0, sizeof(unsigned long long), st));
             timed("k_leafgroup_mma2", [&] {
                 const int on = first && stats_on;
-                k_leafgroup_mma2<<<grid, kM2Threads, smb, st>>>(iv, qv, srows, items, nitems, cur.p, r32.p, r64.p, cb,
-                                                             verified.p, on, on ? work.p : nullptr, cols, nmax,
-                                                             on ? fhist.p : nullptr, r0.p, ks.p);
+                k_leafgroup_mma2<NT, NSTAGE><<<grid, NT, smb, st>>>(iv, qv, srows, items, nitems, cur.p, r32.p, r64.p,
+                                                                  cb, verified.p, on, on ? work.p : nullptr, cols,
+                                                                  nmax, on ? fhist.p : nullptr, r0.p, ks.p);
             });
             LAUNCH_CHECK();
         });
@@ -3779,7 +3819,12 @@ gts_queries *upload_queries(gts_index *ix, const gts_query_batch *qb, cudaStream
             for (int64_t i = 0; i < nq; i++) {
                 int64_t m = qb->offsets[i + 1] - qb->offsets[i];
                 if (m < 0) fail(GTS_EINVAL, "query offsets not monotone");
-                if (m > 32 * kMaxWords) fail(GTS_EINVAL, "query string longer than %d symbols", 32 * kMaxWords);
+                // patterns beyond 32 * kMaxWords symbols run the row-band DP
+                // (myers_banded), which holds per-text-column carries: one
+                // side of every pair must fit 32 * kMaxWords symbols
+                if (m > 32 * kMaxWords && std::max(ix->max_len, ix->cache_max_len) > 32 * kMaxWords)
+                    fail(GTS_EINVAL, "query of %lld symbols against stored strings of more than %d symbols",
+                         (long long)m, 32 * kMaxWords);
                 q->max_len = std::max<int>(q->max_len, (int)m);
                 peq_off[(size_t)i + 1] = peq_off[(size_t)i] + (int64_t)ix->A * ((m + 31) / 32);
             }
@@ -4806,6 +4851,7 @@ extern "C" int gts_index_cache_set(gts_index *ix, const gts_dataset *items, void
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t n = items->n;
     ix->cache_n = 0;
+    ix->cache_max_len = 0;
     ix->cache_radius = 0.f;
     if (n == 0) return GTS_OK;
     if (n > (1 << 30)) fail(GTS_EINVAL, "cache too large");
@@ -4829,6 +4875,8 @@ extern "C" int gts_index_cache_set(gts_index *ix, const gts_dataset *items, void
         h2d(ix->cache_sword.p, wstart.data(), wstart.size(), st);
         ix->cache_slen.alloc(lens.size(), st);
         h2d(ix->cache_slen.p, lens.data(), lens.size(), st);
+        ix->cache_max_len = 0;
+        for (auto l : lens) ix->cache_max_len = std::max<int>(ix->cache_max_len, l);
     } else {
         if (items->dim != ix->D) fail(GTS_EMETRIC, "cache dimensionality %lld != %d", (long long)items->dim, ix->D);
         ix->cache_vec64.alloc((size_t)(n * ix->D), st);
@@ -4928,7 +4976,8 @@ extern "C" int gts_pair_distances(int32_t metric, int64_t np, int64_t dim, const
     std::vector<int64_t> peq_off((size_t)np + 1, 0);
     for (int64_t i = 0; i < np; i++) {
         int64_t m = a_off[i + 1] - a_off[i];
-        if (m > 32 * kMaxWords) fail(GTS_EINVAL, "string too long");
+        if (m > 32 * kMaxWords && b_off[i + 1] - b_off[i] > 32 * kMaxWords)
+            fail(GTS_EINVAL, "both strings of pair %lld longer than %d symbols", (long long)i, 32 * kMaxWords);
         peq_off[(size_t)i + 1] = peq_off[(size_t)i] + (int64_t)A * ((m + 31) / 32);
     }
     DBuf<int32_t> dalpha(std::max<size_t>(alpha.size(), 1), st);

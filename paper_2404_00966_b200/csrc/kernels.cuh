@@ -305,8 +305,44 @@ __device__ __forceinline__ int myers_smem_aw(const uint32_t *peq, int m, const u
     return score;
 }
 
+// Patterns longer than 32 * kMaxWords symbols (texts of at most that many):
+// the same recurrence in row-band order.  Band b (pattern rows 32b..32b+31)
+// sweeps the whole text; the horizontal carry (hp: +1, hm: -1) of every text
+// column passes from band b to band b+1 through two bit arrays of n bits
+// (band 0 sees the top boundary row D[0][j] = j: hp = 1, hm = 0).  The score
+// is n plus the vertical deltas of the last column, summed band by band.
+__device__ __noinline__ int myers_banded(const uint32_t *peq, int W, int m, const uint32_t *__restrict__ t4, int n)
+{
+    uint32_t cp[kMaxWords], cm[kMaxWords];   // per text column: carry of the band above
+    const int nw = (n + 31) >> 5;
+    for (int k = 0; k < nw; k++) { cp[k] = ~0u; cm[k] = 0u; }
+    const uint32_t lastmask = (m & 31) ? ((1u << (m & 31)) - 1u) : ~0u;
+    int score = n;
+    for (int b = 0; b < W; b++) {
+        uint32_t P = ~0u, M = 0u;
+        for (int k = 0; k < nw; k++) {
+            uint32_t op = 0u, om = 0u;
+            const int jn = min(32, n - 32 * k);
+            for (int t = 0; t < jn; t++) {
+                const int j = 32 * k + t;
+                const uint32_t c = (__ldg(t4 + (j >> 2)) >> (8 * (j & 3))) & 0xffu;
+                uint32_t hp = (cp[k] >> t) & 1u, hm = (cm[k] >> t) & 1u;
+                myers_stepb(peq[c * W + b], P, M, hp, hm);
+                op |= hp << t;
+                om |= hm << t;
+            }
+            cp[k] = op;
+            cm[k] = om;
+        }
+        const uint32_t mk = (b == W - 1) ? lastmask : ~0u;
+        score += __popc(P & mk) - __popc(M & mk);
+    }
+    return score;
+}
+
 __device__ __noinline__ int myers_generic(const uint32_t *peq, int W, int m, const uint32_t *__restrict__ t4, int n)
 {
+    if (W > kMaxWords) return n <= 32 * kMaxWords ? myers_banded(peq, W, m, t4, n) : -1;
     uint32_t P[kMaxWords], M[kMaxWords];
     for (int b = 0; b < W; b++) { P[b] = ~0u; M[b] = 0u; }
     for (int j = 0; j < n; j++) {

@@ -36,48 +36,57 @@ __device__ __forceinline__ double exact_dist(const IndexView &ix, const QueryVie
 }
 
 // One thread per item: the descent, the float64 distance to every pivot on
-// the path (dpath[i * levels + l], l = 0 is the root), the leaf reached
-// (-1: no leaf with a free slot under the path).
+// the path (dpath[t * levels + l], l = 0 is the root), the leaf reached
+// (-1: the tree has no free slot).  Item t of this launch is query qidx[t]
+// of the uploaded batch; node_free[v] = free slots in the leaves under node
+// v, so the descent only enters subtrees that can still take the item.
 template <int MET>
-__global__ void k_insert_path(IndexView ix, QueryView qv, int nitems, const int32_t *__restrict__ leaf_cap,
-                              int32_t *out_leaf, double *dpath)
+__global__ void k_insert_path(IndexView ix, QueryView qv, int nitems, const int32_t *__restrict__ qidx,
+                              const int32_t *__restrict__ node_free, int32_t *out_leaf, double *dpath)
 {
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= nitems) return;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nitems) return;
+    const int q = qidx[t];
     const int nc = ix.nc, L = ix.levels;
     int node = 1;
     for (int l = 0; l + 1 < L; l++) {
         const double dv = exact_dist<MET>(ix, qv, q, ix.node[node].piv);
-        dpath[(size_t)q * L + l] = dv;
+        dpath[(size_t)t * L + l] = dv;
         const int c0 = (node - 1) * nc + 2;
+        // nearest ring first; among rings at the same gap (often many hold
+        // d: edit distances to a pivot concentrate), the one whose centre is
+        // nearest, so a batch spreads over the children instead of piling
+        // into the first one
         int best = -1;
-        double bgap = INFINITY;
+        double bgap = INFINITY, bctr = INFINITY;
         if (l + 2 < L) {
             // internal children: rings of distances to this node's pivot
             for (int j = 0; j < nc; j++) {
                 const NodeRec c = ix.node[c0 + j];
-                if (c.size <= 0) continue;
+                if (c.size <= 0 || node_free[c0 + j] <= 0) continue;
                 const double gap = fmax(0.0, fmax((double)c.mn - dv, dv - (double)c.mx));
-                if (gap < bgap) { bgap = gap; best = c0 + j; }
+                const double ctr = fabs(dv - 0.5 * ((double)c.mn + (double)c.mx));
+                if (gap < bgap || (gap == bgap && ctr < bctr)) { bgap = gap; bctr = ctr; best = c0 + j; }
             }
         } else {
             // leaf children: own-pivot ranges, only leaves with a free slot
             for (int j = 0; j < nc; j++) {
                 const NodeRec c = ix.node[c0 + j];
-                if (c.size <= 0 || c.size >= leaf_cap[c0 + j - ix.leaf_first]) continue;
+                if (c.size <= 0 || node_free[c0 + j] <= 0) continue;
                 const double dl = exact_dist<MET>(ix, qv, q, c.piv);
                 const double gap = fmax(0.0, fmax((double)c.mn - dl, dl - (double)c.mx));
-                if (gap < bgap) { bgap = gap; best = c0 + j; }
+                const double ctr = fabs(dl - 0.5 * ((double)c.mn + (double)c.mx));
+                if (gap < bgap || (gap == bgap && ctr < bctr)) { bgap = gap; bctr = ctr; best = c0 + j; }
             }
         }
         node = best;
         if (node < 0) break;
     }
     if (node >= 0 && L >= 1) {
-        if (L == 1 && ix.node[1].size >= leaf_cap[0]) node = -1;
-        if (node >= 0) dpath[(size_t)q * L + (L - 1)] = exact_dist<MET>(ix, qv, q, ix.node[node].piv);
+        if (L == 1 && node_free[1] <= 0) node = -1;
+        if (node >= 0) dpath[(size_t)t * L + (L - 1)] = exact_dist<MET>(ix, qv, q, ix.node[node].piv);
     }
-    out_leaf[q] = node;
+    out_leaf[t] = node;
 }
 
 // Scatter the placed items into their slots.  Vectors: the uploaded
@@ -281,22 +290,59 @@ extern "C" int gts_index_insert(gts_index *ix, const gts_dataset *items, int32_t
     struct QGuard { gts_queries *q; ~QGuard() { delete q; } } qg{q};
     const IndexView iv = make_view(ix, q);
     const QueryView qv = make_qview(ix, q);
-    std::vector<int32_t> hcap((size_t)ix->leaf_count);
-    for (int64_t l = 0; l < ix->leaf_count; l++) hcap[(size_t)l] = (int32_t)ix->leaf_cap[(size_t)l];
-    DBuf<int32_t> dcap, dleaf((size_t)m, st);
-    h2d_vec(dcap, hcap, st);
-    DBuf<double> dpath((size_t)m * ix->levels, st);
-    const unsigned g = grid_for(m, 128);
-    switch (ix->metric) {
-    case GTS_EDIT: k_insert_path<kMetricEdit><<<g, 128, 0, st>>>(iv, qv, (int)m, dcap.p, dleaf.p, dpath.p); break;
-    case GTS_L1: k_insert_path<kMetricL1><<<g, 128, 0, st>>>(iv, qv, (int)m, dcap.p, dleaf.p, dpath.p); break;
-    default: k_insert_path<kMetricL2><<<g, 128, 0, st>>>(iv, qv, (int)m, dcap.p, dleaf.p, dpath.p); break;
-    }
-    LAUNCH_CHECK();
-    const std::vector<int32_t> leaf = d2h_vec(dleaf.p, (size_t)m, st);
-    const std::vector<double> path = d2h_vec(dpath.p, (size_t)m * ix->levels, st);
-    // slots, in item order; ranges of every node on the path widen
+    // Descent rounds: every item of a round descends against the free-slot
+    // counts at the start of the round, so items racing for the same leaf
+    // can overfill it; those are descended again, with the leaves filled by
+    // this batch excluded, for up to eight rounds.
     const int L = ix->levels, nc = ix->nc;
+    std::vector<int32_t> leaf((size_t)m, -1);
+    std::vector<double> path((size_t)m * L, 0.0);
+    std::vector<int32_t> free_((size_t)ix->leaf_count);
+    for (int64_t l = 0; l < ix->leaf_count; l++)
+        free_[(size_t)l] = (int32_t)(ix->leaf_cap[(size_t)l] - ix->leaf_size[(size_t)l]);
+    std::vector<int32_t> todo((size_t)m);
+    for (int64_t j = 0; j < m; j++) todo[(size_t)j] = (int32_t)j;
+    for (int round = 0; round < 8 && !todo.empty(); round++) {
+        const int nt = (int)todo.size();
+        // free slots per node (leaves, then summed up the tree; Eq. 1 parent)
+        std::vector<int32_t> nfree((size_t)ix->nodes + 1, 0);
+        for (int64_t l = 0; l < ix->leaf_count; l++) nfree[(size_t)(ix->leaf_first + l)] = free_[(size_t)l];
+        for (int64_t v = ix->nodes; v >= 2; v--) nfree[(size_t)((v - 2) / nc + 1)] += nfree[(size_t)v];
+        DBuf<int32_t> dfree, dq, dleaf((size_t)nt, st);
+        h2d_vec(dfree, nfree, st);
+        h2d_vec(dq, todo, st);
+        DBuf<double> dpath((size_t)nt * L, st);
+        const unsigned g = grid_for(nt, 128);
+        switch (ix->metric) {
+        case GTS_EDIT: k_insert_path<kMetricEdit><<<g, 128, 0, st>>>(iv, qv, nt, dq.p, dfree.p, dleaf.p, dpath.p); break;
+        case GTS_L1: k_insert_path<kMetricL1><<<g, 128, 0, st>>>(iv, qv, nt, dq.p, dfree.p, dleaf.p, dpath.p); break;
+        default: k_insert_path<kMetricL2><<<g, 128, 0, st>>>(iv, qv, nt, dq.p, dfree.p, dleaf.p, dpath.p); break;
+        }
+        LAUNCH_CHECK();
+        const std::vector<int32_t> rl = d2h_vec(dleaf.p, (size_t)nt, st);
+        const std::vector<double> rp = d2h_vec(dpath.p, (size_t)nt * L, st);
+        std::vector<int32_t> again;
+        for (int t = 0; t < nt; t++) {
+            const int32_t j = todo[(size_t)t], lf = rl[(size_t)t];
+            if (lf < 0) continue;                                   // no free leaf under its path
+            int32_t &fr = free_[(size_t)(lf - ix->leaf_first)];
+            if (fr <= 0) { again.push_back(j); continue; }          // filled by an earlier item of this round
+            fr--;
+            leaf[(size_t)j] = lf;
+            std::copy(rp.begin() + (size_t)t * L, rp.begin() + (size_t)(t + 1) * L, path.begin() + (size_t)j * L);
+        }
+        static const bool trace = std::getenv("GTS_TRACE") != nullptr;
+        if (trace) {
+            int none = 0;
+            for (int t = 0; t < nt; t++) none += rl[(size_t)t] < 0;
+            int64_t tf = 0;
+            for (auto f : free_) tf += f;
+            fprintf(stderr, "[gts] insert round %d: %d items, %d without a leaf, %zu collided, %lld free slots left, "
+                            "levels %d, leaves %d\n", round, nt, none, again.size(), (long long)tf, L, ix->leaf_count);
+        }
+        todo.swap(again);
+    }
+    // slots, in item order; ranges of every node on the path widen
     std::vector<float> hdis((size_t)m, 0.f);
     std::vector<int32_t> hpiv((size_t)m, 0), cslot((size_t)m, -1);
     std::vector<int64_t> cids((size_t)m);
@@ -316,11 +362,6 @@ extern "C" int gts_index_insert(gts_index *ix, const gts_dataset *items, int32_t
         if (lf < 0) continue;
         const int64_t li = lf - ix->leaf_first;
         if (ix->leaf_size[(size_t)li] >= ix->leaf_cap[(size_t)li]) continue;
-        // k_leafgroup_edit stages a leaf with the last entry's length as the
-        // stride: keep each leaf's longest string last
-        if (edit && ix->leaf_size[(size_t)li] > 0 &&
-            lens[(size_t)i] > ix->h_slen[(size_t)(ix->leaf_dpos[(size_t)li] + ix->leaf_size[(size_t)li] - 1)])
-            continue;
         const int64_t s = ix->leaf_dpos[(size_t)li] + ix->leaf_size[(size_t)li];
         ix->leaf_size[(size_t)li]++;
         slots[i] = (int32_t)s;

@@ -30,6 +30,8 @@ def stdlib_words(limit=5000):
                 urllib, re, np):
         for name in dir(mod):
             doc = getattr(getattr(mod, name, None), "__doc__", None) or ""
+            if not isinstance(doc, str):   # e.g. a slot's member_descriptor
+                continue
             for tok in re.findall(r"[a-z]{2,14}", doc.lower()):
                 if re.search(r"[aeiouy]", tok) and not re.search(r"(.)\1\1", tok):
                     words.add(tok)

@@ -86,6 +86,22 @@ def full_capture(path):
     return "\n".join(lines)
 
 
+def capture_traffic(path):
+    """(kernel short name, dram read + write bytes) of a --set full capture."""
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    r = list(csv.reader(io.StringIO(raw)))
+    h, v = r[0], r[2] if len(r) > 2 else r[1]
+    units = r[1] if len(r) > 2 else [""] * len(h)
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    tot = 0.0
+    for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        if m in h:
+            tot += float(v[h.index(m)].replace(",", "")) * scale.get(units[h.index(m)], 1)
+    name = v[h.index("Kernel Name")] if "Kernel Name" in h else "?"
+    short = name.split("(")[0].replace("void ", "").split("<")[0].split("::")[-1].strip()
+    return short, int(tot)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--tag", required=True)
@@ -107,6 +123,14 @@ def main():
                     + sorted(glob.glob(os.path.join(OUT, f"prof_leaf_{a.tag}.ncu-rep")))):
         parts += [f"## full capture `{os.path.basename(rep)}` (ncu --set full --clock-control none)", "",
                   full_capture(rep), ""]
+        # roofline.traffic source for bench.py: DRAM bytes per launch of the captured kernel
+        kname, tb = capture_traffic(rep)
+        tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        tab = json.load(open(tpath)) if os.path.exists(tpath) else {}
+        tab[f"{a.workload}:{kname}"] = {"dram_bytes_per_launch": tb, "capture": os.path.basename(rep),
+                                        "note": "dram__bytes_read.sum + dram__bytes_write.sum, one launch, "
+                                                "ncu --set full --clock-control none"}
+        json.dump(tab, open(tpath, "w"), indent=1, sort_keys=True)
     os.makedirs(os.path.dirname(os.path.abspath(a.out)), exist_ok=True)
     open(a.out, "w").write("\n".join(parts))
     print(a.out)
