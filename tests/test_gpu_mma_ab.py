@@ -1,7 +1,9 @@
-"""A/B: the tensor-core L2 paths (pipelined k_leafgroup_mma2, single-stage
-k_leafgroup_mma) and the CUDA-core path give identical answers and identical
-verified counts (GTS_NO_MMA selects the CUDA-core path at index creation,
-GTS_MMA_V1 the single-stage kernel; each variant runs in its own process)."""
+"""A/B: the tensor-core L2 paths (barrier-free k_leafgroup_mma3, the default;
+block-barrier k_leafgroup_mma2 in both shapes; single-stage k_leafgroup_mma)
+and the CUDA-core path give identical answers and identical verified counts
+(GTS_NO_MMA selects the CUDA-core path at index creation, GTS_MMA_V2 /
+GTS_MMA_SHAPE / GTS_MMA_V1 the older kernels; each variant runs in its own
+process)."""
 
 import json
 import os
@@ -39,10 +41,12 @@ def run(env_extra):
 
 
 def test_mma_equals_cuda_core_path():
-    a = run({})                          # k_leafgroup_mma2 + k_recheck_l2 (default)
+    a = run({})                          # k_leafgroup_mma3 + k_recheck (default)
     b = run({"GTS_NO_MMA": "1"})         # CUDA-core k_leafgroup_vec
     c = run({"GTS_MMA_V1": "1"})         # single-stage k_leafgroup_mma, inline recheck
-    for x in (b, c):
+    d = run({"GTS_MMA_V2": "1"})         # k_leafgroup_mma2, one CTA per SM
+    e = run({"GTS_MMA_V2": "1", "GTS_MMA_SHAPE": "256"})   # k_leafgroup_mma2, two CTAs per SM
+    for x in (b, c, d, e):
         assert a["r"] == x["r"] and a["rd"] == x["rd"]
         assert a["k"] == x["k"] and a["kd"] == x["kd"]
         assert a["ver"] == x["ver"]

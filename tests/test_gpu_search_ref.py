@@ -178,3 +178,28 @@ def test_knn_probe_paths_exact_with_tombstones(probe, metric, dim, n, nc, monkey
     for k in (1, 10, 100, 1500):
         got, _ = eng.knn_batch(queries, k)
         assert_matches(got, O.brute(od, oq, O.KNN, ks=np.full(40, k), dead_rows=dead_rows))
+
+
+@pytest.mark.parametrize("metric", [P.EDIT, P.L2])
+def test_knn_verified_stats_semantics(metric):
+    """kNN `verified` counts are the device pass's own: the
+    live entries that pass lemma 1 under the query's radius as it shrinks
+    during the pass, not the reference's count under its witness-pool bound
+    (search.py:540-570), which depends on the reference's visiting order.
+    What holds for both: every answer was verified, the count never exceeds
+    the live collection, and pruning off verifies every live entry."""
+    tree, ds, payloads, od = make_index(600, metric=metric, nc=5, seed=4)
+    q = [payloads[i] for i in range(0, 600, 37)]
+    eng = P.BatchSearcher(tree)
+    ans, st = eng.knn_batch(q, 7)
+    assert np.all(st.verified >= np.array([a[0].size for a in ans]))
+    assert np.all(st.verified <= 600)
+    _, st_off = P.BatchSearcher(tree, pruning=False).knn_batch(q, 7)
+    assert np.all(st_off.verified == 600)
+    # and the range stats stay the reference's (edit: equal; floats: >=)
+    ref = O.search(O.build(od, 5, 4), od, oq_of(metric, q), O.RANGE, radii=np.full(len(q), 3.0 if metric == P.EDIT else 0.2))
+    _, sr = eng.range_batch(q, 3.0 if metric == P.EDIT else 0.2)
+    if metric == P.EDIT:
+        assert np.array_equal(sr.verified, ref.verified)
+    else:
+        assert np.all(sr.verified >= ref.verified)
