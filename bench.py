@@ -189,9 +189,13 @@ def bench_config(args, w, world):
 class ClockSampler:
     """SM clocks + throttle reasons sampled DURING the timed region.
 
-    In-process NVML (pynvml) polled from a thread: NVML is initialised when the
-    sampler is created (before warm-up), so no nvidia-smi start-up (driver init,
-    seconds-long lock hold) ever lands inside a timed step."""
+    In-process NVML (pynvml), initialised when the sampler is created (before
+    warm-up), so no nvidia-smi start-up lands inside a timed step.  Default
+    mode "between": one synchronous sample after each timed step's final
+    sync (tick()), outside that step's device interval -- an NVML call
+    concurrent with a step measured 5-20 ms and stretched steps that
+    synchronise with the host several times (words: 99-171 ms steps against
+    84 ms of kernels).  GTS_CLOCK_MODE=full keeps the polling thread."""
 
     REASONS = (("hw_slowdown", 0x8), ("sw_thermal_slowdown", 0x20), ("hw_thermal_slowdown", 0x40),
                ("sw_power_cap", 0x4), ("hw_power_brake_slowdown", 0x80))
@@ -204,7 +208,7 @@ class ClockSampler:
         self.quit = threading.Event()
         self.err = None
         self.call_ms = []
-        self.mode = os.environ.get("GTS_CLOCK_MODE", "full")   # full | clock | none | off (diagnostics)
+        self.mode = os.environ.get("GTS_CLOCK_MODE", "between")   # between | full | clock | none | off
         if self.mode == "off":
             self.nv, self.th = None, None
             self.err = "sampler off (GTS_CLOCK_MODE=off)"
@@ -221,8 +225,10 @@ class ClockSampler:
         except Exception as e:  # noqa: BLE001
             self.nv = None
             self.err = f"nvml unavailable: {e}"
-        self.th = threading.Thread(target=self._run, daemon=True)
-        self.th.start()
+        self.th = None
+        if self.mode != "between":
+            self.th = threading.Thread(target=self._run, daemon=True)
+            self.th.start()
 
     def _sample(self):
         t0 = time.perf_counter()
@@ -246,6 +252,14 @@ class ClockSampler:
         self.samples = []
         self.on.set()
 
+    def tick(self):
+        """One sample now (mode "between": called between timed steps)."""
+        if self.mode == "between" and self.nv is not None:
+            try:
+                self.samples.append(self._sample())
+            except Exception as e:  # noqa: BLE001
+                self.err = str(e)
+
     def stop(self):
         self.on.clear()
         # one sample right at the end so even a short timed region has one
@@ -258,7 +272,9 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [self.err or "no samples"], "samples": 0}
         reasons = sorted({nm for _, r in self.samples for nm, bit in self.REASONS if r & bit})
         return {"sm_mhz": statistics.median(s for s, _ in self.samples), "sm_max_mhz": self.smax,
-                "reasons": reasons, "samples": len(self.samples), "source": "nvml (in-process)",
+                "reasons": reasons, "samples": len(self.samples),
+                "source": "nvml (in-process, " + ("sampled after each timed step)" if self.mode == "between"
+                                                  else "polling thread)"),
                 "nvml_call_ms_max": max((a + b for a, b in self.call_ms), default=None)}
 
     def close(self):
@@ -488,11 +504,14 @@ def run_stream(args, rank, world, local_rank):
     launches0 = _lib.launch_count()
     rb0 = si.rebuild_count
     clocks.start()
-    t0 = time.perf_counter()
+    tot = 0.0
     for _ in range(args.steps):
+        t0 = time.perf_counter()
         step()
-    torch.cuda.synchronize()
-    ms = (time.perf_counter() - t0) * 1e3 / args.steps
+        torch.cuda.synchronize()
+        tot += time.perf_counter() - t0
+        clocks.tick()
+    ms = tot * 1e3 / args.steps
     clk = clocks.stop()
     clocks.close()
     gc.enable()
@@ -561,22 +580,26 @@ def run_ours(args, rank, world, local_rank):
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     t_wall = time.perf_counter()
-    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    ea = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    eb = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev0.record(stream)
-    evs[0].record(stream)
     for i in range(args.steps):
+        ea[i].record(stream)
         one_step()
-        evs[i + 1].record(stream)
-        evs[i + 1].synchronize()
+        eb[i].record(stream)
+        eb[i].synchronize()
+        clocks.tick()
     ev1.record(stream)
     torch.cuda.synchronize()
-    step_ms = [round(evs[i].elapsed_time(evs[i + 1]), 3) for i in range(args.steps)]
+    step_ms = [round(ea[i].elapsed_time(eb[i]), 3) for i in range(args.steps)]
     wall_ms = (time.perf_counter() - t_wall) * 1e3 / args.steps
     barrier()
     launches = _lib.launch_count() - launches0
     clk = clocks.stop()
     clocks.close()
-    ms = ev0.elapsed_time(ev1) / args.steps
+    # the K steps' device intervals (each from its first launch to its final
+    # sync); the clock samples between steps are outside them
+    ms = sum(ea[i].elapsed_time(eb[i]) for i in range(args.steps)) / args.steps
     if world > 1:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -600,7 +623,8 @@ def run_ours(args, rank, world, local_rank):
     nmodes = len(eng.modes)
     qps = nmodes * nq / (ms / 1e3)
     # the dominant leaf-verification kernel of this workload (whichever ran)
-    cands = ("k_leafgroup_edit", "k_leaf_edit") if eng.edit else ("k_leafgroup_mma2", "k_leafgroup_mma", "k_leafgroup_tile", "k_leafgroup_vec", "k_verify")
+    cands = ("k_leafgroup_edit", "k_leaf_edit") if eng.edit else ("k_leafgroup_mma3", "k_leafgroup_mma2", "k_leafgroup_mma", "k_leafgroup_tile", "k_leafgroup_vec",
+                                                                     "k_verify")
     kname = max(cands, key=lambda k: prof["kernels"].get(k, {"ms": 0.0})["ms"])
     kver = dict(prof["kernels"].get(kname, {"ms": 0.0, "count": 0}), name=kname)
     work = prof["work"]
@@ -693,17 +717,19 @@ def run_sharded(args, rank, world, local_rank):
     torch.cuda.synchronize()
     clocks.start()
     launches0 = _lib.launch_count()
-    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
-    evs[0].record(stream)
+    ea = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    eb = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     for i in range(args.steps):
+        ea[i].record(stream)
         one_step()
-        evs[i + 1].record(stream)
-        evs[i + 1].synchronize()
+        eb[i].record(stream)
+        eb[i].synchronize()
+        clocks.tick()
     torch.cuda.synchronize()
     launches = _lib.launch_count() - launches0
     clk = clocks.stop()
-    step_ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
-    t = torch.tensor([evs[0].elapsed_time(evs[-1]) / args.steps], device=dev)
+    step_ms = [ea[i].elapsed_time(eb[i]) for i in range(args.steps)]
+    t = torch.tensor([sum(step_ms) / args.steps], device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     dist.barrier()
@@ -903,7 +929,7 @@ def roofline(eng, prof, kver, step_ms_prof):
             "peak_source": "gts_bench_int_peak: best of LOP3-only / IMAD-only / mixed 16-chain loops on all SMs, "
                            "measured in this run (MEASURED_PEAKS.json has no integer peak)"})
     D = eng.w.get("dim", 2)
-    if kver["name"] in ("k_leafgroup_mma", "k_leafgroup_mma2"):
+    if kver["name"] in ("k_leafgroup_mma", "k_leafgroup_mma2", "k_leafgroup_mma3"):
         tf = peaks.get("bf16_tflops_sustained") or peaks.get("bf16_tflops") or 1590.0
         flops = work["pairs"] * 2 * D
         achieved = flops / t / 1e12 if t else None

@@ -127,7 +127,13 @@ struct DBuf {
     {
         release();
         s = st;
+        static const bool trace = std::getenv("GTS_TRACE_ALLOC") != nullptr;
+        const auto t0 = trace ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point{};
         if (cnt) CK(cudaMallocAsync((void **)&p, cnt * sizeof(T), st));
+        if (trace) {
+            const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+            if (ms > 0.5) fprintf(stderr, "[gts] slow cudaMallocAsync: %.2f ms for %zu bytes\n", ms, cnt * sizeof(T));
+        }
         n = cnt;
     }
     void release()
@@ -1009,6 +1015,158 @@ __global__ void __launch_bounds__(256) k_expand_grouped(IndexView ix, QueryView 
     }
 }
 
+// Register-tiled variant of k_expand_grouped (vectors, the default for
+// D >= 16): the item's <= 128 query vectors are staged in shared memory next
+// to the node's child pivots, and a thread computes a 2-row x CPG-child tile
+// (rows a and a + 64, children CPG g .. CPG g + CPG - 1 for child group
+// g = threadIdx / 64), so one float4 step issues 2 + CPG shared loads for
+// 2 CPG distances instead of 2 loads per distance.  Same per-float4
+// accumulation order as k_expand_grouped (identical child distances), same
+// keep tests (search.py:425-433, 467-471), pruned counts summed per row in
+// shared memory, one block-wide compaction per item.
+constexpr int kXtRows = 128;
+template <int MET, int CPG>
+__global__ void __launch_bounds__(256, 2) k_expand_tile(IndexView ix, QueryView qv, const Row *__restrict__ srows,
+                                                        const Item *__restrict__ items, int nitems, int own,
+                                                        int pruning, const float *__restrict__ r32, Row *out,
+                                                        unsigned long long *counter, unsigned long long *pruned_stat)
+{
+    extern __shared__ float4 xt_smem4[];
+    const int ps = ix.Dp + 4;   // 16-byte skew: consecutive rows on different banks
+    float *piv_s = reinterpret_cast<float *>(xt_smem4);
+    float *qs_s = piv_s + (size_t)4 * CPG * ps;
+    NodeRec *rec_s = reinterpret_cast<NodeRec *>(qs_s + (size_t)kXtRows * ps);
+    __shared__ int s_q[kXtRows];
+    __shared__ float s_dqp[kXtRows], s_r[kXtRows];
+    __shared__ unsigned s_pruned[kXtRows];
+    __shared__ int sh_warp[8];
+    __shared__ unsigned long long sh_base;
+    const int nc = ix.nc, d4 = ix.Dp >> 2;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int ra = tid & 63, g = tid >> 6;
+    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+        const Item item = items[it];
+        const int child0 = (item.leaf - 1) * nc + 2;   // Eq. 1
+        __syncthreads();   // the previous item's smem is no longer read
+        if (tid < 4 * CPG) {
+            NodeRec c{0.f, 0.f, 0, 0};
+            if (tid < nc) c = ix.node[child0 + tid];
+            rec_s[tid] = c;
+        }
+        if (tid < kXtRows) {
+            int q = -1;
+            float dqp = 0.f, r = 0.f;
+            if (tid < item.count) {
+                const Row pr = srows[item.start + tid];
+                q = pr.q;
+                dqp = pr.dqp;
+                r = r32[q];
+            }
+            s_q[tid] = q;
+            s_dqp[tid] = dqp;
+            s_r[tid] = r;
+            s_pruned[tid] = 0u;
+        }
+        __syncthreads();
+        for (int t = tid; t < 4 * CPG * d4; t += blockDim.x) {
+            const int j = t / d4, c = t - j * d4;
+            reinterpret_cast<float4 *>(piv_s + (size_t)j * ps)[c] =
+                j < nc ? __ldg(reinterpret_cast<const float4 *>(ix.vec32 + (size_t)rec_s[j].piv * ix.Dp) + c)
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        for (int t = tid; t < kXtRows * d4; t += blockDim.x) {
+            const int a = t / d4, c = t - a * d4;
+            const int q = s_q[a];
+            reinterpret_cast<float4 *>(qs_s + (size_t)a * ps)[c] =
+                q >= 0 ? __ldg(reinterpret_cast<const float4 *>(qv.vec32 + (size_t)q * ix.Dp) + c)
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        __syncthreads();
+        float acc[2][CPG];
+#pragma unroll
+        for (int u = 0; u < 2; u++)
+#pragma unroll
+            for (int k = 0; k < CPG; k++) acc[u][k] = 0.f;
+        const float4 *xa = reinterpret_cast<const float4 *>(qs_s + (size_t)ra * ps);
+        const float4 *xb = reinterpret_cast<const float4 *>(qs_s + (size_t)(ra + 64) * ps);
+        const float4 *py = reinterpret_cast<const float4 *>(piv_s + (size_t)g * CPG * ps);
+        for (int c = 0; c < d4; c++) {
+            const float4 x0 = xa[c], x1 = xb[c];
+#pragma unroll
+            for (int k = 0; k < CPG; k++) {
+                const float4 y = py[(size_t)k * (ps >> 2) + c];   // warp-uniform: broadcast
+                {
+                    const float d0 = y.x - x0.x, d1 = y.y - x0.y, d2 = y.z - x0.z, d3 = y.w - x0.w;
+                    if (MET == kMetricL1) acc[0][k] += (fabsf(d0) + fabsf(d1)) + (fabsf(d2) + fabsf(d3));
+                    else acc[0][k] += (d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3);
+                }
+                {
+                    const float d0 = y.x - x1.x, d1 = y.y - x1.y, d2 = y.z - x1.z, d3 = y.w - x1.w;
+                    if (MET == kMetricL1) acc[1][k] += (fabsf(d0) + fabsf(d1)) + (fabsf(d2) + fabsf(d3));
+                    else acc[1][k] += (d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3);
+                }
+            }
+        }
+        // keep tests, pruned counts, this thread's kept rows
+        uint32_t keepm = 0;   // bit u * CPG + k
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+            const int a = ra + 64 * u;
+            const int q = s_q[a];
+            if (q < 0) continue;
+            const float dqp = s_dqp[a], r = s_r[a];
+            unsigned pr = 0;
+#pragma unroll
+            for (int k = 0; k < CPG; k++) {
+                const int j = g * CPG + k;
+                if (j >= nc) continue;
+                const NodeRec c = rec_s[j];
+                if (c.size <= 0) continue;
+                bool keep = true;
+                if (!own && pruning) {
+                    const float e = slack(ix, dqp, r);
+                    keep = (dqp + r + e >= c.mn) && (dqp - r - e <= c.mx);
+                }
+                const float cd = MET == kMetricL1 ? acc[u][k] : sqrtf(acc[u][k]);
+                acc[u][k] = cd;
+                if (keep && own && pruning) {
+                    const float e = slack(ix, cd, r);
+                    keep = (cd + r + e >= c.mn) && (cd - r - e <= c.mx);
+                }
+                if (keep) keepm |= 1u << (u * CPG + k);
+                else pr++;
+            }
+            if (pr) atomicAdd(&s_pruned[a], pr);
+        }
+        // block-wide compaction: warp scan of the per-thread counts
+        const unsigned nk = __popc(keepm);
+        unsigned incl = nk;
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned v = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += v;
+        }
+        if (lane == 31) sh_warp[warp] = (int)incl;
+        __syncthreads();
+        if (tid == 0) {
+            int tot = 0;
+            for (int w = 0; w < 8; w++) { const int c = sh_warp[w]; sh_warp[w] = tot; tot += c; }
+            sh_base = tot ? atomicAdd(counter, (unsigned long long)tot) : 0ull;
+        }
+        __syncthreads();
+        unsigned long long slot = sh_base + (unsigned long long)sh_warp[warp] + (incl - nk);
+#pragma unroll
+        for (int u = 0; u < 2; u++)
+#pragma unroll
+            for (int k = 0; k < CPG; k++)
+                if ((keepm >> (u * CPG + k)) & 1u) {
+                    const int a = ra + 64 * u;
+                    out[slot++] = Row{s_q[a], child0 + g * CPG + k, acc[u][k], 0};
+                }
+        if (tid < kXtRows && s_pruned[tid] && s_q[tid] >= 0)
+            atomicAdd(pruned_stat + s_q[tid], (unsigned long long)s_pruned[tid]);
+    }
+}
+
 __device__ __forceinline__ void fhist_add(unsigned *hist, const float *r0, int q, double d);
 __device__ __forceinline__ void fhist_shrink(unsigned *hist, const float *r0, const int32_t *ks, float *r32,
                                              double *r64, int q);
@@ -1220,14 +1378,14 @@ __global__ void __launch_bounds__(256, 4) k_leafgroup_tile(IndexView ix, QueryVi
             for (int a = 0; a < 4; a++) {
                 const int row = lane + 32 * a;
                 const int q = s_q[row];
-                if (q < 0) continue;
                 const float r = s_r[row];
                 const float2 rg = make_float2(s_lo[row], s_hi[row]);
                 bool any_ub = false;
+                uint32_t cmask = 0;   // candidates of this row among the 4 entries
 #pragma unroll
                 for (int b = 0; b < 4; b++) {
                     const int j = e0 + b;
-                    if (j >= size) continue;
+                    if (q < 0 || j >= size) continue;
                     const float dis = s_dis[j];
                     if (!(dis == dis)) continue;   // tombstoned
                     if (pruning && !lemma1_in(dis, rg)) continue;
@@ -1236,17 +1394,36 @@ __global__ void __launch_bounds__(256, 4) k_leafgroup_tile(IndexView ix, QueryVi
                     const float sl = slack(ix, d, 0.f);
                     if (!(d - sl <= r)) continue;
                     // candidate: exact float64 check later (k_recheck) against the final radius
-                    const unsigned long long o = atomicAdd(cb.counter, 1ull);
-                    if (o < cb.cap) {
-                        const float lb = fmaxf(d - sl, 0.f) * (1.f - 1e-6f);
-                        cb.q[o] = q;
-                        cb.e[o] = pos + j;
-                        cb.lb[o] = MET == kMetricL2 ? lb * lb : lb;
-                    }
+                    cmask |= 1u << b;
                     if (fhist && d + sl <= r) {
                         // the true distance is <= d + slack: a valid upper bound for the shrink
                         fhist_add(fhist, r0, q, (double)(d + sl) * (1.0 + 1e-6));
                         any_ub = true;
+                    }
+                }
+                // warp-aggregated append (one atomic per warp instead of per candidate)
+                if (__any_sync(kFull, cmask)) {
+                    const unsigned nc = __popc(cmask);
+                    unsigned incl = nc;
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const unsigned v = __shfl_up_sync(kFull, incl, o);
+                        if (lane >= o) incl += v;
+                    }
+                    const unsigned wtot = __shfl_sync(kFull, incl, 31);
+                    unsigned long long base = 0;
+                    if (lane == 31) base = atomicAdd(cb.counter, (unsigned long long)wtot);
+                    base = __shfl_sync(kFull, base, 31) + (incl - nc);
+#pragma unroll
+                    for (int b = 0; b < 4; b++) {
+                        if (!((cmask >> b) & 1u)) continue;
+                        if (base < cb.cap) {
+                            const float d = MET == kMetricL1 ? acc[a][b] : sqrtf(acc[a][b]);
+                            const float lb = fmaxf(d - slack(ix, d, 0.f), 0.f) * (1.f - 1e-6f);
+                            cb.q[base] = q;
+                            cb.e[base] = pos + e0 + b;
+                            cb.lb[base] = MET == kMetricL2 ? lb * lb : lb;
+                        }
+                        base++;
                     }
                 }
                 if (any_ub) {
@@ -1963,6 +2140,321 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
     __syncthreads();
     tc::fence_after_sync();
     if (warp == 0) tc::tmem_dealloc(tmem, NSTAGE * acc_cols);
+}
+
+// ---------------------------------------------------------------------------
+// k_leafgroup_mma3: the tensor-core L2 screen as a barrier-free pipeline
+// (the default; k_leafgroup_mma2 with GTS_MMA_V2=1).  Same algorithm and
+// error band as k_leafgroup_mma2; what changes is the synchronisation:
+//  * no block barrier per item.  Stage s (A/B operands) is filled by
+//    cp.async from every thread and completes an mbarrier (full[s], 512
+//    noinc arrivals); one thread waits it and issues the MMA, whose commit
+//    completes mma_done[s]; each warp waits mma_done[s] before reading the
+//    accumulator, and after its last TMEM read arrives on acc_free[s]
+//    (16 arrivals), which the MMA issuer waits before reusing accumulator s.
+//    Warps drift up to one item apart instead of meeting at a barrier.
+//  * no shared-memory metadata rings: a thread owns one accumulator row
+//    (TMEM lane) and one quarter of the columns, loads its row's {q, dqp,
+//    r, |q|, r0} into registers one item ahead and copies its quarter of the
+//    row's bf16 query vector; the per-entry column terms {dis | NaN,
+//    y - z | NaN, y + z, dis} come precomputed (k_colrec, per call) from
+//    global memory as warp-uniform (broadcast) loads.
+// ---------------------------------------------------------------------------
+constexpr int kM3Threads = 512;   // 16 warps: 4 per TMEM lane quadrant
+
+// per-entry column terms of the screen (see k_leafgroup_mma2's meta_store)
+__global__ void k_colrec(IndexView ix, int64_t n, float4 *colrec)
+{
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n + 16) return;
+    const float nan = __int_as_float(0x7fc00000);
+    float4 col = make_float4(nan, nan, 0.f, INFINITY);
+    if (e < n) {
+        const float dis = ix.dis[e], se = ix.vse[e];
+        const float y = fmaf(dis, dis, 2.f * se), z = 8.f * ix.rel * dis * dis;
+        if (is_alive(ix.alive, (int)e)) {
+            col.x = dis;
+            col.y = y - z;
+        }
+        col.z = y + z;
+        col.w = dis;
+    }
+    colrec[e] = col;
+}
+
+__global__ void __launch_bounds__(kM3Threads, 1)
+k_leafgroup_mma3(IndexView ix, QueryView qv, const Row *__restrict__ srows, const Item *__restrict__ items, int nitems,
+                 const float4 *__restrict__ colrec, float *r32, double *r64, CandBuf cb,
+                 unsigned long long *verified_stat, int stats_on, unsigned long long *work, uint32_t acc_cols,
+                 int nmax, unsigned *fhist, const float *r0, const int32_t *ks)
+{
+    extern __shared__ __align__(1024) uint8_t smraw[];
+    __shared__ uint64_t full[2], mma_done[2], acc_free[2];
+    __shared__ float4 s_col[4][256];   // column terms, ring by item % 4 (see below)
+    __shared__ uint32_t tmem_slot;
+    const uint32_t pad = (1024u - (tc::smem_u32(smraw) & 1023u)) & 1023u;
+    uint8_t *sm = smraw + pad;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int qd = warp & 3, part = warp >> 2;
+    const int row = 32 * qd + lane;                  // this thread's accumulator row (TMEM lane)
+    const int nkb = ix.Dk >> 6;
+    const int c16 = ix.Dk >> 3;                      // 16-byte chunks per bf16 row
+    const int lc = c16 == 16 ? 4 : 3;
+    const size_t a_bytes = (size_t)nkb * 16384;
+    const size_t stage_bytes = a_bytes + (size_t)nkb * nmax * 128;
+    const int G = gridDim.x;
+    auto idx = [&](int i) { return (int)blockIdx.x + i * G; };
+    if (warp == 0) tc::tmem_alloc(&tmem_slot, 2 * acc_cols);
+    if (tid == 0) {
+        for (int k = 0; k < 2; k++) {
+            tc::mbar_init(&full[k], kM3Threads);
+            tc::mbar_init(&mma_done[k], 1);
+            tc::mbar_init(&acc_free[k], kM3Threads / 32);
+        }
+        tc::fence_mbar_init();
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tmem = tmem_slot;
+
+    struct It {
+        int start, count, size, pos;
+    };
+    auto item_of = [&](int i) {
+        It t{0, 0, 0, 0};
+        if (idx(i) < nitems) {
+            const Item x = items[idx(i)];
+            t = It{x.start, x.count, x.size, x.pos};
+        }
+        return t;
+    };
+    struct RowMeta {
+        int q;
+        float dqp, r, qn, r0;
+    };
+    auto row_meta = [&](const It &t) {
+        RowMeta m{-1, 0.f, -1.f, 0.f, 0.f};
+        if (row < t.count) {
+            const Row lr = srows[t.start + row];
+            m.q = lr.q;
+            m.dqp = lr.dqp;
+            m.r = __ldcg(r32 + lr.q);
+            m.qn = qv.qn[lr.q];
+            m.r0 = r0 ? r0[lr.q] : 0.f;
+        }
+        return m;
+    };
+    // operands of item i into stage i & 1, then this thread's noinc arrival
+    // on full[i & 1] (fires when its copies have landed)
+    auto stage = [&](int i, const It &t, int q) {
+        const int st = i & 1;
+        const int N = max(16, (t.size + 15) & ~15);
+        const uint32_t A = tc::smem_u32(sm + st * stage_bytes);
+        const uint32_t B = A + (uint32_t)a_bytes;
+        // A: this row's query vector, quarter `part` of its chunks
+        const int per = c16 >> 2;
+        const uint4 *qsrc = qv.qbf + (size_t)max(q, 0) * c16;
+#pragma unroll 4
+        for (int k = 0; k < per; k++) {
+            const int c = part * per + k;
+            tc::cp_async16(A + (uint32_t)(c >> 3) * 16384u + tc::sw128_offset(row, c & 7), qsrc + c,
+                           q >= 0 ? 16u : 0u);
+        }
+        // column terms of the item into ring slot i % 4: a warp issuing the
+        // copies of item i+2 has passed mma_done(i), and MMA i was issued after
+        // acc_free(i-2), so no warp still reads slot (i-2) % 4 = (i+2) % 4;
+        // slots i-1 .. i+1 may be in use
+        if (tid < N) tc::cp_async16(tc::smem_u32(&s_col[i & 3][tid]), colrec + t.pos + tid, 16u);
+        // B: the leaf's centred entries, N rows (rows >= size zero-filled;
+        // their source stays inside vcent's 16-row zero tail)
+        const int total = N * c16;
+        for (int f = tid; f < total; f += kM3Threads) {
+            const int r = f >> lc, c = f & (c16 - 1);
+            tc::cp_async16(B + (uint32_t)(c >> 3) * (uint32_t)N * 128u + tc::sw128_offset(r, c & 7),
+                           ix.vcent + (size_t)(t.pos + r) * c16 + c, r < t.size ? 16u : 0u);
+        }
+        tc::cp_async_mbar_arrive(&full[st]);
+    };
+    auto mma = [&](int i, const It &t) {
+        const int st = i & 1;
+        const int N = max(16, (t.size + 15) & ~15);
+        const uint32_t idesc = tc::idesc_bf16(128, N);
+        const uint32_t a0 = tc::smem_u32(sm + st * stage_bytes), b0 = a0 + (uint32_t)a_bytes;
+        for (int kb = 0; kb < nkb; kb++) {
+#pragma unroll
+            for (int k4 = 0; k4 < 4; k4++) {
+                const uint64_t ad = tc::desc_k_sw128(a0 + kb * 16384 + k4 * 32);
+                const uint64_t bd = tc::desc_k_sw128(b0 + kb * N * 128 + k4 * 32);
+                tc::mma_bf16(tmem + st * acc_cols, ad, bd, idesc, (kb | k4) ? 1u : 0u);
+            }
+        }
+        tc::mma_commit(&mma_done[st]);
+    };
+
+    unsigned long long pairs = 0, w_entries = 0, w_rows = 0, w_macs = 0;
+    // row metadata runs two items ahead, so the query id a copy needs is in
+    // a register when the copy is issued
+    It cur = item_of(0), nxt = item_of(1);
+    RowMeta mc = row_meta(cur), mn = row_meta(nxt);
+    if (idx(0) < nitems) {
+        stage(0, cur, mc.q);
+        if (tid == 0) {
+            tc::mbar_wait(&full[0], 0u);
+            tc::fence_async_smem();
+            tc::fence_after_sync();
+            mma(0, cur);
+        }
+    }
+    for (int i = 0; idx(i) < nitems; i++) {
+        const int s = i & 1;
+        const uint32_t ph = (uint32_t)(i >> 1) & 1u;
+        const It n2 = item_of(i + 2);
+        const RowMeta m2 = row_meta(n2);
+        // operands of item i+1 into the other stage (MMA i-1, its last reader,
+        // completed before this thread's epilogue of item i-1)
+        if (idx(i + 1) < nitems) stage(i + 1, nxt, mn.q);
+        tc::mbar_wait(&mma_done[s], ph);
+        tc::mbar_wait(&full[s], ph);   // (complete already) acquire: the column terms landed
+        tc::fence_after_sync();
+        // ---- epilogue of item i: row `row`, columns 16 * part + 64 k ----
+        {
+            const int size = cur.size;
+            const int N = max(16, (size + 15) & ~15);
+            const int q = mc.q;
+            const bool valid = q >= 0;
+            const float dqp = mc.dqp, qnorm = mc.qn;
+            float r = mc.r;
+            const float dq2 = dqp * dqp;
+            const float cA = ((dqp + qnorm) * 0x1p-7f) + ((qnorm) * 0x1p-18f) + 4.f * ix.abs_eps;
+            const float kq = 8.f * ix.rel * dq2 + 4.f * ix.abs_eps * (dqp + ix.abs_eps);
+            float T1, T2;
+            auto set_r = [&](float rr) {
+                const float R2 = rr * rr * (1.f + 1e-6f);
+                const float mg = ((dq2 + qnorm * qnorm + R2) * 0x1p-18f);
+                T1 = R2 + kq - dq2 + mg;
+                T2 = R2 - kq - dq2 - mg;
+            };
+            set_r(r);
+            const float2 rg = lemma1_range(ix, dqp, r);
+            float hinv = 0.f;
+            if (fhist && valid) {
+                const float R0 = mc.r0;
+                hinv = (R0 > 0.f && !isinf(R0)) ? (float)kFHist / R0 : 0.f;
+            }
+            unsigned ver = 0;
+            const uint32_t lane_base = tmem + s * acc_cols + ((uint32_t)(qd * 32) << 16);
+            const float4 *cols = s_col[i & 3];
+            for (int c0 = 16 * part; c0 < N; c0 += 64) {
+                uint32_t ar[16];
+                tc::tmem_ld16_issue(lane_base + (uint32_t)c0, ar);
+                const int nv = size - c0;   // valid columns of this chunk
+                const uint32_t vm = nv >= 16 ? 0xffffu : (nv > 0 ? (1u << nv) - 1u : 0u);
+                float4 col[16];
+#pragma unroll
+                for (int jj = 0; jj < 16; jj++) col[jj] = cols[c0 + jj];   // broadcast LDS.128
+                tc::tmem_wait_ld();
+                tc::tmem_tie(ar);
+                uint32_t win = 0, cm = 0;
+#pragma unroll
+                for (int jj = 0; jj < 16; jj++) {
+                    const float m2a = fmaf(-2.f, __uint_as_float(ar[jj]), col[jj].y);
+                    win |= (uint32_t)lemma1_in(col[jj].x, rg) << jj;
+                    cm |= (uint32_t)(fmaf(-cA, col[jj].w, m2a) <= T1) << jj;
+                }
+                win &= vm;
+                ver += __popc(win);
+                uint32_t fm = 0;
+                if (hinv > 0.f && (cm & win)) {
+#pragma unroll
+                    for (int jj = 0; jj < 16; jj++)
+                        fm |= (uint32_t)(fmaf(cA, col[jj].w, fmaf(-2.f, __uint_as_float(ar[jj]), col[jj].z)) <= T2)
+                              << jj;
+                }
+                cm &= win;
+                fm &= cm;
+                if (!valid) cm = fm = 0, ver = 0;
+                if (__any_sync(kFull, cm)) {
+                    const unsigned nc = __popc(cm);
+                    unsigned incl = nc;
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const unsigned v = __shfl_up_sync(kFull, incl, o);
+                        if (lane >= o) incl += v;
+                    }
+                    const unsigned wtot = __shfl_sync(kFull, incl, 31);
+                    unsigned long long base = 0;
+                    if (lane == 31) base = atomicAdd(cb.counter, (unsigned long long)wtot);
+                    base = __shfl_sync(kFull, base, 31) + (incl - nc);
+#pragma unroll
+                    for (int jj = 0; jj < 16; jj++) {
+                        if (!((cm >> jj) & 1u)) continue;
+                        if (base < cb.cap) {
+                            cb.q[base] = q;
+                            cb.e[base] = cur.pos + c0 + jj;
+                            cb.lb[base] = (fmaf(-cA, col[jj].w, fmaf(-2.f, __uint_as_float(ar[jj]), col[jj].y)) + dq2 -
+                                           kq) * (1.f - 1e-5f) -
+                                          ((dq2 + qnorm * qnorm) * 0x1p-18f);
+                        }
+                        base++;
+                    }
+                }
+                if (fm && hinv > 0.f) {
+#pragma unroll
+                    for (int jj = 0; jj < 16; jj++) {
+                        if (!((fm >> jj) & 1u)) continue;
+                        const float d2u = fmaf(cA, col[jj].w, fmaf(-2.f, __uint_as_float(ar[jj]), col[jj].z)) + dq2 +
+                                          kq + ((dq2 + qnorm * qnorm) * 0x1p-18f);
+                        const float dub = sqrtf(fmaxf(d2u, 0.f)) * (1.f + 1e-6f) + 1e-30f;
+                        const int b = min((int)(dub * hinv * (1.f + 1e-6f)), kFHist - 1);
+                        atomicAdd(fhist + (size_t)q * kFHist + b, 1u);
+                    }
+                    __threadfence();
+                    fhist_shrink(fhist, r0, ks, r32, r64, q);
+                    r = __ldcg(r32 + q);
+                    set_r(r);
+                }
+            }
+            if (valid && stats_on && ver) atomicAdd(verified_stat + q, (unsigned long long)ver);
+            pairs += ver;
+            if (tid == 0) {
+                w_entries += (unsigned long long)size * cur.count;
+                w_rows += (unsigned long long)cur.count;
+                w_macs += (unsigned long long)128 * N * ix.Dk;
+            }
+        }
+        // accumulator s read by this warp
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&acc_free[s]);
+        // MMA of item i+1 into accumulator s^1: its operands landed (full) and
+        // every warp finished item i-1, the accumulator's previous user
+        if (tid == 0 && idx(i + 1) < nitems) {
+            tc::mbar_wait(&full[s ^ 1], (uint32_t)((i + 1) >> 1) & 1u);
+            if (i >= 1) tc::mbar_wait(&acc_free[s ^ 1], (uint32_t)((i - 1) >> 1) & 1u);
+            tc::fence_async_smem();
+            tc::fence_after_sync();
+            mma(i + 1, nxt);
+        }
+        __syncwarp();
+        cur = nxt;
+        mc = mn;
+        nxt = n2;
+        mn = m2;
+    }
+    if (work) {
+        for (int o = 16; o > 0; o >>= 1) pairs += __shfl_down_sync(kFull, pairs, o);
+        if (lane == 0) atomicAdd(work + kWorkPairs, pairs);
+        if (tid == 0) {
+            atomicAdd(work + kWorkEntries, w_entries);
+            atomicAdd(work + kWorkRows, w_rows);
+            atomicAdd(work + kWorkSteps, w_macs);
+        }
+    }
+    // every MMA was waited (mma_done) before its epilogue; all TMEM reads done
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    if (warp == 0) tc::tmem_dealloc(tmem, 2 * acc_cols);
 }
 
 // Exact float64 recheck of screened candidates against the final radius
@@ -2844,6 +3336,7 @@ struct gts_index {
     // (k_root_radius) and of the pending cache (host, float64), and the root
     // pivot's payload for the latter
     float root_radius = INFINITY, cache_radius = 0.f;
+    std::atomic<int64_t> hbm_rows_cached{0};   // device default frontier-table rows (hbm_rows)
     double avg_text_bytes = 0.0;   // strings: mean stored bytes per entry (traversal byte counts)
     // leaf slack (in-place inserts): device slot layout and
     // host mirrors of what the insert path changes
@@ -2979,6 +3472,45 @@ unsigned long long *pinned_counters()
     static thread_local unsigned long long *p = nullptr;
     if (!p) CK(cudaMallocHost((void **)&p, 4 * sizeof(unsigned long long)));
     return p;
+}
+
+// Per-thread pinned staging for the small per-call host->device copies
+// (radii, k, initial bounds).  A cudaMemcpyAsync from pageable memory first
+// synchronises the stream, which serialised the host with the previous
+// call's device work; from pinned memory it is truly asynchronous.  The
+// arena is rewound at every search call: the previous call's copies have
+// completed by then (every call ends with a stream synchronisation).
+struct PinnedArena {
+    char *p = nullptr;
+    size_t cap = 0, off = 0;
+    template <class T>
+    const T *stage(const T *src, size_t cnt)
+    {
+        const size_t bytes = ((cnt * sizeof(T)) + 255) & ~(size_t)255;
+        if (off + bytes > cap) {
+            // grow (only between calls in practice; earlier stagings of this call stay valid
+            // because the old block is released only after the stream drains)
+            size_t ncap = std::max<size_t>(cap * 2, off + bytes + (1 << 20));
+            char *np = nullptr;
+            CK(cudaMallocHost((void **)&np, ncap));
+            if (p) {
+                CK(cudaDeviceSynchronize());
+                std::memcpy(np, p, off);
+                cudaFreeHost(p);
+            }
+            p = np;
+            cap = ncap;
+        }
+        T *dst = reinterpret_cast<T *>(p + off);
+        std::memcpy(dst, src, cnt * sizeof(T));
+        off += bytes;
+        return dst;
+    }
+};
+static PinnedArena &pinned_arena()
+{
+    static thread_local PinnedArena a;
+    return a;
 }
 
 // The per-call search driver.
@@ -3187,6 +3719,10 @@ struct Search {
     // candidate pairs (k_recheck)
     void launch_mma2(const Row *srows, const Item *items, int nitems, int stats_on)
     {
+        if (std::getenv("GTS_MMA_V2") == nullptr) {
+            launch_mma3(srows, items, nitems, stats_on);
+            return;
+        }
         // default: one 512-thread CTA per SM, two stages (343 ms per vec128
         // step); GTS_MMA_SHAPE=256 runs two 256-thread one-stage CTAs per SM
         // (measured 443 ms: the shorter epilogues do not cover the exposed
@@ -3194,6 +3730,33 @@ struct Search {
         static const bool two_cta = std::getenv("GTS_MMA_SHAPE") && std::atoi(std::getenv("GTS_MMA_SHAPE")) == 256;
         if (two_cta) launch_mma2_shape<256, 1>(srows, items, nitems, stats_on, 2);
         else launch_mma2_shape<512, 2>(srows, items, nitems, stats_on, 1);
+    }
+
+    // barrier-free pipelined tensor-core screen (k_leafgroup_mma3)
+    void launch_mma3(const Row *srows, const Item *items, int nitems, int stats_on)
+    {
+        const int nmax = std::max(16, (ix->max_leaf + 15) & ~15);
+        uint32_t cols = 32;
+        while ((int)cols < nmax) cols <<= 1;
+        const size_t nkb = (size_t)ix->Dk / 64;
+        const size_t smb = 2 * (nkb * 16384 + nkb * (size_t)nmax * 128) + 1024;
+        smem_optin((const void *)k_leafgroup_mma3, smb);
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
+        const unsigned grid = (unsigned)std::min<int>(nitems, sms);
+        // column terms of every slot (+16 padding records past the end)
+        DBuf<float4> colrec((size_t)ix->n + 16, st);
+        k_colrec<<<grid_for(ix->n + 16, 256), 256, 0, st>>>(iv, ix->n, colrec.p);
+        LAUNCH_CHECK();
+        with_candidates<kMetricL2>([&](const CandBuf &cb, int first) {
+            timed("k_leafgroup_mma3", [&] {
+                const int on = first && stats_on;
+                k_leafgroup_mma3<<<grid, kM3Threads, smb, st>>>(iv, qv, srows, items, nitems, colrec.p, r32.p, r64.p,
+                                                               cb, verified.p, on, on ? work.p : nullptr, cols, nmax,
+                                                               on ? fhist.p : nullptr, r0.p, ks.p);
+            });
+            LAUNCH_CHECK();
+        });
     }
 
     template <int NT, int NSTAGE>
@@ -3449,6 +4012,25 @@ struct Search {
             group_rows(in, m, G, kItemQueries, first, (int)c);
             CK(cudaMemsetAsync(counter.p, 0, sizeof(unsigned long long), st));
             if (G.nitems == 0) return 0;
+            if (ix->nc <= 32 && ix->Dp <= 128 && std::getenv("GTS_EXPAND_NOTILE") == nullptr) {
+                const int need = (ix->nc + 3) / 4;
+                const int cpg = need <= 2 ? 2 : (need <= 5 ? 5 : 8);   // the kernel's CPG (smem sized for it)
+                const size_t smt = ((size_t)4 * cpg * (ix->Dp + 4) + (size_t)kXtRows * (ix->Dp + 4)) * sizeof(float) +
+                                   (size_t)4 * cpg * sizeof(NodeRec);
+                const unsigned gt = (unsigned)std::min<int>(G.nitems, 148 * 2);
+                auto go = [&](auto kern) {
+                    smem_optin((const void *)kern, smt);
+                    timed("k_expand", [&] {
+                        kern<<<gt, 256, smt, st>>>(iv, qv, G.srows.p, G.items.p, G.nitems, own, pruning, r32.p, out,
+                                                   counter.p, pruned.p);
+                    });
+                };
+                if (cpg == 2) go(k_expand_tile<MET, 2>);
+                else if (cpg == 5) go(k_expand_tile<MET, 5>);
+                else go(k_expand_tile<MET, 8>);
+                LAUNCH_CHECK();
+                return (int64_t)read_counter(0);
+            }
             const size_t smb = (size_t)ix->nc * (ix->Dp + 4) * sizeof(float) + (size_t)ix->nc * sizeof(NodeRec);
             smem_optin((const void *)k_expand_grouped<MET>, smb);
             const unsigned grid = (unsigned)std::min<int>(G.nitems, 148 * 8);
@@ -3903,7 +4485,7 @@ static double now_ms()
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
-int64_t hbm_rows(const gts_index *ix)
+int64_t hbm_rows_query(const gts_index *ix)
 {
     static const char *env = std::getenv("GTS_DEFAULT_ROWS");
     if (env) return std::max<int64_t>(std::atoll(env), ix->nc);
@@ -3918,6 +4500,19 @@ int64_t hbm_rows(const gts_index *ix)
     // at 2^26 for the same DP work (larger leaf launches run superlinearly
     // slower), and vec128 551 vs 614 ms per step (allocation gaps)
     return std::max<int64_t>(std::min<int64_t>(rows, 1ll << 24), std::max<int64_t>(ix->nc, 1ll << 16));
+}
+
+// cudaMemGetInfo asks the resource manager and measured 50-80 ms when it
+// coincided with other driver activity (words bench, B200): query free HBM
+// once per index and reuse it
+int64_t hbm_rows(gts_index *ix)
+{
+    int64_t v = ix->hbm_rows_cached.load();
+    if (v <= 0) {
+        v = hbm_rows_query(ix);
+        ix->hbm_rows_cached.store(v);
+    }
+    return v;
 }
 
 gts_result *run_search(gts_index *ix, const gts_queries *q, int mode, const double *radii, const int64_t *ks,
@@ -3936,6 +4531,8 @@ gts_result *run_search(gts_index *ix, const gts_queries *q, int mode, const doub
     const int64_t cap = memory_units > 0 ? memory_units : hbm_rows(ix);
     if (ix->n > 0 && cap < ix->nc) fail(GTS_EBUDGET, "memory_units %lld below fan-out %d", (long long)cap, ix->nc);
     const int64_t nq = q->nq;
+    PinnedArena &pa = pinned_arena();
+    pa.off = 0;
     Search s(ix, q, st, mode, cap, pruning);
     s.max_qlen = q->max_len;
     s.r32.alloc((size_t)std::max<int64_t>(nq, 1), st);
@@ -3951,8 +4548,8 @@ gts_result *run_search(gts_index *ix, const gts_queries *q, int mode, const doub
                 h32[(size_t)i] = round_up_f32(radii[i]);
             }
         }
-        h2d(s.r32.p, h32.data(), (size_t)nq, st);
-        h2d(s.r64.p, radii, (size_t)nq, st);
+        h2d(s.r32.p, pa.stage(h32.data(), (size_t)nq), (size_t)nq, st);
+        h2d(s.r64.p, pa.stage(radii, (size_t)nq), (size_t)nq, st);
     } else {
         std::vector<int32_t> hk((size_t)nq);
         for (int64_t i = 0; i < nq; i++) {
@@ -3960,12 +4557,12 @@ gts_result *run_search(gts_index *ix, const gts_queries *q, int mode, const doub
             hk[(size_t)i] = (int32_t)std::min<int64_t>(ks[i], (1ll << 31) - 1);
         }
         s.ks.alloc((size_t)std::max<int64_t>(nq, 1), st);
-        h2d(s.ks.p, hk.data(), (size_t)nq, st);
+        h2d(s.ks.p, pa.stage(hk.data(), (size_t)nq), (size_t)nq, st);
         // +inf until the probe (if any) estimates a radius
         std::vector<float> inf32((size_t)nq, INFINITY);
         std::vector<double> inf64((size_t)nq, INFINITY);
-        h2d(s.r32.p, inf32.data(), (size_t)nq, st);
-        h2d(s.r64.p, inf64.data(), (size_t)nq, st);
+        h2d(s.r32.p, pa.stage(inf32.data(), (size_t)nq), (size_t)nq, st);
+        h2d(s.r64.p, pa.stage(inf64.data(), (size_t)nq), (size_t)nq, st);
     }
     const double t1 = trace ? now_ms() : 0.0;
     s.use_cache = use_cache;

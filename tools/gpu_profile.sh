@@ -15,3 +15,4 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -
     -o gpurun_out/prof_${W}_${TAG} -f \
     python bench.py --workload $W --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_${W}_${TAG}.log 2>&1
 echo "ncu_${W}=$?" >> gpurun_out/status_${TAG}.txt
+tools/ncu_shrink.sh gpurun_out/prof_${W}_${TAG}.ncu-rep

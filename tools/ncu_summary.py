@@ -67,8 +67,17 @@ def launch_table(path):
     return "\n".join(lines)
 
 
+def raw_csv(path):
+    """The raw metrics page of a capture: the .ncu-rep, or its shrunk
+    <name>.raw.csv.gz (tools/ncu_shrink.sh)."""
+    if path.endswith(".raw.csv.gz"):
+        import gzip
+        return gzip.open(path, "rt").read()
+    return subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+
+
 def full_capture(path):
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    raw = raw_csv(path)
     r = list(csv.reader(io.StringIO(raw)))
     h, v = r[0], r[2] if len(r) > 2 else r[1]
     units = r[1] if len(r) > 2 else [""] * len(h)
@@ -88,7 +97,7 @@ def full_capture(path):
 
 def capture_traffic(path):
     """(kernel short name, dram read + write bytes) of a --set full capture."""
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    raw = raw_csv(path)
     r = list(csv.reader(io.StringIO(raw)))
     h, v = r[0], r[2] if len(r) > 2 else r[1]
     units = r[1] if len(r) > 2 else [""] * len(h)
@@ -120,7 +129,7 @@ def main():
         parts += ["## launch list (ncu --metrics gpu__time_duration.sum --clock-control none; cold, serialised;"
                   " shares are what to compare)", "", launch_table(lp), ""]
     for rep in sorted(glob.glob(os.path.join(OUT, f"prof_*{a.workload}*_{a.tag}.ncu-rep"))
-                    + sorted(glob.glob(os.path.join(OUT, f"prof_leaf_{a.tag}.ncu-rep")))):
+                    + sorted(glob.glob(os.path.join(OUT, f"prof_*{a.workload}*_{a.tag}.raw.csv.gz")))):
         parts += [f"## full capture `{os.path.basename(rep)}` (ncu --set full --clock-control none)", "",
                   full_capture(rep), ""]
         # roofline.traffic source for bench.py: DRAM bytes per launch of the captured kernel

@@ -22,12 +22,14 @@ if has words; then
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_expand -s 6 -c 1 \
       -o gpurun_out/prof_trav_words_$T -f python bench.py --workload words --steps 1 --warmup 1 --no-cpu-baseline \
       > gpurun_out/ncu_trav_words_$T.log 2>&1; st ncu_trav_words $?
+  tools/ncu_shrink.sh gpurun_out/prof_trav_words_$T.ncu-rep
 fi
 if has vec128; then
-  tools/gpu_profile.sh vec128 $T k_leafgroup_mma2 6
+  tools/gpu_profile.sh vec128 $T k_leafgroup_mma 6
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_expand -s 20 -c 1 \
       -o gpurun_out/prof_trav_vec128_$T -f python bench.py --workload vec128 --steps 1 --warmup 1 --no-cpu-baseline \
       > gpurun_out/ncu_trav_vec128_$T.log 2>&1; st ncu_trav_vec128 $?
+  tools/ncu_shrink.sh gpurun_out/prof_trav_vec128_$T.ncu-rep
 fi
 if has small; then
   for w in tloc dna; do timeout 900 python bench.py --workload $w > gpurun_out/bench_${w}_$T.json 2> gpurun_out/bench_${w}_$T.err; st bench_$w $?; done
@@ -38,6 +40,7 @@ if has l1; then
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_leafgroup_tile -s 20 -c 1 \
       -o gpurun_out/prof_l1shard_$T -f python bench.py --workload l1shard --steps 1 --warmup 1 --no-cpu-baseline \
       > gpurun_out/ncu_l1shard_$T.log 2>&1; st ncu_l1shard $?
+  tools/ncu_shrink.sh gpurun_out/prof_l1shard_$T.ncu-rep
 fi
 if has l1big; then
   timeout 2400 python bench.py --workload l1_100m --steps 3 --warmup 3 > gpurun_out/bench_l1_100m_$T.json 2> gpurun_out/bench_l1_100m_$T.err; st bench_l1_100m $?
