@@ -2218,38 +2218,48 @@ k_leafgroup_mma3(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
     tc::fence_after_sync();
     const uint32_t tmem = tmem_slot;
 
-    struct It {
-        int start, count, size, pos;
+    struct It {   // item descriptor; count (<= 128) and size packed in one word
+        int start, cs, pos;
+        __device__ int count() const { return cs & 0xff; }
+        __device__ int size() const { return cs >> 8; }
     };
     auto item_of = [&](int i) {
-        It t{0, 0, 0, 0};
+        It t{0, 0, 0};
         if (idx(i) < nitems) {
             const Item x = items[idx(i)];
-            t = It{x.start, x.count, x.size, x.pos};
+            t = It{x.start, x.count | (x.size << 8), x.pos};
         }
         return t;
     };
+    // Row metadata in three pipelined steps, one per iteration, so no load
+    // of an iteration waits on another load of the same iteration:
+    //   descriptor of item i+4 -> this row's (q, dqp) of item i+3 ->
+    //   r, |q|, r0 of item i+2 (queries the row holds)
     struct RowMeta {
         int q;
         float dqp, r, qn, r0;
     };
-    auto row_meta = [&](const It &t) {
+    auto row_of = [&](const It &t) {
         RowMeta m{-1, 0.f, -1.f, 0.f, 0.f};
-        if (row < t.count) {
+        if (row < t.count()) {
             const Row lr = srows[t.start + row];
             m.q = lr.q;
             m.dqp = lr.dqp;
-            m.r = __ldcg(r32 + lr.q);
-            m.qn = qv.qn[lr.q];
-            m.r0 = r0 ? r0[lr.q] : 0.f;
         }
         return m;
+    };
+    auto finish_meta = [&](RowMeta &m) {
+        if (m.q >= 0) {
+            m.r = __ldcg(r32 + m.q);
+            m.qn = qv.qn[m.q];
+            m.r0 = r0 ? r0[m.q] : 0.f;
+        }
     };
     // operands of item i into stage i & 1, then this thread's noinc arrival
     // on full[i & 1] (fires when its copies have landed)
     auto stage = [&](int i, const It &t, int q) {
         const int st = i & 1;
-        const int N = max(16, (t.size + 15) & ~15);
+        const int N = max(16, (t.size() + 15) & ~15);
         const uint32_t A = tc::smem_u32(sm + st * stage_bytes);
         const uint32_t B = A + (uint32_t)a_bytes;
         // A: this row's query vector, quarter `part` of its chunks
@@ -2272,13 +2282,13 @@ k_leafgroup_mma3(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
         for (int f = tid; f < total; f += kM3Threads) {
             const int r = f >> lc, c = f & (c16 - 1);
             tc::cp_async16(B + (uint32_t)(c >> 3) * (uint32_t)N * 128u + tc::sw128_offset(r, c & 7),
-                           ix.vcent + (size_t)(t.pos + r) * c16 + c, r < t.size ? 16u : 0u);
+                           ix.vcent + (size_t)(t.pos + r) * c16 + c, r < t.size() ? 16u : 0u);
         }
         tc::cp_async_mbar_arrive(&full[st]);
     };
     auto mma = [&](int i, const It &t) {
         const int st = i & 1;
-        const int N = max(16, (t.size + 15) & ~15);
+        const int N = max(16, (t.size() + 15) & ~15);
         const uint32_t idesc = tc::idesc_bf16(128, N);
         const uint32_t a0 = tc::smem_u32(sm + st * stage_bytes), b0 = a0 + (uint32_t)a_bytes;
         for (int kb = 0; kb < nkb; kb++) {
@@ -2295,8 +2305,10 @@ k_leafgroup_mma3(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
     unsigned long long pairs = 0, w_entries = 0, w_rows = 0, w_macs = 0;
     // row metadata runs two items ahead, so the query id a copy needs is in
     // a register when the copy is issued
-    It cur = item_of(0), nxt = item_of(1);
-    RowMeta mc = row_meta(cur), mn = row_meta(nxt);
+    It cur = item_of(0), nxt = item_of(1), nx2 = item_of(2), nx3 = item_of(3);
+    RowMeta mc = row_of(cur), mn = row_of(nxt), m2 = row_of(nx2);
+    finish_meta(mc);
+    finish_meta(mn);
     if (idx(0) < nitems) {
         stage(0, cur, mc.q);
         if (tid == 0) {
@@ -2309,8 +2321,9 @@ k_leafgroup_mma3(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
     for (int i = 0; idx(i) < nitems; i++) {
         const int s = i & 1;
         const uint32_t ph = (uint32_t)(i >> 1) & 1u;
-        const It n2 = item_of(i + 2);
-        const RowMeta m2 = row_meta(n2);
+        const It nx4 = item_of(i + 4);     // step 1
+        const RowMeta m3 = row_of(nx3);    // step 2 (descriptor loaded last iteration)
+        finish_meta(m2);                   // step 3 (row loaded last iteration)
         // operands of item i+1 into the other stage (MMA i-1, its last reader,
         // completed before this thread's epilogue of item i-1)
         if (idx(i + 1) < nitems) stage(i + 1, nxt, mn.q);
@@ -2319,7 +2332,7 @@ k_leafgroup_mma3(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
         tc::fence_after_sync();
         // ---- epilogue of item i: row `row`, columns 16 * part + 64 k ----
         {
-            const int size = cur.size;
+            const int size = cur.size();
             const int N = max(16, (size + 15) & ~15);
             const int q = mc.q;
             const bool valid = q >= 0;
@@ -2417,8 +2430,8 @@ k_leafgroup_mma3(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
             if (valid && stats_on && ver) atomicAdd(verified_stat + q, (unsigned long long)ver);
             pairs += ver;
             if (tid == 0) {
-                w_entries += (unsigned long long)size * cur.count;
-                w_rows += (unsigned long long)cur.count;
+                w_entries += (unsigned long long)size * cur.count();
+                w_rows += (unsigned long long)cur.count();
                 w_macs += (unsigned long long)128 * N * ix.Dk;
             }
         }
@@ -2437,9 +2450,12 @@ k_leafgroup_mma3(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
         }
         __syncwarp();
         cur = nxt;
+        nxt = nx2;
+        nx2 = nx3;
+        nx3 = nx4;
         mc = mn;
-        nxt = n2;
         mn = m2;
+        m2 = m3;
     }
     if (work) {
         for (int o = 16; o > 0; o >>= 1) pairs += __shfl_down_sync(kFull, pairs, o);
