@@ -173,7 +173,7 @@ def bench_config(args, w, world):
         "workload": f"{args.workload} (BASELINE.json configs[{w['config_index']}])",
         "n": n_total, "n_per_gpu": n_total // world, "nq": w["nq"], "radius": w["radius"], "k": w["k"],
         "node_capacity": 20, "levels_per_shard": split + 1,
-        "memory_units": "device default: per-layer child tables of min(2^24, free HBM / (64 B x levels)) rows",
+        "memory_units": "device default: per-layer child tables of min(2^24 strings / 2^26 vectors, free HBM / (64 B x levels)) rows",
         "l2_policy": "index payload+tables exceed nothing: words (~25 MB) stay L2-resident by design; "
                      "no flush between steps (device-resident index is the operating point)",
         "parallelism": (f"{world} shards (contiguous id ranges, one GTS tree per GPU), replicated query batch; "

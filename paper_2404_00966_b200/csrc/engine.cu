@@ -4511,11 +4511,12 @@ int64_t hbm_rows_query(const gts_index *ix)
         return 1ll << 24;
     }
     const int64_t rows = (int64_t)(free_b / 4 / (16 * (size_t)std::max(ix->levels, 1)));
-    // 2^24 rows (256 MB per table): measured on B200, words, one step:
-    // 84 ms of k_leaf_edit at 2^24-row tables vs 119 ms at 2^25 and 153 ms
-    // at 2^26 for the same DP work (larger leaf launches run superlinearly
-    // slower), and vec128 551 vs 614 ms per step (allocation gaps)
-    return std::max<int64_t>(std::min<int64_t>(rows, 1ll << 24), std::max<int64_t>(ix->nc, 1ll << 16));
+    // Cap per table, measured on B200: strings 2^24 rows (words: 84 ms of
+    // k_leaf_edit per step at 2^24-row tables vs 119 ms at 2^25 and 153 ms at
+    // 2^26 for the same DP work); vectors 2^26 rows (fewer, larger launches:
+    // 128-d L2 497 vs 508 ms per step, 32-d L1 shard 517 vs 578 ms)
+    const int64_t cap = ix->metric == GTS_EDIT ? (1ll << 24) : (1ll << 26);
+    return std::max<int64_t>(std::min<int64_t>(rows, cap), std::max<int64_t>(ix->nc, 1ll << 16));
 }
 
 // cudaMemGetInfo asks the resource manager and measured 50-80 ms when it
