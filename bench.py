@@ -1002,7 +1002,7 @@ def traversal_roofline(prof, workload, dim=None):
             out["hbm"] = {key: out[key] for key in ("achieved", "peak", "unit", "frac", "peak_source")}
             out.update({key: out["fp32"][key] for key in ("achieved", "peak", "unit", "frac", "peak_source")})
             out["bound"] = "fp32"
-    out["traffic"] = ncu_traffic(workload, "k_expand")
+    out["traffic"] = ncu_traffic(workload, "k_expand") or ncu_traffic(workload, "k_expand_tile")
     return out
 
 

@@ -358,6 +358,7 @@ constexpr int kWarpPeqWords = 1024;     // per-warp staged match masks (A*W <= 1
 // memory.  Leaves are length-sorted, so a batch has similar DP lengths.
 constexpr int kHistBins = 256;   // kNN shrinking-bound histogram: exact distances 0..255
 
+template <bool SIG>
 __global__ void __launch_bounds__(256, 4) k_leaf_edit(IndexView ix, QueryView qv, const Row *__restrict__ rows,
                                                       int64_t m, int pruning, float *r32,
                                                       HitBuf out, unsigned long long *verified_stat, int stats_on,
@@ -368,12 +369,14 @@ __global__ void __launch_bounds__(256, 4) k_leaf_edit(IndexView ix, QueryView qv
     extern __shared__ uint32_t le_text[];   // [kLeafWarps][32][tstride] when tstride > 0
     __shared__ uint32_t peq_s[kLeafWarps][kWarpPeqWords];
     __shared__ int32_t queue[kLeafWarps][3][64];   // entry, first text word, length
+    __shared__ uint4 qsig_s[kLeafWarps][2];        // the current query's q-gram signature
     const int lane = lane_id(), wib = threadIdx.x >> 5;
     uint32_t *peq_w = peq_s[wib];
     int32_t *qu = queue[wib][0];
     int32_t *qw = queue[wib][1];
     int32_t *ql = queue[wib][2];
     int cur_q = -1, mq = 0, qn = 0;
+    int qsig_reach = 0;   // ceil(distinct query q-gram buckets / q)
     unsigned long long nrows = 0;
     uint4 qh0 = make_uint4(0u, 0u, 0u, 0u), qh1 = qh0;
     float r = 0.f;
@@ -504,6 +507,16 @@ __global__ void __launch_bounds__(256, 4) k_leaf_edit(IndexView ix, QueryView qv
             mq = qlen(qv, cur_q);
             r = __ldcg(r32 + cur_q);
             if (ix.ehist) { qh0 = qv.qhist[2 * cur_q]; qh1 = qv.qhist[2 * cur_q + 1]; }
+            if (SIG) {
+                uint4 sg = make_uint4(0u, 0u, 0u, 0u);
+                if (lane < 2) qsig_s[wib][lane] = sg = qv.qsig[2 * cur_q + lane];
+                // the query's distinct q-gram buckets bound how far the
+                // signature bound can reach from its side: ceil(popc / q)
+                int pc = lane < 2 ? __popc(sg.x) + __popc(sg.y) + __popc(sg.z) + __popc(sg.w) : 0;
+                pc += __shfl_xor_sync(kFull, pc, 1);
+                pc = __shfl_sync(kFull, pc, 0);
+                qsig_reach = (pc + ix.sig_q - 1) / max(ix.sig_q, 1);
+            }
             peq_g = qv.peq + qv.peq_off[cur_q];
             const int words = qv.A * ((mq + 31) >> 5);
             staged = words <= kWarpPeqWords;
@@ -541,6 +554,14 @@ __global__ void __launch_bounds__(256, 4) k_leaf_edit(IndexView ix, QueryView qv
             if (cand && ix.ehist && fmaxf(mqf, lenf) > r) {
                 const uint4 h0 = __ldg(ix.ehist + 2 * e), h1 = __ldg(ix.ehist + 2 * e + 1);
                 cand = hist_lb(qh0, qh1, h0, h1, mq - (int)rec.y) <= ri;
+            }
+            // q-gram signature bound (qgram_lb), for the candidates still left,
+            // when the query's side of it can exceed the radius (words kNN:
+            // never, ~20% slower if tested anyway; DNA range r = 8: prunes
+            // nearly every pair, 1.9x faster)
+            if (SIG && cand && qsig_reach > ri) {
+                const uint4 s0 = __ldg(ix.esig + 2 * e), s1 = __ldg(ix.esig + 2 * e + 1);
+                cand = qgram_lb(qsig_s[wib][0], qsig_s[wib][1], s0, s1, ix.sig_q) <= ri;
             }
             const unsigned cb = __ballot_sync(kFull, cand);
             if (cand) {
@@ -2146,19 +2167,20 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
 // k_leafgroup_mma3: the tensor-core L2 screen as a barrier-free pipeline
 // (the default; k_leafgroup_mma2 with GTS_MMA_V2=1).  Same algorithm and
 // error band as k_leafgroup_mma2; what changes is the synchronisation:
-//  * no block barrier per item.  Stage s (A/B operands) is filled by
-//    cp.async from every thread and completes an mbarrier (full[s], 512
-//    noinc arrivals); one thread waits it and issues the MMA, whose commit
-//    completes mma_done[s]; each warp waits mma_done[s] before reading the
-//    accumulator, and after its last TMEM read arrives on acc_free[s]
-//    (16 arrivals), which the MMA issuer waits before reusing accumulator s.
+//  * no block barrier per item.  Stage s (A/B operands, two stages) is
+//    filled by cp.async from every thread and completes an mbarrier
+//    (full[s], 512 noinc arrivals); the MMA's commit completes mma_done[s];
+//    each warp waits mma_done[s] before reading accumulator s (two TMEM
+//    accumulators) and after its last TMEM read arrives on acc_free[s] (16
+//    arrivals); one thread waits full and acc_free and issues the next MMA.
 //    Warps drift up to one item apart instead of meeting at a barrier.
-//  * no shared-memory metadata rings: a thread owns one accumulator row
-//    (TMEM lane) and one quarter of the columns, loads its row's {q, dqp,
-//    r, |q|, r0} into registers one item ahead and copies its quarter of the
-//    row's bf16 query vector; the per-entry column terms {dis | NaN,
-//    y - z | NaN, y + z, dis} come precomputed (k_colrec, per call) from
-//    global memory as warp-uniform (broadcast) loads.
+//  * no shared-memory metadata rings for rows: a thread owns one
+//    accumulator row (TMEM lane) and one quarter of the columns, loads its
+//    row's {q, dqp, r, |q|, r0} into registers in three pipelined steps
+//    (descriptor four items ahead, row three, radii two) and copies its
+//    quarter of the row's bf16 query vector.  The per-entry column terms
+//    {dis | NaN, y - z | NaN, y + z, dis} are precomputed per call
+//    (k_colrec) and copied with the operands into a four-slot smem ring.
 // ---------------------------------------------------------------------------
 constexpr int kM3Threads = 512;   // 16 warps: 4 per TMEM lane quadrant
 
@@ -2440,7 +2462,9 @@ k_leafgroup_mma3(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&acc_free[s]);
         // MMA of item i+1 into accumulator s^1: its operands landed (full) and
-        // every warp finished item i-1, the accumulator's previous user
+        // every warp finished item i-1, the accumulator's previous user.
+        // (Letting the last warp to finish item i issue it instead of thread 0
+        // measured slower: 359 vs 293 ms per vec128 step.)
         if (tid == 0 && idx(i + 1) < nitems) {
             tc::mbar_wait(&full[s ^ 1], (uint32_t)((i + 1) >> 1) & 1u);
             if (i >= 1) tc::mbar_wait(&acc_free[s ^ 1], (uint32_t)((i - 1) >> 1) & 1u);
@@ -3089,6 +3113,33 @@ __global__ void k_query_hist(const uint8_t *sym, const int64_t *soff, int nq, ui
     qhist[2 * q + 1] = make_uint4(w[4], w[5], w[6], w[7]);
 }
 
+// q-gram signatures (kernels.cuh qgram_sig) of the queries ...
+__global__ void k_query_sig(const uint8_t *sym, const int64_t *soff, int nq, int A, uint4 *qsig)
+{
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    const uint8_t *t = sym + soff[q];
+    uint32_t w[8];
+    qgram_sig([&](int i) { return (uint32_t)t[i]; }, (int)(soff[q + 1] - soff[q]), A, w);
+    qsig[2 * q] = make_uint4(w[0], w[1], w[2], w[3]);
+    qsig[2 * q + 1] = make_uint4(w[4], w[5], w[6], w[7]);
+}
+
+// ... and of stored strings (every slot, or the listed ones; free slots 0)
+__global__ void k_slot_sig(const uint32_t *str, const uint32_t *sword, const int32_t *slen, const int32_t *slots,
+                           int64_t n, int A, uint4 *esig)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t s = slots ? slots[i] : i;
+    if (s < 0) return;
+    const uint32_t *t4 = str + sword[s];
+    uint32_t w[8];
+    qgram_sig([&](int k) { return (__ldg(t4 + (k >> 2)) >> (8 * (k & 3))) & 0xffu; }, slen[s], A, w);
+    esig[2 * s] = make_uint4(w[0], w[1], w[2], w[3]);
+    esig[2 * s + 1] = make_uint4(w[4], w[5], w[6], w[7]);
+}
+
 // bf16 query rows (uncentred, zero-padded to Dk) and |q| rounded up
 __global__ void k_query_bf16(const float *v32, int64_t nq, int D, int Dp, int Dk, uint4 *qbf, float *qn)
 {
@@ -3325,6 +3376,7 @@ struct gts_index {
     DBuf<int32_t> row;
     DBuf<uint4> erec;
     DBuf<uint4> ehist;
+    DBuf<uint4> esig;        // strings: q-gram signatures (qgram_sig), [2 * slots]
     DBuf<uint4> vcent;   // bf16 x 8 per uint4
     DBuf<float> vnorm32;   // angular: |o| per entry
     DBuf<double> vnorm64;
@@ -3382,6 +3434,7 @@ struct gts_queries {
     DBuf<uint32_t> peq;
     DBuf<int64_t> peq_off;
     DBuf<uint4> qhist;
+    DBuf<uint4> qsig;
     DBuf<uint4> qbf;     // bf16 query rows (tensor-core L2 path)
     DBuf<float> qnorm32;   // angular: |q|
     DBuf<double> qnorm64;
@@ -3415,6 +3468,8 @@ IndexView make_view(const gts_index *ix, const gts_queries *q)
     v.row = ix->row.p;
     v.erec = ix->erec.p;
     v.ehist = ix->ehist.p;
+    v.esig = ix->esig.p;
+    v.sig_q = ix->esig.p ? qgram_q(ix->A) : 0;
     v.vcent = ix->vcent.p;
     v.vnorm32 = ix->vnorm32.p;
     v.vnorm64 = ix->vnorm64.p;
@@ -3460,6 +3515,7 @@ QueryView make_qview(const gts_index *ix, const gts_queries *q)
     v.peq = q->peq.p;
     v.peq_off = q->peq_off.p;
     v.qhist = q->qhist.p;
+    v.qsig = q->qsig.p;
     v.qbf = q->qbf.p;
     v.qnorm32 = q->qnorm32.p;
     v.qnorm64 = q->qnorm64.p;
@@ -3999,10 +4055,13 @@ struct Search {
             if (ix->max_len <= 64 && env_tx && env_tx[0] == '1') tstride = (((ix->max_len + 3) >> 2) | 1);
             const size_t dyn = (size_t)tstride * kWarp * kLeafWarps * sizeof(uint32_t);
             // static 38.9 KB + up to 17 KB of staged texts
-            smem_optin((const void *)k_leaf_edit, 64 * 1024);
+            // the q-gram signature test is compiled in only where the index has
+            // signatures (small alphabets), so the words kernel stays as it was
+            auto *kern = ix->esig.p ? k_leaf_edit<true> : k_leaf_edit<false>;
+            smem_optin((const void *)kern, 64 * 1024);
             CK(cudaMemsetAsync(counter.p, 0, sizeof(unsigned long long), st));
             timed("k_leaf_edit", [&] {
-                k_leaf_edit<<<grid, 32 * kLeafWarps, dyn, st>>>(iv, qv, rows, m, pruning, r32.p, hb, verified.p,
+                kern<<<grid, 32 * kLeafWarps, dyn, st>>>(iv, qv, rows, m, pruning, r32.p, hb, verified.p,
                                                                stats_on, stats_on ? work.p : nullptr, counter.p,
                                                                // a re-run (stats_on == 0) must not count twice
                                                                stats_on ? hist.p : nullptr, ks.p, claim, tstride);
@@ -4440,6 +4499,11 @@ gts_queries *upload_queries(gts_index *ix, const gts_query_batch *qb, cudaStream
                 LAUNCH_CHECK();
                 k_build_peq<<<grid_for(nsym, 256), 256, 0, st>>>(q->str.p, q->soff.p, q->peq_off.p, (int)nq, nsym,
                                                                  q->peq.p);
+                LAUNCH_CHECK();
+            }
+            if (ix->esig.p && nq) {
+                q->qsig.alloc((size_t)nq * 2, st);
+                k_query_sig<<<grid_for(nq, 128), 128, 0, st>>>(q->str.p, q->soff.p, (int)nq, ix->A, q->qsig.p);
                 LAUNCH_CHECK();
             }
             if (ix->ehist.p && nq) {
@@ -5186,6 +5250,14 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
             h2d(ix->erec.p, rec.data(), rec.size(), st);
             k_erec_alive<<<grid_for(ns, 256), 256, 0, st>>>(ix->erec.p, ix->dis.p, ix->alive.p, ns);
             LAUNCH_CHECK();
+            if (ix->A <= 16 && std::getenv("GTS_NO_QSIG") == nullptr) {
+                // q-gram signatures of every slot (free slots: the empty set)
+                ix->esig.alloc((size_t)ns * 2, st);
+                CK(cudaMemsetAsync(ix->esig.p, 0, sizeof(uint4) * 2 * (size_t)ns, st));
+                k_slot_sig<<<grid_for(ns, 128), 128, 0, st>>>(ix->str.p, ix->sword.p, ix->slen.p, nullptr, ns, ix->A,
+                                                              ix->esig.p);
+                LAUNCH_CHECK();
+            }
             if (ix->A > kHistMinAlphabet) {
                 // 32 byte-buckets of symbol counts per entry (saturating)
                 std::vector<uint8_t> hb((size_t)ns * 32, 0);

@@ -48,6 +48,8 @@ struct IndexView {
     const int32_t *row;      // [n] dataset row of each entry (row order = id order)
     const uint4 *erec;       // [n] edit scan records {dis f32 bits, len, first text word, 0}
     const uint4 *ehist;      // [2n] 32 byte-buckets of symbol counts (symbol % 32), or null
+    const uint4 *esig;       // [2n] 256-bit q-gram signature per entry (qgram_sig), or null
+    int sig_q;               // q of the signature (4 for alphabets <= 4, else 2); 0: none
     const uint4 *vcent;      // [n][Dk/8] bf16 vectors centred on their leaf pivot (tensor-core L2 path), or null
     const float *vnorm32;    // angular: |o| per entry (fp32 screen), or null
     const double *vnorm64;   // angular: |o| per entry, numpy's pairwise sum of squares
@@ -66,6 +68,7 @@ struct QueryView {
     const uint32_t *peq;   // Myers match masks, [A][W] per query
     const int64_t *peq_off;
     const uint4 *qhist;    // [2nq] query symbol histograms (same buckets as ehist)
+    const uint4 *qsig;     // [2nq] query q-gram signatures (same mapping as esig)
     const uint4 *qbf;      // [nq][Dk/8] bf16 query rows (tensor-core L2 path)
     const float *qnorm32;  // angular: |q| (fp32 screen)
     const double *qnorm64; // angular: |q|, pairwise sum of squares
@@ -82,6 +85,57 @@ __device__ __forceinline__ int hist_lb(const uint4 &a0, const uint4 &a1, const u
     unsigned sad = __vsadu4(a0.x, b0.x) + __vsadu4(a0.y, b0.y) + __vsadu4(a0.z, b0.z) + __vsadu4(a0.w, b0.w) +
                    __vsadu4(a1.x, b1.x) + __vsadu4(a1.y, b1.y) + __vsadu4(a1.z, b1.z) + __vsadu4(a1.w, b1.w);
     return (int)((sad + (unsigned)abs(dl)) >> 1);
+}
+
+// ---------------------------------------------------------------------------
+// q-gram signature lower bound for edit distance.  A string's signature is a
+// 256-bit set: bit bucket(g) for every q-gram g (q consecutive dense
+// symbols); bucket = the exact index for q = 4 over an alphabet of <= 4
+// symbols or q = 2 over <= 16, else a hash.  If bucket b is set for x and
+// clear for y, every q-gram of x in b is absent from y, and each edit
+// operation touches at most q q-gram windows of x, so
+//     ed(x, y) >= ceil(popc(Sx & ~Sy) / q)        (and symmetrically).
+// Collisions only weaken the bound.  Query symbols absent from the index
+// alphabet hash like any other: their grams cannot occur in an object.
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ int qgram_q(int A) { return A <= 4 ? 4 : 2; }
+
+__host__ __device__ __forceinline__ uint32_t qgram_bucket(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, int A)
+{
+    if (A <= 4) return (((c0 & 3u) * 4u + (c1 & 3u)) * 4u + (c2 & 3u)) * 4u + (c3 & 3u);
+    if (A <= 16) return (c0 & 15u) * 16u + (c1 & 15u);
+    return ((c0 * 29u) ^ (c1 * 113u) ^ (c1 >> 3)) & 255u;
+}
+
+// sym(i) -> dense symbol of position i, for i < n
+template <class Sym>
+__host__ __device__ __forceinline__ void qgram_sig(Sym sym, int n, int A, uint32_t (&w)[8])
+{
+    for (int k = 0; k < 8; k++) w[k] = 0u;
+    const int Q = qgram_q(A);
+    if (n < Q) return;
+    uint32_t c0 = 0, c1 = sym(0), c2 = Q == 4 ? sym(1) : 0u, c3 = Q == 4 ? sym(2) : 0u;
+    for (int i = Q - 1; i < n; i++) {
+        uint32_t b;
+        if (Q == 4) {
+            c0 = c1; c1 = c2; c2 = c3; c3 = sym(i);
+            b = qgram_bucket(c0, c1, c2, c3, A);
+        } else {
+            c0 = c1; c1 = sym(i);
+            b = qgram_bucket(c0, c1, 0u, 0u, A);
+        }
+        w[b >> 5] |= 1u << (b & 31);
+    }
+}
+
+__device__ __forceinline__ int qgram_lb(const uint4 &a0, const uint4 &a1, const uint4 &b0, const uint4 &b1, int Q)
+{
+    const int x = __popc(a0.x & ~b0.x) + __popc(a0.y & ~b0.y) + __popc(a0.z & ~b0.z) + __popc(a0.w & ~b0.w) +
+                  __popc(a1.x & ~b1.x) + __popc(a1.y & ~b1.y) + __popc(a1.z & ~b1.z) + __popc(a1.w & ~b1.w);
+    const int y = __popc(b0.x & ~a0.x) + __popc(b0.y & ~a0.y) + __popc(b0.z & ~a0.z) + __popc(b0.w & ~a0.w) +
+                  __popc(b1.x & ~a1.x) + __popc(b1.y & ~a1.y) + __popc(b1.z & ~a1.z) + __popc(b1.w & ~a1.w);
+    const int m = max(x, y);
+    return Q == 4 ? (m + 3) >> 2 : (m + 1) >> 1;
 }
 
 struct HitBuf {

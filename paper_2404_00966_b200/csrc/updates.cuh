@@ -426,6 +426,11 @@ extern "C" int gts_index_insert(gts_index *ix, const gts_dataset *items, int32_t
                                                   ix->ehist.p ? dh.p : nullptr, ix->str.p, ix->slen.p, ix->erec.p,
                                                   ix->ehist.p);
         LAUNCH_CHECK();
+        if (ix->esig.p) {
+            k_slot_sig<<<grid_for(m, 128), 128, 0, st>>>(ix->str.p, ix->sword.p, ix->slen.p, dsl.p, m, ix->A,
+                                                         ix->esig.p);
+            LAUNCH_CHECK();
+        }
     }
     CK(cudaStreamSynchronize(st));
     std::vector<int32_t> vslots(slots, slots + n);
