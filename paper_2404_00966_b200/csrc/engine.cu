@@ -597,6 +597,36 @@ __global__ void __launch_bounds__(256, 4) k_leaf_edit(IndexView ix, QueryView qv
     }
 }
 
+// kNN: drop the hits already outside their query's (shrunk) radius.  The
+// radius only shrinks to values that keep k objects (and their ties) at or
+// below it, so such a hit can never be among the final k.  Output order is
+// free (collect sorts).
+__global__ void k_compact_hits(const int32_t *__restrict__ q, const int32_t *__restrict__ e,
+                               const double *__restrict__ d, int64_t n, const float *__restrict__ r32,
+                               const double *__restrict__ r64, int32_t *oq, int32_t *oe, double *od,
+                               unsigned long long *cnt)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool keep = false;
+    int32_t qi = 0;
+    if (i < n) {
+        qi = q[i];
+        keep = d[i] <= (r64 ? __ldcg(r64 + qi) : (double)__ldcg(r32 + qi));
+    }
+    const unsigned b = __ballot_sync(kFull, keep);
+    if (!b) return;
+    unsigned long long base = 0;
+    const int lane = lane_id();
+    if (lane == __ffs(b) - 1) base = atomicAdd(cnt, (unsigned long long)__popc(b));
+    base = __shfl_sync(kFull, base, __ffs(b) - 1);
+    if (keep) {
+        const unsigned long long o = base + __popc(b & ((1u << lane) - 1u));
+        oq[o] = qi;
+        oe[o] = e[i];
+        od[o] = d[i];
+    }
+}
+
 // erec.x = dis of live entries, NaN of tombstoned ones (every test fails)
 __global__ void k_erec_alive(uint4 *erec, const float *dis, const uint32_t *alive, int64_t n)
 {
@@ -1089,19 +1119,21 @@ __global__ void __launch_bounds__(256, 2) k_expand_tile(IndexView ix, QueryView 
             s_pruned[tid] = 0u;
         }
         __syncthreads();
+        // staging by cp.async (many 16-byte copies in flight per thread;
+        // absent rows / children zero-filled)
         for (int t = tid; t < 4 * CPG * d4; t += blockDim.x) {
             const int j = t / d4, c = t - j * d4;
-            reinterpret_cast<float4 *>(piv_s + (size_t)j * ps)[c] =
-                j < nc ? __ldg(reinterpret_cast<const float4 *>(ix.vec32 + (size_t)rec_s[j].piv * ix.Dp) + c)
-                       : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float *src = ix.vec32 + (size_t)(j < nc ? rec_s[j].piv : 0) * ix.Dp + 4 * c;
+            tc::cp_async16(tc::smem_u32(piv_s + (size_t)j * ps + 4 * c), src, j < nc ? 16u : 0u);
         }
         for (int t = tid; t < kXtRows * d4; t += blockDim.x) {
             const int a = t / d4, c = t - a * d4;
             const int q = s_q[a];
-            reinterpret_cast<float4 *>(qs_s + (size_t)a * ps)[c] =
-                q >= 0 ? __ldg(reinterpret_cast<const float4 *>(qv.vec32 + (size_t)q * ix.Dp) + c)
-                       : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float *src = qv.vec32 + (size_t)max(q, 0) * ix.Dp + 4 * c;
+            tc::cp_async16(tc::smem_u32(qs_s + (size_t)a * ps + 4 * c), src, q >= 0 ? 16u : 0u);
         }
+        tc::cp_async_commit();
+        tc::cp_async_wait_all();
         __syncthreads();
         float acc[2][CPG];
 #pragma unroll
@@ -1366,25 +1398,30 @@ __global__ void __launch_bounds__(256, 4) k_leafgroup_tile(IndexView ix, QueryVi
                        : make_float4(0.f, 0.f, 0.f, 0.f);
         }
         __syncthreads();
+        // tasks = (4-entry chunk, half of the 128 rows): a lane computes a
+        // 2-row x 4-entry tile.  Small leaves (the 12.5M shard's ~78 entries:
+        // 20 chunks) then split evenly over the 8 warps (40 tasks) instead of
+        // 3 / 2 chunks per warp waiting at the item barrier.
         const int nchunks = (size + 3) >> 2;
-        unsigned ver[4] = {0u, 0u, 0u, 0u};
-        for (int ch = warp; ch < nchunks; ch += 8) {
+        for (int task = warp; task < 2 * nchunks; task += 8) {
+            const int ch = task >> 1, half = task & 1;
             const int e0 = ch * 4;
-            float acc[4][4];
+            const int rbase = lane + 64 * half;   // rows rbase, rbase + 32
+            float acc[2][4];
 #pragma unroll
-            for (int a = 0; a < 4; a++)
+            for (int a = 0; a < 2; a++)
 #pragma unroll
                 for (int b = 0; b < 4; b++) acc[a][b] = 0.f;
-            const float *qrow = qs + lane * stride;
+            const float *qrow = qs + rbase * stride;
             const float *erow = ent + e0 * stride;
             for (int c = 0; c < d4; c++) {
-                float4 x[4], y[4];
+                float4 x[2], y[4];
 #pragma unroll
-                for (int a = 0; a < 4; a++) x[a] = *reinterpret_cast<const float4 *>(qrow + a * 32 * stride + 4 * c);
+                for (int a = 0; a < 2; a++) x[a] = *reinterpret_cast<const float4 *>(qrow + a * 32 * stride + 4 * c);
 #pragma unroll
                 for (int b = 0; b < 4; b++) y[b] = *reinterpret_cast<const float4 *>(erow + b * stride + 4 * c);
 #pragma unroll
-                for (int a = 0; a < 4; a++)
+                for (int a = 0; a < 2; a++)
 #pragma unroll
                     for (int b = 0; b < 4; b++) {
                         const float d0 = x[a].x - y[b].x, d1 = x[a].y - y[b].y;
@@ -1396,12 +1433,13 @@ __global__ void __launch_bounds__(256, 4) k_leafgroup_tile(IndexView ix, QueryVi
                     }
             }
 #pragma unroll
-            for (int a = 0; a < 4; a++) {
-                const int row = lane + 32 * a;
+            for (int a = 0; a < 2; a++) {
+                const int row = rbase + 32 * a;
                 const int q = s_q[row];
                 const float r = s_r[row];
                 const float2 rg = make_float2(s_lo[row], s_hi[row]);
                 bool any_ub = false;
+                unsigned ver = 0;
                 uint32_t cmask = 0;   // candidates of this row among the 4 entries
 #pragma unroll
                 for (int b = 0; b < 4; b++) {
@@ -1410,7 +1448,7 @@ __global__ void __launch_bounds__(256, 4) k_leafgroup_tile(IndexView ix, QueryVi
                     const float dis = s_dis[j];
                     if (!(dis == dis)) continue;   // tombstoned
                     if (pruning && !lemma1_in(dis, rg)) continue;
-                    ver[a]++;
+                    ver++;
                     const float d = MET == kMetricL1 ? acc[a][b] : sqrtf(acc[a][b]);
                     const float sl = slack(ix, d, 0.f);
                     if (!(d - sl <= r)) continue;
@@ -1422,6 +1460,7 @@ __global__ void __launch_bounds__(256, 4) k_leafgroup_tile(IndexView ix, QueryVi
                         any_ub = true;
                     }
                 }
+                if (ver) atomicAdd(s_ver + row, ver);
                 // warp-aggregated append (one atomic per warp instead of per candidate)
                 if (__any_sync(kFull, cmask)) {
                     const unsigned nc = __popc(cmask);
@@ -1455,9 +1494,6 @@ __global__ void __launch_bounds__(256, 4) k_leafgroup_tile(IndexView ix, QueryVi
                 }
             }
         }
-#pragma unroll
-        for (int a = 0; a < 4; a++)
-            if (ver[a]) atomicAdd(s_ver + lane + 32 * a, ver[a]);
         __syncthreads();
         if (threadIdx.x < 128) {
             const int q = s_q[threadIdx.x];
@@ -4010,6 +4046,29 @@ struct Search {
             after = read_counter(1);
         }
         hits = after;
+        if (mode == 1 && hits > compact_at) compact_hits();
+    }
+
+    // kNN hit buffers: keep only the hits inside the current radii (bounds
+    // the buffers and the final sort; a 1M-query k = 100 batch over 100M
+    // objects otherwise collects > 2^31 tie-inclusive hits)
+    unsigned long long compact_at = 1ull << 26;
+    void compact_hits()
+    {
+        const int64_t n = (int64_t)hits;
+        DBuf<int32_t> nq_((size_t)n, st), ne_((size_t)n, st);
+        DBuf<double> nd_((size_t)n, st);
+        CK(cudaMemsetAsync(counter.p + 1, 0, sizeof(unsigned long long), st));
+        k_compact_hits<<<grid_for(n, 256), 256, 0, st>>>(hq.p, he.p, hd.p, n, r32.p,
+                                                         ix->metric == GTS_EDIT ? nullptr : r64.p, nq_.p, ne_.p,
+                                                         nd_.p, counter.p + 1);
+        LAUNCH_CHECK();
+        const unsigned long long kept = read_counter(1);
+        CK(cudaMemcpyAsync(hq.p, nq_.p, kept * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(he.p, ne_.p, kept * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(hd.p, nd_.p, kept * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        hits = kept;
+        compact_at = std::max<unsigned long long>(compact_at, 2 * kept);
     }
 
     DBuf<unsigned> hist;   // kNN edit: per-query distance histogram (shrinking bound)

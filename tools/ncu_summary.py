@@ -111,6 +111,29 @@ def capture_traffic(path):
     return short, int(tot)
 
 
+def source_hotspots(src_gz, top=12):
+    """Per-CUDA-line stall samples and executed instructions from the shrunk
+    source page (<name>.src.csv.gz, --print-source cuda,sass)."""
+    import gzip
+    rows = list(csv.reader(io.StringIO(gzip.open(src_gz, "rt").read())))
+    lines = []
+    fname = "?"
+    for r in rows:
+        if r and r[0] == "File Path" and len(r) > 1:
+            fname = os.path.basename(r[1])
+        elif r and r[0].strip().isdigit():
+            try:
+                lines.append((f"{fname}:{int(r[0])}", float(r[4]), float(r[7]), r[1].strip()[:90]))
+            except (ValueError, IndexError):
+                pass
+    ts = sum(x[1] for x in lines) or 1.0
+    ti = sum(x[2] for x in lines) or 1.0
+    out = ["| file:line | stall samples | instructions | source |", "|---|---:|---:|---|"]
+    for ln, st, ins, src in sorted(lines, key=lambda x: -x[1])[:top]:
+        out.append(f"| {ln} | {100 * st / ts:.1f}% | {100 * ins / ti:.1f}% | `{src.replace('|', '\\|')}` |")
+    return "\n".join(out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--tag", required=True)
@@ -132,6 +155,10 @@ def main():
                     + sorted(glob.glob(os.path.join(OUT, f"prof_*{a.workload}*_{a.tag}.raw.csv.gz")))):
         parts += [f"## full capture `{os.path.basename(rep)}` (ncu --set full --clock-control none)", "",
                   full_capture(rep), ""]
+        src = rep.replace(".raw.csv.gz", ".src.csv.gz")
+        if src != rep and os.path.exists(src):
+            parts += ["source hot spots (share of stall samples, share of executed warp instructions):", "",
+                      source_hotspots(src), ""]
         # roofline.traffic source for bench.py: DRAM bytes per launch of the captured kernel
         kname, tb = capture_traffic(rep)
         tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
