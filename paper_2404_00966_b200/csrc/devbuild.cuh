@@ -661,6 +661,7 @@ extern "C" int gts_index_create_f32dev(const gts_tree *t, int32_t metric, int64_
             ix->vse.alloc((size_t)ns, st);
             k_vse<<<grid_for(ns, 256), 256, 0, st>>>(ix->vec32.p, ix->D, ix->Dp, ix->Dk, dep.p, vc, ns, ix->vse.p);
             LAUNCH_CHECK();
+            build_vtile(ix, st);
         }
         CK(cudaStreamSynchronize(st));
         // max |x| (used only by inexact data's slack; kept for completeness)

@@ -713,15 +713,18 @@ __global__ void k_item_counts(const int *cnt, int nleaf, int per, int *nitem)
 }
 
 __global__ void k_make_items(const int *cnt, const int *off, const int *item_off, int nleaf, int leaf_first, int per,
-                             const NodeRec *node, const int32_t *npos, Item *items)
+                             const NodeRec *node, const int32_t *npos, Item *items, const int32_t *vt_off,
+                             const int32_t *vt_rows)
 {
     int l = blockIdx.x * blockDim.x + threadIdx.x;
     if (l >= nleaf) return;
     const int c = cnt[l];
     const int nd = leaf_first + l;
     const int size = c ? node[nd].size : 0, pos = c ? npos[nd] : 0;
+    // pad0: the leaf's image in vtile, (offset / 2 KB) << 8 | rows / 16
+    const int tr = c && vt_off ? (int)(((uint32_t)(vt_off[l] >> 4) << 8) | (uint32_t)(vt_rows[l] >> 4)) : 0;
     for (int j = 0, s = 0; s < c; j++, s += per)
-        items[item_off[l] + j] = Item{nd, off[l] + s, min(per, c - s), size, pos, 0, 0, 0};
+        items[item_off[l] + j] = Item{nd, off[l] + s, min(per, c - s), size, pos, tr, 0, 0};
 }
 
 // ---------------------------------------------------------------------------
@@ -2220,6 +2223,29 @@ k_leafgroup_mma2(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
 // ---------------------------------------------------------------------------
 constexpr int kM3Threads = 512;   // 16 warps: 4 per TMEM lane quadrant
 
+// vcent per leaf in the MMA's shared-memory image: leaf l owns R = rows[l]
+// (its slot capacity rounded up to 16) rows; K-block kb of row r, 16-byte
+// chunk c sits at off[l] * 128 + kb * R * 128 + sw128_offset(r, c), so one
+// bulk copy of N * 128 bytes per K-block lands a leaf's first N rows in
+// exactly the SW128 K-major layout the MMA descriptor reads (rows past the
+// capacity are zero).  Rebuilt after in-place inserts.
+__global__ void k_vtile(const uint4 *__restrict__ vcent, int c16, const int64_t *__restrict__ dpos,
+                        const int64_t *__restrict__ cap, const int32_t *__restrict__ off,
+                        const int32_t *__restrict__ rows, int nleaf, uint4 *vtile)
+{
+    for (int l = blockIdx.x; l < nleaf; l += gridDim.x) {
+        const int R = rows[l];
+        const int64_t p = dpos[l], cp = cap[l];
+        uint4 *dst = vtile + (size_t)off[l] * 8;
+        for (int t = threadIdx.x; t < R * c16; t += blockDim.x) {
+            const int r = t / c16, c = t - r * c16;
+            uint4 v = make_uint4(0u, 0u, 0u, 0u);
+            if (r < cp) v = vcent[(size_t)(p + r) * c16 + c];
+            dst[((size_t)(c >> 3) * R * 128 + tc::sw128_offset(r, c & 7)) >> 4] = v;
+        }
+    }
+}
+
 // per-entry column terms of the screen (see k_leafgroup_mma2's meta_store)
 __global__ void k_colrec(IndexView ix, int64_t n, float4 *colrec)
 {
@@ -2265,7 +2291,8 @@ k_leafgroup_mma3(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
     if (warp == 0) tc::tmem_alloc(&tmem_slot, 2 * acc_cols);
     if (tid == 0) {
         for (int k = 0; k < 2; k++) {
-            tc::mbar_init(&full[k], kM3Threads);
+            // + 1: the bulk-copy thread's expect_tx arrival
+            tc::mbar_init(&full[k], kM3Threads + (ix.vtile ? 1 : 0));
             tc::mbar_init(&mma_done[k], 1);
             tc::mbar_init(&acc_free[k], kM3Threads / 32);
         }
@@ -2334,13 +2361,30 @@ k_leafgroup_mma3(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
         // acc_free(i-2), so no warp still reads slot (i-2) % 4 = (i+2) % 4;
         // slots i-1 .. i+1 may be in use
         if (tid < N) tc::cp_async16(tc::smem_u32(&s_col[i & 3][tid]), colrec + t.pos + tid, 16u);
-        // B: the leaf's centred entries, N rows (rows >= size zero-filled;
-        // their source stays inside vcent's 16-row zero tail)
-        const int total = N * c16;
-        for (int f = tid; f < total; f += kM3Threads) {
-            const int r = f >> lc, c = f & (c16 - 1);
-            tc::cp_async16(B + (uint32_t)(c >> 3) * (uint32_t)N * 128u + tc::sw128_offset(r, c & 7),
-                           ix.vcent + (size_t)(t.pos + r) * c16 + c, r < t.size() ? 16u : 0u);
+        // B: the leaf's centred entries, N rows.  With the leaf images
+        // (vtile): one thread posts the byte count and issues one bulk copy
+        // per K-block (the TMA engine moves the tile; no per-thread copies).
+        // Otherwise per-thread cp.async with rows >= size zero-filled (their
+        // source stays inside vcent's 16-row zero tail).
+        if (ix.vtile) {
+            if (tid == 0) {
+                const uint32_t bytes = (uint32_t)N * 128u;
+                tc::mbar_arrive_expect_tx(&full[st], bytes * (uint32_t)nkb);
+                // the item's image word (its descriptor was read four items
+                // ago, so this is an L1 hit; kept out of It for registers)
+                const uint32_t tr = (uint32_t)items[idx(i)].pad0;
+                const uint4 *src = ix.vtile + (size_t)(tr >> 8) * 128;   // 2 KB = 128 uint4
+                const size_t kstride = (size_t)(tr & 0xffu) * 128;       // 16 rows x 128 B
+                for (int kb = 0; kb < nkb; kb++)
+                    tc::bulk_g2s(B + (uint32_t)kb * bytes, src + kb * kstride, bytes, &full[st]);
+            }
+        } else {
+            const int total = N * c16;
+            for (int f = tid; f < total; f += kM3Threads) {
+                const int r = f >> lc, c = f & (c16 - 1);
+                tc::cp_async16(B + (uint32_t)(c >> 3) * (uint32_t)N * 128u + tc::sw128_offset(r, c & 7),
+                               ix.vcent + (size_t)(t.pos + r) * c16 + c, r < t.size() ? 16u : 0u);
+            }
         }
         tc::cp_async_mbar_arrive(&full[st]);
     };
@@ -3414,6 +3458,8 @@ struct gts_index {
     DBuf<uint4> ehist;
     DBuf<uint4> esig;        // strings: q-gram signatures (qgram_sig), [2 * slots]
     DBuf<uint4> vcent;   // bf16 x 8 per uint4
+    DBuf<uint4> vtile;   // vcent per leaf in the MMA's SW128 smem image (k_vtile), or empty
+    DBuf<int32_t> vt_off, vt_rows;   // per leaf: image offset (128-byte units), rows (capacity rounded to 16)
     DBuf<float> vnorm32;   // angular: |o| per entry
     DBuf<double> vnorm64;
     DBuf<float> vse;     // c . vcent_e per entry
@@ -3489,6 +3535,37 @@ struct gts_result {
 
 namespace {
 
+// Leaf images of vcent for the tensor-core screen's bulk copies (k_vtile).
+// GTS_NO_VTILE=1 keeps the per-thread cp.async path.
+void build_vtile(gts_index *ix, cudaStream_t st)
+{
+    ix->vtile.release();
+    if (!ix->vcent.p || ix->leaf_count == 0 || std::getenv("GTS_NO_VTILE")) return;
+    const int64_t nl = ix->leaf_count;
+    const int c16 = ix->Dk / 8, nkb = ix->Dk / 64;
+    std::vector<int32_t> off((size_t)nl), rows((size_t)nl);
+    int64_t tot = 0;
+    for (int64_t l = 0; l < nl; l++) {
+        // items carry (offset / 2 KB) in 24 bits and rows / 16 in 8 bits
+        rows[(size_t)l] = (int32_t)std::max<int64_t>(16, (ix->leaf_cap[(size_t)l] + 15) & ~15ll);
+        off[(size_t)l] = (int32_t)tot;
+        tot += (int64_t)nkb * rows[(size_t)l];
+        if (tot >= (1ll << 28) || rows[(size_t)l] > 255 * 16) return;   // past 32 GB of images: keep cp.async
+    }
+    ix->vtile.alloc((size_t)tot * 8, st);
+    ix->vt_off.alloc((size_t)nl, st);
+    h2d(ix->vt_off.p, off.data(), off.size(), st);
+    ix->vt_rows.alloc((size_t)nl, st);
+    h2d(ix->vt_rows.p, rows.data(), rows.size(), st);
+    DBuf<int64_t> dpos((size_t)nl, st), cap((size_t)nl, st);
+    h2d(dpos.p, ix->leaf_dpos.data(), (size_t)nl, st);
+    h2d(cap.p, ix->leaf_cap.data(), (size_t)nl, st);
+    k_vtile<<<(unsigned)std::min<int64_t>(nl, 1 << 20), 256, 0, st>>>(ix->vcent.p, c16, dpos.p, cap.p, ix->vt_off.p,
+                                                                     ix->vt_rows.p, (int)nl, ix->vtile.p);
+    LAUNCH_CHECK();
+    CK(cudaStreamSynchronize(st));
+}
+
 IndexView make_view(const gts_index *ix, const gts_queries *q)
 {
     IndexView v{};
@@ -3507,6 +3584,7 @@ IndexView make_view(const gts_index *ix, const gts_queries *q)
     v.esig = ix->esig.p;
     v.sig_q = ix->esig.p ? qgram_q(ix->A) : 0;
     v.vcent = ix->vcent.p;
+    v.vtile = ix->vtile.p;
     v.vnorm32 = ix->vnorm32.p;
     v.vnorm64 = ix->vnorm64.p;
     v.vse = ix->vse.p;
@@ -3763,7 +3841,7 @@ struct Search {
         if (G.nitems == 0) return;
         G.items.alloc((size_t)G.nitems, st);
         k_make_items<<<grid_for(nleaf, 256), 256, 0, st>>>(cnt.p, off.p, ioff.p, nleaf, first, per, ix->node.p,
-                                                           ix->npos.p, G.items.p);
+                                                           ix->npos.p, G.items.p, ix->vt_off.p, ix->vt_rows.p);
         LAUNCH_CHECK();
     }
 
@@ -5395,6 +5473,7 @@ extern "C" int gts_index_create(const gts_dataset *ds, const gts_tree *t, int de
                 ix->vse.alloc((size_t)ns, st);
                 h2d(ix->vse.p, se.data(), (size_t)ns, st);
                 CK(cudaStreamSynchronize(st));
+                build_vtile(ix, st);
             }
             if (ds->metric == GTS_ANGULAR) {
                 std::vector<double> nrm((size_t)ns, 0.0), tmp;

@@ -51,6 +51,7 @@ struct IndexView {
     const uint4 *esig;       // [2n] 256-bit q-gram signature per entry (qgram_sig), or null
     int sig_q;               // q of the signature (4 for alphabets <= 4, else 2); 0: none
     const uint4 *vcent;      // [n][Dk/8] bf16 vectors centred on their leaf pivot (tensor-core L2 path), or null
+    const uint4 *vtile;      // the same per leaf, in the MMA's shared-memory image (k_vtile), or null
     const float *vnorm32;    // angular: |o| per entry (fp32 screen), or null
     const double *vnorm64;   // angular: |o| per entry, numpy's pairwise sum of squares
     const float *vse;        // [n] c . vcent_e (pivot . centred bf16 entry), tensor-core path

@@ -172,5 +172,21 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *mbar)
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+// Bulk (TMA-engine) copies: one thread posts the stage's byte count on the
+// mbarrier (an arrival) and issues cp.async.bulk copies that complete it.
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *mbar, uint32_t bytes)
+{
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(smem_u32(mbar)),
+                 "r"(bytes)
+                 : "memory");
+}
+// global -> shared, `bytes` a multiple of 16, both addresses 16-byte aligned
+__device__ __forceinline__ void bulk_g2s(uint32_t saddr, const void *g, uint32_t bytes, uint64_t *mbar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(saddr),
+                 "l"(g), "r"(bytes), "r"(smem_u32(mbar))
+                 : "memory");
+}
+
 }  // namespace tc
 }  // namespace gts

@@ -412,6 +412,7 @@ extern "C" int gts_index_insert(gts_index *ix, const gts_dataset *items, int32_t
         k_insert_vcent<<<(unsigned)m, 128, 0, st>>>((int)m, dsl.p, dpv.p, ix->vec32.p, ix->D, ix->Dp, ix->Dk,
                                                     reinterpret_cast<__nv_bfloat16 *>(ix->vcent.p), ix->vse.p);
         LAUNCH_CHECK();
+        build_vtile(ix, st);   // the leaf images follow vcent
     }
     if (edit) {
         DBuf<uint32_t> dw;
