@@ -706,25 +706,78 @@ __global__ void k_leaf_scatter(const Row *rows, int64_t m, int leaf_first, int *
     if (key >= 0) out[base + __popc(peers & ((1u << lane) - 1u))] = r;
 }
 
+// The same counting sort with block-private shared-memory counters (indexes
+// of <= kPrivLeaves leaves): a block counts a contiguous slice of rows with
+// shared atomics, then claims its per-leaf bases with one global atomic per
+// non-empty leaf (bbase[block][leaf]); the scatter re-walks the same slice
+// and places rows through shared cursors.  Two global atomics per (block,
+// leaf) instead of one per row on a few thousand hot counters.
+constexpr int kPrivLeaves = 40 * 1024;   // 160 KB of counters
+constexpr int kPrivThreads = 1024;
+
+__global__ void __launch_bounds__(kPrivThreads) k_leaf_hist_priv(const Row *__restrict__ rows, int64_t m,
+                                                                 int leaf_first, int nleaf, int *cnt, int *bbase)
+{
+    extern __shared__ int hcount[];
+    for (int l = threadIdx.x; l < nleaf; l += blockDim.x) hcount[l] = 0;
+    __syncthreads();
+    const int64_t per = (m + gridDim.x - 1) / gridDim.x;
+    const int64_t a = (int64_t)blockIdx.x * per, b = min(m, a + per);
+    for (int64_t i = a + threadIdx.x; i < b; i += blockDim.x) {
+        const int key = rows[i].node - leaf_first;
+        if ((unsigned)key < (unsigned)nleaf) atomicAdd(&hcount[key], 1);
+    }
+    __syncthreads();
+    int *bb = bbase + (size_t)blockIdx.x * nleaf;
+    for (int l = threadIdx.x; l < nleaf; l += blockDim.x) {
+        const int c = hcount[l];
+        bb[l] = c ? atomicAdd(cnt + l, c) : 0;
+    }
+}
+
+__global__ void __launch_bounds__(kPrivThreads) k_leaf_scatter_priv(const Row *__restrict__ rows, int64_t m,
+                                                                    int leaf_first, int nleaf,
+                                                                    const int *__restrict__ off,
+                                                                    const int *__restrict__ bbase, Row *out)
+{
+    extern __shared__ int hcur[];
+    const int *bb = bbase + (size_t)blockIdx.x * nleaf;
+    for (int l = threadIdx.x; l < nleaf; l += blockDim.x) hcur[l] = off[l] + bb[l];
+    __syncthreads();
+    const int64_t per = (m + gridDim.x - 1) / gridDim.x;
+    const int64_t a = (int64_t)blockIdx.x * per, b = min(m, a + per);
+    for (int64_t i = a + threadIdx.x; i < b; i += blockDim.x) {
+        const Row r = rows[i];
+        const int key = r.node - leaf_first;
+        if ((unsigned)key < (unsigned)nleaf) out[atomicAdd(&hcur[key], 1)] = r;
+    }
+}
+
 __global__ void k_item_counts(const int *cnt, int nleaf, int per, int *nitem)
 {
     int l = blockIdx.x * blockDim.x + threadIdx.x;
     if (l < nleaf) nitem[l] = (cnt[l] + per - 1) / per;
 }
 
-__global__ void k_make_items(const int *cnt, const int *off, const int *item_off, int nleaf, int leaf_first, int per,
-                             const NodeRec *node, const int32_t *npos, Item *items, const int32_t *vt_off,
-                             const int32_t *vt_rows)
+// one thread per item: its leaf is the last l with item_off[l] <= item
+// (leaves without rows have item_off[l] == item_off[l + 1])
+__global__ void k_make_items(const int *cnt, const int *off, const int *item_off, int nleaf, int nitems,
+                             int leaf_first, int per, const NodeRec *node, const int32_t *npos, Item *items,
+                             const int32_t *vt_off, const int32_t *vt_rows)
 {
-    int l = blockIdx.x * blockDim.x + threadIdx.x;
-    if (l >= nleaf) return;
-    const int c = cnt[l];
-    const int nd = leaf_first + l;
-    const int size = c ? node[nd].size : 0, pos = c ? npos[nd] : 0;
+    const int it = blockIdx.x * blockDim.x + threadIdx.x;
+    if (it >= nitems) return;
+    int lo = 0, hi = nleaf;   // upper_bound(it) over item_off[0..nleaf) - 1
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (item_off[mid] <= it) lo = mid + 1; else hi = mid;
+    }
+    const int l = lo - 1;
+    const int c = cnt[l], nd = leaf_first + l;
+    const int s = (it - item_off[l]) * per;
     // pad0: the leaf's image in vtile, (offset / 2 KB) << 8 | rows / 16
-    const int tr = c && vt_off ? (int)(((uint32_t)(vt_off[l] >> 4) << 8) | (uint32_t)(vt_rows[l] >> 4)) : 0;
-    for (int j = 0, s = 0; s < c; j++, s += per)
-        items[item_off[l] + j] = Item{nd, off[l] + s, min(per, c - s), size, pos, tr, 0, 0};
+    const int tr = vt_off ? (int)(((uint32_t)(vt_off[l] >> 4) << 8) | (uint32_t)(vt_rows[l] >> 4)) : 0;
+    items[it] = Item{nd, off[l] + s, min(per, c - s), node[nd].size, npos[nd], tr, 0, 0};
 }
 
 // ---------------------------------------------------------------------------
@@ -3820,14 +3873,35 @@ struct Search {
         DBuf<int> nit((size_t)nleaf + 1, st), ioff((size_t)nleaf + 1, st);
         G.srows.alloc((size_t)m, st);
         CK(cudaMemsetAsync(cnt.p, 0, sizeof(int) * (nleaf + 1), st));
-        k_leaf_hist<<<grid_for(m, 256), 256, 0, st>>>(rows, m, first, cnt.p);
+        // block-private counters when the leaves fit in shared memory
+        // (GTS_GROUP_ATOMIC=1: the per-row global-atomic kernels)
+        static const bool atomic_only = std::getenv("GTS_GROUP_ATOMIC") != nullptr;
+        const bool priv = !atomic_only && nleaf <= kPrivLeaves && m >= (int64_t)kPrivThreads * 64;
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
+        const unsigned pgrid = 2u * (unsigned)sms;
+        DBuf<int> bbase;
+        if (priv) {
+            const size_t sb = (size_t)nleaf * sizeof(int);
+            smem_optin((const void *)k_leaf_hist_priv, sb);
+            smem_optin((const void *)k_leaf_scatter_priv, sb);
+            bbase.alloc((size_t)pgrid * nleaf, st);
+            k_leaf_hist_priv<<<pgrid, kPrivThreads, sb, st>>>(rows, m, first, nleaf, cnt.p, bbase.p);
+        } else {
+            k_leaf_hist<<<grid_for(m, 256), 256, 0, st>>>(rows, m, first, cnt.p);
+        }
         LAUNCH_CHECK();
         size_t tb = 0;
         cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.p, off.p, nleaf + 1, st);
         DBuf<uint8_t> tmp(tb, st);
         CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, cnt.p, off.p, nleaf + 1, st));
-        CK(cudaMemcpyAsync(cur.p, off.p, sizeof(int) * (nleaf + 1), cudaMemcpyDeviceToDevice, st));
-        k_leaf_scatter<<<grid_for(m, 256), 256, 0, st>>>(rows, m, first, cur.p, G.srows.p);
+        if (priv) {
+            k_leaf_scatter_priv<<<pgrid, kPrivThreads, (size_t)nleaf * sizeof(int), st>>>(rows, m, first, nleaf, off.p,
+                                                                                         bbase.p, G.srows.p);
+        } else {
+            CK(cudaMemcpyAsync(cur.p, off.p, sizeof(int) * (nleaf + 1), cudaMemcpyDeviceToDevice, st));
+            k_leaf_scatter<<<grid_for(m, 256), 256, 0, st>>>(rows, m, first, cur.p, G.srows.p);
+        }
         LAUNCH_CHECK();
         k_item_counts<<<grid_for(nleaf, 256), 256, 0, st>>>(cnt.p, nleaf, per, nit.p);
         LAUNCH_CHECK();
@@ -3840,8 +3914,9 @@ struct Search {
         G.nitems = *h_nitems;
         if (G.nitems == 0) return;
         G.items.alloc((size_t)G.nitems, st);
-        k_make_items<<<grid_for(nleaf, 256), 256, 0, st>>>(cnt.p, off.p, ioff.p, nleaf, first, per, ix->node.p,
-                                                           ix->npos.p, G.items.p, ix->vt_off.p, ix->vt_rows.p);
+        k_make_items<<<grid_for(G.nitems, 256), 256, 0, st>>>(cnt.p, off.p, ioff.p, nleaf, G.nitems, first, per,
+                                                              ix->node.p, ix->npos.p, G.items.p, ix->vt_off.p,
+                                                              ix->vt_rows.p);
         LAUNCH_CHECK();
     }
 
