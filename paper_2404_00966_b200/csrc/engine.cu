@@ -4414,7 +4414,9 @@ struct Search {
     template <int MET>
     void launch_probe_grouped()
     {
-        const int64_t qchunk = std::min<int64_t>(nq, 1 << 17);   // <= 4 GiB of candidate distances
+        // 2^15 queries per pass: <= 1 GiB of candidate distances (kProbeCand
+        // floats per query) whatever the batch size
+        const int64_t qchunk = std::min<int64_t>(nq, 1 << 15);
         const size_t pd_smem = (size_t)2 * kPT * (kPD + 4) * sizeof(float);
         smem_optin((const void *)k_probe_dist<kMetricL1>, pd_smem);
         smem_optin((const void *)k_probe_dist<kMetricL2>, pd_smem);
