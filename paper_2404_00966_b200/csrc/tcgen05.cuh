@@ -78,6 +78,11 @@ __device__ __forceinline__ void mbar_init(uint64_t *mbar, uint32_t count)
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mbar)), "r"(count));
 }
 
+// try_wait's suspend-time hint: a waiting thread may sleep until the phase
+// completes (or the hint expires) instead of re-issuing the probe, leaving
+// the issue slots to the warps that have work
+constexpr uint32_t kMbarSuspendHint = 0x989680u;
+
 __device__ __forceinline__ void mbar_wait(uint64_t *mbar, uint32_t phase)
 {
     uint32_t done = 0;
@@ -85,10 +90,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t *mbar, uint32_t phase)
     while (!done) {
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
             "selp.u32 %0, 1, 0, p;\n\t}"
             : "=r"(done)
-            : "r"(a), "r"(phase)
+            : "r"(a), "r"(phase), "r"(kMbarSuspendHint)
             : "memory");
     }
 }
