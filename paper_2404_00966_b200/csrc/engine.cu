@@ -358,7 +358,9 @@ constexpr int kWarpPeqWords = 1024;     // per-warp staged match masks (A*W <= 1
 // memory.  Leaves are length-sorted, so a batch has similar DP lengths.
 constexpr int kHistBins = 256;   // kNN shrinking-bound histogram: exact distances 0..255
 
-template <bool SIG>
+// SIG: q-gram signatures; PRUNE: lemma-1 test (pruning on); EHIST: symbol
+// histograms (compile-time, so the entry loop carries no runtime flags)
+template <bool SIG, bool PRUNE, bool EHIST>
 __global__ void __launch_bounds__(256, 4) k_leaf_edit(IndexView ix, QueryView qv, const Row *__restrict__ rows,
                                                       int64_t m, int pruning, float *r32,
                                                       HitBuf out, unsigned long long *verified_stat, int stats_on,
@@ -506,7 +508,7 @@ __global__ void __launch_bounds__(256, 4) k_leaf_edit(IndexView ix, QueryView qv
             cur_q = lr.q;
             mq = qlen(qv, cur_q);
             r = __ldcg(r32 + cur_q);
-            if (ix.ehist) { qh0 = qv.qhist[2 * cur_q]; qh1 = qv.qhist[2 * cur_q + 1]; }
+            if (EHIST) { qh0 = qv.qhist[2 * cur_q]; qh1 = qv.qhist[2 * cur_q + 1]; }
             if (SIG) {
                 uint4 sg = make_uint4(0u, 0u, 0u, 0u);
                 if (lane < 2) qsig_s[wib][lane] = sg = qv.qsig[2 * cur_q + lane];
@@ -545,13 +547,13 @@ __global__ void __launch_bounds__(256, 4) k_leaf_edit(IndexView ix, QueryView qv
             if (b + kWarp + lane < leaf.size) nrec = __ldg(ix.erec + e + kWarp);
             const float dis = __uint_as_float(rec.x), lenf = __uint_as_float(rec.w);
             bool pass = false;
-            if (k < leaf.size) pass = pruning ? fabsf(dis - lr.dqp) <= r : dis == dis;
+            if (k < leaf.size) pass = PRUNE ? fabsf(dis - lr.dqp) <= r : dis == dis;
             ver += __popc(__ballot_sync(kFull, pass));
             bool cand = pass && fabsf(mqf - lenf) <= r;
             // the histogram bound never exceeds max(|q|, |o|): skip it when that
             // fits.  (Issuing these loads before the lemma-1 work, for every
             // length-passing entry, measured slower: 86.8 vs 84 ms on words.)
-            if (cand && ix.ehist && fmaxf(mqf, lenf) > r) {
+            if (EHIST && cand && fmaxf(mqf, lenf) > r) {
                 const uint4 h0 = __ldg(ix.ehist + 2 * e), h1 = __ldg(ix.ehist + 2 * e + 1);
                 cand = hist_lb(qh0, qh1, h0, h1, mq - (int)rec.y) <= ri;
             }
@@ -4269,7 +4271,13 @@ struct Search {
             // static 38.9 KB + up to 17 KB of staged texts
             // the q-gram signature test is compiled in only where the index has
             // signatures (small alphabets), so the words kernel stays as it was
-            auto *kern = ix->esig.p ? k_leaf_edit<true> : k_leaf_edit<false>;
+            using KernT = decltype(&k_leaf_edit<false, true, true>);
+            static const KernT kerns[2][2][2] = {
+                {{k_leaf_edit<false, false, false>, k_leaf_edit<false, false, true>},
+                 {k_leaf_edit<false, true, false>, k_leaf_edit<false, true, true>}},
+                {{k_leaf_edit<true, false, false>, k_leaf_edit<true, false, true>},
+                 {k_leaf_edit<true, true, false>, k_leaf_edit<true, true, true>}}};
+            auto *kern = kerns[ix->esig.p ? 1 : 0][pruning ? 1 : 0][ix->ehist.p ? 1 : 0];
             smem_optin((const void *)kern, 64 * 1024);
             CK(cudaMemsetAsync(counter.p, 0, sizeof(unsigned long long), st));
             timed("k_leaf_edit", [&] {
