@@ -3879,6 +3879,8 @@ struct Search {
         // (GTS_GROUP_ATOMIC=1: the per-row global-atomic kernels)
         static const bool atomic_only = std::getenv("GTS_GROUP_ATOMIC") != nullptr;
         const bool priv = !atomic_only && nleaf <= kPrivLeaves && m >= (int64_t)kPrivThreads * 64;
+        static const bool trace = std::getenv("GTS_TRACE") != nullptr;
+        if (trace) fprintf(stderr, "[gts] group_rows m=%lld nodes=%d private=%d\n", (long long)m, nleaf, (int)priv);
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
         const unsigned pgrid = 2u * (unsigned)sms;
