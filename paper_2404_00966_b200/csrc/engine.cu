@@ -3841,6 +3841,10 @@ struct Search {
         // use the largest hits-per-query ratio this process has seen, +25%
         hcap = std::max<size_t>(hcap, (size_t)std::min(g_hits_per_query[mode].load() * (double)nq * 1.25,
                                                        (double)(1ll << 27)));
+        // test hooks: GTS_HIT_CAP0 = initial hit-buffer rows (no hints), so the
+        // grow-and-re-run path runs; GTS_COMPACT_AT = kNN hit compaction threshold
+        if (const char *e = std::getenv("GTS_HIT_CAP0")) hcap = (size_t)std::max(1ll, std::atoll(e));
+        if (const char *e = std::getenv("GTS_COMPACT_AT")) compact_at = (unsigned long long)std::max(1ll, std::atoll(e));
         hq.alloc(hcap, st);
         he.alloc(hcap, st);
         hd.alloc(hcap, st);
@@ -4062,6 +4066,8 @@ struct Search {
         // overflow costs a full re-run of the screening kernel
         const size_t hint = (size_t)ix->cand_hint.load();
         size_t cap = std::max<size_t>((size_t)1 << 22, hint + hint / 2);
+        // test hook: GTS_CAND_CAP0 = initial candidate-buffer rows (no hint)
+        if (const char *e = std::getenv("GTS_CAND_CAP0")) cap = (size_t)std::max(1ll, std::atoll(e));
         DBuf<unsigned long long> cnt(1, st);
         for (int attempt = 0;; attempt++) {
             if (cq.n < cap) {
