@@ -77,3 +77,26 @@ def test_buffer_grow_and_rerun_paths(kind, monkeypatch):
         radii = rng.uniform(0.2, 1.0, 200) * scale
     tree = P.build(ds, P.TreeConfig(20, 1))
     check_against_oracle(ds, tree, q, od, oq, radii, rng.integers(1, 80, 200), threads=16)
+
+
+def test_l1_32d_2m_shard_batch_20k():
+    # the L1 shard shape (configs[4] per GPU: spread 0.01, range r = 0.5, kNN k = 100)
+    rng = np.random.default_rng(58)
+    mat = f32(P.generate_clustered(2_000_000, 32, 1000, seed=59, spread=0.01))
+    tree = P.build(P.Dataset.from_vectors(mat, P.L1), P.TreeConfig(20, 0))
+    q = f32(mat[rng.integers(0, 2_000_000, 20_000)] + rng.normal(0, 0.005, (20_000, 32)))
+    sample = rng.choice(20_000, 48, replace=False)
+    sample_matches(P.BatchSearcher(tree), list(q), np.full(20_000, 0.5), np.full(20_000, 100),
+                   O.Payloads(O.L1, vec=mat), lambda qs: O.Payloads(O.L1, vec=np.array(qs)), sample)
+
+
+def test_dna_108_1m_batch_2k():
+    # configs[3] shape (range r = 8, kNN k = 10); the brute-force check of a
+    # 108 x 108 DP per pair over 1M objects keeps the sample small
+    rng = np.random.default_rng(60)
+    strs = P.generate_sequences(1_000_000, seed=61, min_len=108, max_len=108, alphabet="ACGT")
+    tree = P.build(P.Dataset.from_strings(strs, P.EDIT), P.TreeConfig(20, 0))
+    q = string_queries(strs, 2_000, rng, "ACGT")
+    sample = rng.choice(2_000, 6, replace=False)
+    sample_matches(P.BatchSearcher(tree), q, np.full(2_000, 8.0), np.full(2_000, 10),
+                   O.Payloads.from_strings(strs), O.Payloads.from_strings, sample)
