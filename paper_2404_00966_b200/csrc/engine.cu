@@ -3336,6 +3336,50 @@ __global__ void k_gather_d(const double *d, const int32_t *perm, int64_t n, unsi
     key[i] = (unsigned long long)__double_as_longlong(d[perm[i]]);
 }
 
+// Float-distance collect in two sorts: key = float32(d) bits (monotonic in
+// d >= 0) << rbits | dataset row, then stable by query; k_fix_f32_ties then
+// puts each run of equal (query, float32(d)) -- whose float64 distances may
+// differ -- in (float64 d, row) order (insertion sort: runs are short, and
+// already sorted when their distances are equal).
+__global__ void k_pack_f32_keys(const int32_t *e, const double *d, int64_t n, const int32_t *row, int rbits,
+                                unsigned long long *key, int32_t *perm)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    key[i] = ((unsigned long long)__float_as_uint((float)d[i]) << rbits) | (unsigned long long)(uint32_t)row[e[i]];
+    perm[i] = (int32_t)i;
+}
+
+__global__ void k_fix_f32_ties(int32_t *perm, const int32_t *q, const int32_t *e, const double *d,
+                               const int32_t *row, int64_t n)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    auto tie_key = [&](int64_t k) {
+        const int32_t p = perm[k];
+        return ((unsigned long long)(uint32_t)q[p] << 32) | __float_as_uint((float)d[p]);
+    };
+    const unsigned long long t = tie_key(i);
+    if (i > 0 && tie_key(i - 1) == t) return;   // not the head of its run
+    int64_t j = i + 1;
+    while (j < n && tie_key(j) == t) j++;
+    if (j - i < 2) return;
+    for (int64_t a = i + 1; a < j; a++) {
+        const int32_t pa = perm[a];
+        const double da = d[pa];
+        const int32_t ra = row[e[pa]];
+        int64_t b = a - 1;
+        while (b >= i) {
+            const int32_t pb = perm[b];
+            const double db = d[pb];
+            if (db < da || (db == da && row[e[pb]] <= ra)) break;
+            perm[b + 1] = pb;
+            b--;
+        }
+        perm[b + 1] = pa;
+    }
+}
+
 __global__ void k_gather_q(const int32_t *q, const int32_t *perm, int64_t n, uint32_t *key)
 {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -4618,6 +4662,32 @@ struct Search {
                                                qbits + dbits + rbits, st));
             g_launches += 4;
             k_seg_counts<<<grid_for(nq, 256), 256, 0, st>>>(kb.p, n, rbits + dbits, (int)nq, counts.p);
+            LAUNCH_CHECK();
+        } else if (n > 0 && !by_id && 32 + rbits <= 64 && std::getenv("GTS_COLLECT_3SORT") == nullptr) {
+            // float distances: (float32(d), row) sort, stable query sort, tie fix-up
+            DBuf<unsigned long long> ka((size_t)n, st), kb((size_t)n, st);
+            perm_a.alloc((size_t)n, st);
+            perm_b.alloc((size_t)n, st);
+            const unsigned g = grid_for(n, 256);
+            k_pack_f32_keys<<<g, 256, 0, st>>>(he.p, hd.p, n, ix->row.p, rbits, ka.p, perm_a.p);
+            LAUNCH_CHECK();
+            size_t tmp_bytes = 0, t2 = 0;
+            cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, ka.p, kb.p, perm_a.p, perm_b.p, (int)n, 0, 32 + rbits, st);
+            cub::DeviceRadixSort::SortPairs(nullptr, t2, (uint32_t *)nullptr, (uint32_t *)nullptr, perm_a.p,
+                                            perm_b.p, (int)n, 0, 32, st);
+            tmp_bytes = std::max(tmp_bytes, t2);
+            DBuf<uint8_t> tmp(tmp_bytes, st);
+            CK(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, ka.p, kb.p, perm_a.p, perm_b.p, (int)n, 0, 32 + rbits,
+                                               st));
+            DBuf<uint32_t> qa((size_t)n, st), qb((size_t)n, st);
+            k_gather_q<<<g, 256, 0, st>>>(hq.p, perm_b.p, n, qa.p);
+            LAUNCH_CHECK();
+            CK(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, qa.p, qb.p, perm_b.p, perm_a.p, (int)n, 0, qbits, st));
+            k_fix_f32_ties<<<g, 256, 0, st>>>(perm_a.p, hq.p, he.p, hd.p, ix->row.p, n);
+            LAUNCH_CHECK();
+            std::swap(perm_a, perm_b);   // k_emit reads perm_b
+            g_launches += 8;
+            k_count<<<g, 256, 0, st>>>(hq.p, n, counts.p);
             LAUNCH_CHECK();
         } else if (n > 0) {
             DBuf<unsigned long long> ka((size_t)n, st), kb((size_t)n, st);

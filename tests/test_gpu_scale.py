@@ -100,3 +100,18 @@ def test_dna_108_1m_batch_2k():
     sample = rng.choice(2_000, 6, replace=False)
     sample_matches(P.BatchSearcher(tree), q, np.full(2_000, 8.0), np.full(2_000, 10),
                    O.Payloads.from_strings(strs), O.Payloads.from_strings, sample)
+
+
+def test_float_collect_orders_ties_below_float32():
+    # distances equal in float32 but not in float64, larger for smaller rows:
+    # the (float32, row) sort puts them in row order and the tie fix-up
+    # (k_fix_f32_ties) must restore (float64 distance, id) order
+    N = 3000
+    mat = np.zeros((N, 2))
+    mat[:, 0] = 1.0 + (N - np.arange(N)) * 2.0 ** -40
+    mat = np.concatenate([mat, np.random.default_rng(62).uniform(3, 4, (5000, 2))])
+    ds = P.Dataset.from_vectors(mat, P.L2)
+    tree = P.build(ds, P.TreeConfig(8, 0))
+    q = [np.zeros(2), np.array([0.0, 1e-9])]
+    check_against_oracle(ds, tree, q, O.Payloads(O.L2, vec=mat), O.Payloads(O.L2, vec=np.array(q)),
+                         np.array([2.0, 1.5]), np.array([N // 2, 7]), threads=8)
