@@ -4129,6 +4129,8 @@ struct Search {
                 unsigned long long c0 = ix->cand_hint.load();
                 while (nc > c0 && !ix->cand_hint.compare_exchange_weak(c0, nc)) {}
             }
+            static const bool trace = std::getenv("GTS_TRACE") != nullptr;
+            if (trace) fprintf(stderr, "[gts] screen candidates=%llu cap=%zu\n", nc, (size_t)cq.n);
             if (nc > cq.n) { cap = (size_t)nc + nc / 2; reruns++; continue; }
             if (nc) {
                 HitBuf hb{hq.p, he.p, hd.p, (unsigned long long)hq.n, counter.p + 1};
