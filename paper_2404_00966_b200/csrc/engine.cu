@@ -2642,7 +2642,7 @@ k_leafgroup_mma3(IndexView ix, QueryView qv, const Row *__restrict__ srows, cons
 // (metrics.py:127-133); larger D runs pw_sum64 on the group's first lane.
 template <int MET>
 __global__ void k_recheck(IndexView ix, QueryView qv, CandBuf cb, unsigned long long ncand, const float *r32,
-                          const double *r64, HitBuf out)
+                          const double *r64, HitBuf out, int prescreen)
 {
     const int lane = lane_id(), j = lane & 7;
     const unsigned long long i = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
@@ -2660,6 +2660,31 @@ __global__ void k_recheck(IndexView ix, QueryView qv, CandBuf cb, unsigned long 
     if (D > 128) {
         if (live && j == 0) d64 = vdist64<MET>(ix, qv, q, e);
     } else if (__any_sync(kFull, live)) {
+        // fp32 pre-screen, the CUDA-core kernels' test (d32 - slack <= r), for
+        // candidates of the tensor-core path: most of them are farther than r
+        // (its bf16 band is wide), and this drops them before the float64
+        // distance and its 8-byte query loads (vec128: 412.2 -> 407.8 ms per
+        // step; the CUDA-core kernels' candidates already passed this test).
+        // The 8 lanes of a group share a candidate.
+        if ((MET == kMetricL1 || MET == kMetricL2) && prescreen) {
+            float acc32 = 0.f;
+            if (live) {
+                const float *of = ix.vec32 + (size_t)e * ix.Dp;
+                const float *qf = qv.vec32 + (size_t)q * ix.Dp;
+                for (int t = j; t < D; t += 8) {
+                    const float df = of[t] - qf[t];
+                    acc32 = MET == kMetricL1 ? acc32 + fabsf(df) : fmaf(df, df, acc32);
+                }
+            }
+            acc32 += __shfl_xor_sync(kFull, acc32, 1);
+            acc32 += __shfl_xor_sync(kFull, acc32, 2);
+            acc32 += __shfl_xor_sync(kFull, acc32, 4);
+            if (live) {
+                const float d32 = MET == kMetricL1 ? acc32 : sqrtf(acc32);
+                live = d32 - slack(ix, d32, 0.f) <= __ldcg(r32 + q) * (1.f + 1e-6f);
+            }
+            if (!__any_sync(kFull, live)) return;
+        }
         const float *o32 = ix.vec64 ? nullptr : ix.vec32 + (size_t)e * ix.Dp;
         const double *o64 = ix.vec64 ? ix.vec64 + (size_t)e * D : nullptr;
         const double *qq = qv.vec64 + (size_t)q * D;
@@ -4069,7 +4094,7 @@ struct Search {
                                                                on ? fhist.p : nullptr, r0.p, ks.p);
             });
             LAUNCH_CHECK();
-        });
+        }, true);
     }
 
     template <int NT, int NSTAGE>
@@ -4096,14 +4121,16 @@ struct Search {
                                                                   nmax, on ? fhist.p : nullptr, r0.p, ks.p);
             });
             LAUNCH_CHECK();
-        });
+        }, true);
     }
 
     // Run a screening kernel that appends (query, entry, lower bound) candidates,
     // growing the buffer and re-running (stats off: counts and histograms must
     // not double) on overflow, then recheck them exactly (k_recheck<MET>).
     template <int MET, class Launch>
-    void with_candidates(Launch &&launch)
+    // prescreen: the candidates come from the tensor-core screen (wide bf16
+    // band), so k_recheck tests them in fp32 before the float64 distance
+    void with_candidates(Launch &&launch, bool prescreen = false)
     {
         // the hint is the largest count seen; 50% headroom, since kNN counts vary
         // from call to call (the shrinking radius is order-dependent) and an
@@ -4135,7 +4162,8 @@ struct Search {
             if (nc) {
                 HitBuf hb{hq.p, he.p, hd.p, (unsigned long long)hq.n, counter.p + 1};
                 timed("k_recheck", [&] {
-                    k_recheck<MET><<<grid_for((int64_t)nc * 8, 256), 256, 0, st>>>(iv, qv, cb, nc, r32.p, r64.p, hb);
+                    k_recheck<MET><<<grid_for((int64_t)nc * 8, 256), 256, 0, st>>>(iv, qv, cb, nc, r32.p, r64.p, hb,
+                                                                                   prescreen ? 1 : 0);
                 });
                 LAUNCH_CHECK();
             }
